@@ -1,0 +1,663 @@
+/*
+ * legend_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C, single-threaded CPU restatement of the reference trainer's hot
+ * path (arXiv 2505.09258 "Legend" reference, /root/reference/proj).  It is the
+ * checker the CUDA path is compared against: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline leg may load it.  The product path never links or
+ * calls anything in this directory.
+ *
+ * Parity pinning: tests/test_oracle_pin.py compares every function here with
+ * the reference library itself (oracle/_ref/liblegend_ref.so, built from the
+ * unmodified reference sources by oracle/Makefile) and with the committed
+ * golden vectors in tests/golden/ (generated from that library by
+ * tests/golden/gen_golden.py).  The arithmetic below reproduces the
+ * reference's FP64 operation order, so results are bit-identical to it.
+ *
+ * Every function cites the reference file:line it restates.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define LO_OK 0
+#define LO_INVALID 1   /* std::invalid_argument */
+#define LO_LOGIC 2     /* std::logic_error */
+#define LO_RANGE 3     /* std::out_of_range */
+#define LO_NOMEM 4
+
+#define LO_NO_REL 0xffffffffu      /* graph.hpp:17 kNoRelation */
+#define LO_KIND_DOT 0              /* train.hpp:13 ScoreKind */
+#define LO_KIND_DISTMULT 1
+#define LO_KIND_COMPLEX 2
+
+/* ------------------------------------------------------------------ RNG --- */
+
+/* rng.hpp:7-12 */
+uint64_t lo_splitmix64(uint64_t* state) {
+  uint64_t z = (*state += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+typedef struct {
+  uint64_t s[4];
+} lo_rng;
+
+/* rng.hpp:18-21: four splitmix64 outputs fill the xoshiro state */
+void lo_rng_init(lo_rng* r, uint64_t seed) {
+  uint64_t s = seed;
+  for (int i = 0; i < 4; ++i) r->s[i] = lo_splitmix64(&s);
+}
+
+static inline uint64_t lo_rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+/* rng.hpp:23-33 xoshiro256** */
+uint64_t lo_rng_next(lo_rng* r) {
+  uint64_t* s = r->s;
+  const uint64_t result = lo_rotl(s[1] * 5, 7) * 9;
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = lo_rotl(s[3], 45);
+  return result;
+}
+
+/* rng.hpp:36 */
+double lo_rng_double(lo_rng* r) { return (double)(lo_rng_next(r) >> 11) * 0x1.0p-53; }
+
+/* rng.hpp:42-48: unbiased rejection sampling; rejected draws consume the stream */
+uint64_t lo_rng_below(lo_rng* r, uint64_t bound) {
+  const uint64_t threshold = (0 - bound) % bound;
+  for (;;) {
+    const uint64_t x = lo_rng_next(r);
+    if (x >= threshold) return x % bound;
+  }
+}
+
+/* rng.hpp:57-67 */
+uint64_t lo_derive_seed(uint64_t base, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t s = base;
+  lo_splitmix64(&s);
+  s ^= 0x516cc24f80775842ull + a;
+  lo_splitmix64(&s);
+  s ^= 0x2545f4914f6cdd1dull * (b + 1);
+  lo_splitmix64(&s);
+  s ^= 0x9e6c63d0876a9a47ull * (c + 1);
+  return lo_splitmix64(&s);
+}
+
+/* ctypes helpers: raw stream, and next_below over a list of bounds */
+void lo_rng_state(uint64_t seed, uint64_t out[4]) {
+  lo_rng r;
+  lo_rng_init(&r, seed);
+  memcpy(out, r.s, sizeof r.s);
+}
+
+void lo_rng_u64(uint64_t seed, uint64_t skip, uint64_t n, uint64_t* out) {
+  lo_rng r;
+  lo_rng_init(&r, seed);
+  for (uint64_t i = 0; i < skip; ++i) lo_rng_next(&r);
+  for (uint64_t i = 0; i < n; ++i) out[i] = lo_rng_next(&r);
+}
+
+/* consumed = number of raw u64 draws used (n + rejections) */
+void lo_rng_below_seq(uint64_t seed, uint64_t skip, const uint64_t* bounds, uint64_t n,
+                      uint64_t* out, uint64_t* consumed) {
+  lo_rng r;
+  lo_rng_init(&r, seed);
+  for (uint64_t i = 0; i < skip; ++i) lo_rng_next(&r);
+  uint64_t used = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t bound = bounds[i];
+    const uint64_t threshold = (0 - bound) % bound;
+    for (;;) {
+      const uint64_t x = lo_rng_next(&r);
+      ++used;
+      if (x >= threshold) {
+        out[i] = x % bound;
+        break;
+      }
+    }
+  }
+  if (consumed) *consumed = used;
+}
+
+/* ------------------------------------------------------- partitions --- */
+
+/* graph.cpp:120-150: stride = ceil(V/n); stable counting sort of edge indices
+ * by bucket (src_part * n + dst_part). */
+int lo_partition_plan(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes, uint32_t n,
+                      uint64_t* stride_out, uint64_t* offsets, uint64_t* edge_order) {
+  if (n < 1) return LO_INVALID;
+  if (n > num_nodes) return LO_INVALID;
+  if (num_edges == 0) return LO_INVALID;
+  const uint64_t stride = (num_nodes + n - 1) / n;
+  const uint64_t buckets = (uint64_t)n * n;
+  memset(offsets, 0, (buckets + 1) * sizeof(uint64_t));
+  for (uint64_t e = 0; e < num_edges; ++e) {
+    const uint64_t b = (edges[3 * e] / stride) * n + edges[3 * e + 2] / stride;
+    offsets[b + 1]++;
+  }
+  for (uint64_t b = 0; b < buckets; ++b) offsets[b + 1] += offsets[b];
+  uint64_t* cursor = (uint64_t*)malloc(buckets * sizeof(uint64_t));
+  if (!cursor) return LO_NOMEM;
+  memcpy(cursor, offsets, buckets * sizeof(uint64_t));
+  for (uint64_t e = 0; e < num_edges; ++e) {
+    const uint64_t b = (edges[3 * e] / stride) * n + edges[3 * e + 2] / stride;
+    edge_order[cursor[b]++] = e;
+  }
+  free(cursor);
+  *stride_out = stride;
+  return LO_OK;
+}
+
+/* --------------------------------------------------------- store init --- */
+
+/* store.cpp:19-25 fill_uniform_rows: f32(U[-b, b)) with b = 0.5/sqrt(dim),
+ * drawn in row-major order from Rng(stream_seed) (rng.hpp:36-39). */
+void lo_init_rows(uint64_t stream_seed, uint64_t rows, uint32_t dim, float* out) {
+  const double bound = 0.5 / sqrt((double)dim);
+  lo_rng r;
+  lo_rng_init(&r, stream_seed);
+  const uint64_t total = rows * dim;
+  const double lo = -bound, hi = bound;
+  for (uint64_t i = 0; i < total; ++i) out[i] = (float)(lo + (hi - lo) * lo_rng_double(&r));
+}
+
+/* store.cpp:59-86 EmbeddingStore::create: partition p seeded with
+ * derive_seed(seed, p), relations with derive_seed(seed, 0x52454c53);
+ * optimizer state zero.  E and S are whole-graph row-major arrays whose
+ * partition p occupies rows [stride*p, min(stride*(p+1), V)). */
+void lo_store_init(uint32_t n, uint64_t num_nodes, uint32_t dim, uint64_t num_relations,
+                   uint64_t seed, float* E, float* S, float* relE, float* relS) {
+  const uint64_t stride = (num_nodes + n - 1) / n;
+  for (uint32_t p = 0; p < n; ++p) {
+    const uint64_t begin = stride * p;
+    uint64_t end = stride * (p + 1);
+    if (end > num_nodes) end = num_nodes;
+    if (end <= begin) continue;
+    lo_init_rows(lo_derive_seed(seed, p, 0, 0), end - begin, dim, E + begin * dim);
+  }
+  if (S) memset(S, 0, num_nodes * dim * sizeof(float));
+  if (num_relations > 0) {
+    lo_init_rows(lo_derive_seed(seed, 0x52454c53ull, 0, 0), num_relations, dim, relE);
+    if (relS) memset(relS, 0, num_relations * dim * sizeof(float));
+  }
+}
+
+/* ---------------------------------------------------------- sampling --- */
+
+/* train.cpp:190-202 resident_node_count / resident_node_at over resident
+ * ranges sorted by first node; train.cpp:365-373 sample_negatives. */
+int lo_sample_negatives_rng(const uint64_t* first, const uint64_t* count, int nparts, uint32_t k,
+                            uint64_t num_positives, lo_rng* rng, uint32_t* out) {
+  if (k == 0) return LO_INVALID;
+  uint64_t total = 0;
+  for (int i = 0; i < nparts; ++i) total += count[i];
+  if (total == 0) return LO_INVALID;
+  const uint64_t draws = num_positives * k;
+  for (uint64_t q = 0; q < draws; ++q) {
+    uint64_t idx = lo_rng_below(rng, total);
+    int i = 0;
+    while (idx >= count[i]) {
+      idx -= count[i];
+      ++i;
+    }
+    out[q] = (uint32_t)(first[i] + idx);
+  }
+  return LO_OK;
+}
+
+int lo_sample_negatives(const uint64_t* first, const uint64_t* count, int nparts, uint32_t k,
+                        uint64_t num_positives, uint64_t seed, uint64_t skip, uint32_t* out) {
+  lo_rng r;
+  lo_rng_init(&r, seed);
+  for (uint64_t i = 0; i < skip; ++i) lo_rng_next(&r);
+  return lo_sample_negatives_rng(first, count, nparts, k, num_positives, &r, out);
+}
+
+/* --------------------------------------------------- score / grad math --- */
+
+/* train.cpp:39-60 combine_src_rel (IR1 = s (x) r) */
+static void combine(int kind, uint32_t d, const float* src, const float* rel, double* out) {
+  switch (kind) {
+    case LO_KIND_DOT:
+      for (uint32_t i = 0; i < d; ++i) out[i] = src[i];
+      break;
+    case LO_KIND_DISTMULT:
+      for (uint32_t i = 0; i < d; ++i) out[i] = (double)src[i] * rel[i];
+      break;
+    default: {
+      const uint32_t h = d / 2;
+      for (uint32_t i = 0; i < h; ++i) {
+        const double sr = src[i], si = src[i + h];
+        const double rr = rel[i], ri = rel[i + h];
+        out[i] = sr * rr - si * ri;
+        out[i + h] = sr * ri + si * rr;
+      }
+    }
+  }
+}
+
+/* train.cpp:65-85 adjoint_combine: out += adj_other(mix) */
+static void adjoint(int kind, uint32_t d, const float* other, const double* mix, double* out) {
+  switch (kind) {
+    case LO_KIND_DOT:
+      for (uint32_t i = 0; i < d; ++i) out[i] += mix[i];
+      break;
+    case LO_KIND_DISTMULT:
+      for (uint32_t i = 0; i < d; ++i) out[i] += (double)other[i] * mix[i];
+      break;
+    default: {
+      const uint32_t h = d / 2;
+      for (uint32_t i = 0; i < h; ++i) {
+        const double orr = other[i], ori = other[i + h];
+        out[i] += orr * mix[i] + ori * mix[i + h];
+        out[i + h] += orr * mix[i + h] - ori * mix[i];
+      }
+    }
+  }
+}
+
+/* train.cpp:342-354 adagrad_update (FP64 math, FP32 storage; the update uses
+ * the unrounded accumulator a) */
+static void adagrad_row(float* theta, float* acc, const double* g, uint32_t d, double lr,
+                        double eps) {
+  for (uint32_t i = 0; i < d; ++i) {
+    const double gi = g[i];
+    const double a = (double)acc[i] + gi * gi;
+    acc[i] = (float)a;
+    theta[i] = (float)((double)theta[i] - lr * gi / (sqrt(a) + eps));
+  }
+}
+
+typedef struct {
+  uint32_t id;
+  uint32_t pad;
+  uint64_t seq; /* enumeration order (p, slot) -- the std::map visit order */
+} lo_contrib;
+
+static int contrib_cmp(const void* a, const void* b) {
+  const lo_contrib* x = (const lo_contrib*)a;
+  const lo_contrib* y = (const lo_contrib*)b;
+  if (x->id != y->id) return x->id < y->id ? -1 : 1;
+  return x->seq < y->seq ? -1 : (x->seq > y->seq ? 1 : 0);
+}
+
+static int check_model(int kind, uint32_t dim) {
+  /* train.cpp:11-16 ScoreModel::validate */
+  if (dim == 0) return LO_INVALID;
+  if (kind == LO_KIND_COMPLEX && dim % 2 != 0) return LO_INVALID;
+  if (kind < 0 || kind > 2) return LO_INVALID;
+  return LO_OK;
+}
+
+/*
+ * One training step: batch_loss (train.cpp:217-278), batch_gradients
+ * (train.cpp:280-340) and, if apply, adagrad_step (train.cpp:356-363) on a
+ * single all-resident table of num_nodes rows.  Gradients are accumulated per
+ * node in the reference's std::map visit order: positives ascending, and per
+ * positive dst, negatives j ascending, then src.  Optional outputs: the sorted
+ * unique node / relation ids and their FP64 gradients.
+ */
+int lo_batch(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes, float* relE,
+             float* relS, uint64_t num_rels, const uint32_t* edges, uint64_t P,
+             const uint32_t* negs, uint32_t k, double lr, double eps, int apply, double* loss_out,
+             uint64_t* n_nodes_out, uint32_t* node_ids, double* node_grads, uint64_t* n_rels_out,
+             uint32_t* rel_ids, double* rel_grads) {
+  int rc = check_model(kind, d);
+  if (rc) return rc;
+  if (k == 0) return LO_INVALID; /* train.cpp:219-221 */
+  const int typed = kind != LO_KIND_DOT;
+  for (uint64_t p = 0; p < P; ++p) {
+    const uint32_t s = edges[3 * p], r = edges[3 * p + 1], t = edges[3 * p + 2];
+    if (s >= num_nodes || t >= num_nodes) return LO_RANGE; /* train.cpp:157 */
+    if (typed) {
+      if (r == LO_NO_REL) return LO_INVALID; /* train.cpp:209-211 */
+      if (r >= num_rels) return LO_RANGE;    /* train.cpp:176 */
+    }
+    for (uint32_t j = 0; j < k; ++j)
+      if (negs[p * k + j] >= num_nodes) return LO_RANGE;
+  }
+
+  const uint64_t slots = (uint64_t)k + 2;
+  double* ir1 = (double*)malloc((P ? P : 1) * d * sizeof(double));
+  double* w = (double*)malloc((P ? P : 1) * k * sizeof(double));
+  double* f = (double*)malloc(k * sizeof(double));
+  lo_contrib* con = (lo_contrib*)malloc((P ? P : 1) * slots * sizeof(lo_contrib));
+  double* mixes = (double*)malloc((P ? P : 1) * d * sizeof(double));
+  double* rowsum = (double*)malloc((P ? P : 1) * sizeof(double));
+  if (!ir1 || !w || !f || !con || !mixes || !rowsum) {
+    free(ir1), free(w), free(f), free(con), free(mixes), free(rowsum);
+    return LO_NOMEM;
+  }
+
+  /* batch_loss: train.cpp:236-275 */
+  double loss = 0.0;
+  for (uint64_t p = 0; p < P; ++p) {
+    const uint32_t s = edges[3 * p], r = edges[3 * p + 1], t = edges[3 * p + 2];
+    double* x = ir1 + p * d;
+    combine(kind, d, E + (uint64_t)s * d, typed ? relE + (uint64_t)r * d : NULL, x);
+    const float* dst = E + (uint64_t)t * d;
+    double pos = 0.0;
+    for (uint32_t i = 0; i < d; ++i) {
+      const double term = x[i] * dst[i];
+      pos += term;
+    }
+    double row_max = -INFINITY;
+    for (uint32_t j = 0; j < k; ++j) {
+      const float* neg = E + (uint64_t)negs[p * k + j] * d;
+      double fj = 0.0;
+      for (uint32_t i = 0; i < d; ++i) fj += x[i] * neg[i];
+      f[j] = fj;
+      row_max = (row_max < fj) ? fj : row_max; /* std::max(row_max, f) */
+    }
+    double sum = 0.0;
+    for (uint32_t j = 0; j < k; ++j) {
+      const double ex = exp(f[j] - row_max);
+      w[p * k + j] = ex;
+      sum += ex;
+    }
+    rowsum[p] = sum; /* IR3 row sum; w holds IR3 until the gradient pass */
+    loss += -(pos - (row_max + log(sum)));
+  }
+
+  /* batch_gradients: per-positive mix, then per-node accumulation in the
+   * std::map visit order (train.cpp:298-333). */
+  for (uint64_t p = 0; p < P; ++p) {
+    const double inv_sum = 1.0 / rowsum[p];
+    for (uint32_t j = 0; j < k; ++j) w[p * k + j] = w[p * k + j] * inv_sum;
+    const float* dst = E + (uint64_t)edges[3 * p + 2] * d;
+    double* mix = mixes + p * d;
+    for (uint32_t i = 0; i < d; ++i) mix[i] = -(double)dst[i];
+    for (uint32_t j = 0; j < k; ++j) {
+      const float* neg = E + (uint64_t)negs[p * k + j] * d;
+      const double wj = w[p * k + j];
+      for (uint32_t i = 0; i < d; ++i) mix[i] += wj * neg[i];
+    }
+    con[p * slots].id = edges[3 * p + 2];
+    con[p * slots].seq = p * slots;
+    for (uint32_t j = 0; j < k; ++j) {
+      con[p * slots + 1 + j].id = negs[p * k + j];
+      con[p * slots + 1 + j].seq = p * slots + 1 + j;
+    }
+    con[p * slots + k + 1].id = edges[3 * p];
+    con[p * slots + k + 1].seq = p * slots + k + 1;
+  }
+  qsort(con, P * slots, sizeof(lo_contrib), contrib_cmp);
+
+  double* g = (double*)malloc(d * sizeof(double));
+  uint64_t n_nodes = 0;
+  /* First pass computes every gradient against the pre-update table; updates
+   * are applied after all gradients exist (adagrad_step runs after
+   * batch_gradients returns). */
+  uint64_t uniq = 0;
+  for (uint64_t c = 0; c < P * slots; ++c)
+    if (c == 0 || con[c].id != con[c - 1].id) ++uniq;
+  double* gall = (double*)malloc((uniq ? uniq : 1) * d * sizeof(double));
+  uint32_t* gid = (uint32_t*)malloc((uniq ? uniq : 1) * sizeof(uint32_t));
+  if (!g || !gall || !gid) {
+    free(ir1), free(w), free(f), free(con), free(mixes), free(rowsum), free(g), free(gall),
+        free(gid);
+    return LO_NOMEM;
+  }
+  for (uint64_t c = 0; c < P * slots;) {
+    const uint32_t id = con[c].id;
+    double* acc = gall + n_nodes * d;
+    for (uint32_t i = 0; i < d; ++i) acc[i] = 0.0;
+    for (; c < P * slots && con[c].id == id; ++c) {
+      const uint64_t p = con[c].seq / slots;
+      const uint64_t slot = con[c].seq % slots;
+      const double* x = ir1 + p * d;
+      if (slot == 0) {
+        for (uint32_t i = 0; i < d; ++i) acc[i] -= x[i]; /* train.cpp:310 */
+      } else if (slot <= k) {
+        const double wj = w[p * k + (slot - 1)];
+        for (uint32_t i = 0; i < d; ++i) acc[i] += wj * x[i]; /* train.cpp:320 */
+      } else {
+        const uint32_t r = edges[3 * p + 1];
+        adjoint(kind, d, typed ? relE + (uint64_t)r * d : NULL, mixes + p * d,
+                acc); /* train.cpp:327 */
+      }
+    }
+    gid[n_nodes] = id;
+    ++n_nodes;
+  }
+
+  /* relation gradients: train.cpp:328-332, positives ascending per relation */
+  uint64_t n_rels = 0;
+  double* rall = NULL;
+  uint32_t* rid = NULL;
+  if (typed && P > 0) {
+    lo_contrib* rc2 = (lo_contrib*)malloc(P * sizeof(lo_contrib));
+    rall = (double*)malloc(P * d * sizeof(double));
+    rid = (uint32_t*)malloc(P * sizeof(uint32_t));
+    for (uint64_t p = 0; p < P; ++p) {
+      rc2[p].id = edges[3 * p + 1];
+      rc2[p].seq = p;
+    }
+    qsort(rc2, P, sizeof(lo_contrib), contrib_cmp);
+    for (uint64_t c = 0; c < P;) {
+      const uint32_t id = rc2[c].id;
+      double* acc = rall + n_rels * d;
+      for (uint32_t i = 0; i < d; ++i) acc[i] = 0.0;
+      for (; c < P && rc2[c].id == id; ++c) {
+        const uint64_t p = rc2[c].seq;
+        adjoint(kind, d, E + (uint64_t)edges[3 * p] * d, mixes + p * d, acc);
+      }
+      rid[n_rels++] = id;
+    }
+    free(rc2);
+  }
+
+  if (n_nodes_out) *n_nodes_out = n_nodes;
+  if (n_rels_out) *n_rels_out = n_rels;
+  if (node_ids) memcpy(node_ids, gid, n_nodes * sizeof(uint32_t));
+  if (node_grads) memcpy(node_grads, gall, n_nodes * d * sizeof(double));
+  if (rel_ids && n_rels) memcpy(rel_ids, rid, n_rels * sizeof(uint32_t));
+  if (rel_grads && n_rels) memcpy(rel_grads, rall, n_rels * d * sizeof(double));
+
+  if (apply) { /* train.cpp:356-363: nodes ascending, then relations */
+    for (uint64_t u = 0; u < n_nodes; ++u)
+      adagrad_row(E + (uint64_t)gid[u] * d, S + (uint64_t)gid[u] * d, gall + u * d, d, lr, eps);
+    for (uint64_t u = 0; u < n_rels; ++u)
+      adagrad_row(relE + (uint64_t)rid[u] * d, relS + (uint64_t)rid[u] * d, rall + u * d, d, lr,
+                  eps);
+  }
+  if (loss_out) *loss_out = loss;
+  free(ir1), free(w), free(f), free(con), free(mixes), free(rowsum), free(g), free(gall),
+      free(gid);
+  free(rall), free(rid);
+  return LO_OK;
+}
+
+/* ------------------------------------------------------------- epoch --- */
+
+/*
+ * Real-train epoch (pipeline.cpp:273-322) restated over one all-resident
+ * table, exactly as the reference's own test does (test_pipeline.cpp:227-269):
+ * the negative-sampling pool of bucket g is the set of partitions resident in
+ * the plan state that contains g.  states is num_states x 3 partition ids
+ * (0xffffffff = unused slot, which lets n <= 3 run as one state holding every
+ * partition); bucket_order is n*n (src_part, dst_part) pairs; state_offsets
+ * has num_states + 1 entries.
+ *
+ * Optional dumps (NULL to skip): per-batch loss and unique node / relation
+ * counts (max_batches entries), the shuffled in-bucket positions of every
+ * trained edge (num_edges entries, in bucket_order), and every negative id
+ * (num_edges * k entries).
+ */
+int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
+                 uint64_t num_rels, uint32_t n, uint64_t stride, const uint64_t* bucket_offsets,
+                 const uint64_t* edge_order, uint64_t num_states, const uint32_t* states,
+                 const uint32_t* bucket_order, const uint64_t* state_offsets, int kind, uint32_t d,
+                 double lr, double eps, uint32_t batch_size, uint32_t k, int shuffle,
+                 uint64_t seed, uint32_t epoch, float* E, float* S, float* relE, float* relS,
+                 double* loss_sum_out, uint64_t* edges_trained_out, uint64_t* buckets_trained_out,
+                 uint64_t* num_batches_out, uint64_t max_batches, double* batch_loss,
+                 uint64_t* batch_nodes, uint64_t* batch_rels, uint32_t* perm_dump,
+                 uint32_t* neg_dump) {
+  int rc = check_model(kind, d);
+  if (rc) return rc;
+  if (kind != LO_KIND_DOT && num_rels == 0) return LO_INVALID; /* pipeline.cpp:228-230 */
+  if (batch_size == 0 || k == 0) return LO_INVALID;
+  const uint64_t G = (uint64_t)n * n;
+  double loss_sum = 0.0;
+  uint64_t edges_trained = 0, buckets_trained = 0, nb = 0, perm_pos = 0, neg_pos = 0;
+  uint64_t state = 0;
+  uint32_t* bucket = NULL;
+  uint32_t* pos = NULL;
+  uint32_t* negs = NULL;
+  uint32_t* batch_edges = NULL;
+  uint64_t cap = 0;
+  rc = LO_OK;
+  for (uint64_t g = 0; g < G; ++g) {
+    while (state + 1 < num_states && g >= state_offsets[state + 1]) ++state;
+    const uint32_t bi = bucket_order[2 * g], bj = bucket_order[2 * g + 1];
+    const uint64_t b = (uint64_t)bi * n + bj;
+    const uint64_t m = bucket_offsets[b + 1] - bucket_offsets[b];
+    if (m == 0) continue; /* pipeline.cpp:291: before the RNG is created */
+    if (m > cap) {
+      free(bucket), free(pos), free(negs), free(batch_edges);
+      cap = m;
+      bucket = (uint32_t*)malloc(cap * 3 * sizeof(uint32_t));
+      pos = (uint32_t*)malloc(cap * sizeof(uint32_t));
+      uint64_t bcap = cap < batch_size ? cap : batch_size;
+      negs = (uint32_t*)malloc(bcap * k * sizeof(uint32_t));
+      batch_edges = (uint32_t*)malloc(bcap * 3 * sizeof(uint32_t));
+      if (!bucket || !pos || !negs || !batch_edges) {
+        rc = LO_NOMEM;
+        goto done;
+      }
+    }
+    for (uint64_t i = 0; i < m; ++i) { /* pipeline.cpp:293-295 */
+      const uint64_t e = edge_order[bucket_offsets[b] + i];
+      memcpy(bucket + 3 * i, edges + 3 * e, 3 * sizeof(uint32_t));
+      pos[i] = (uint32_t)i;
+    }
+    lo_rng rng; /* pipeline.cpp:296 "bukt" stream */
+    lo_rng_init(&rng, lo_derive_seed(seed, 0x62756b74ull, epoch, g));
+    if (shuffle) { /* pipeline.cpp:297-301 Fisher-Yates */
+      for (uint64_t i = m; i > 1; --i) {
+        const uint64_t j = lo_rng_below(&rng, i);
+        uint32_t tmp[3];
+        memcpy(tmp, bucket + 3 * (i - 1), sizeof tmp);
+        memcpy(bucket + 3 * (i - 1), bucket + 3 * j, sizeof tmp);
+        memcpy(bucket + 3 * j, tmp, sizeof tmp);
+        const uint32_t tp = pos[i - 1];
+        pos[i - 1] = pos[j];
+        pos[j] = tp;
+      }
+    }
+    if (perm_dump) memcpy(perm_dump + perm_pos, pos, m * sizeof(uint32_t));
+    perm_pos += m;
+    /* resident pool of this state, ascending node ranges (train.cpp:112-119) */
+    uint64_t first[3], count[3];
+    int np = 0;
+    uint32_t ids[3];
+    for (int s2 = 0; s2 < 3; ++s2) {
+      const uint32_t p = states[3 * state + s2];
+      if (p == 0xffffffffu) continue;
+      ids[np++] = p;
+    }
+    for (int a = 0; a < np; ++a)
+      for (int c = a + 1; c < np; ++c)
+        if (ids[c] < ids[a]) {
+          uint32_t t = ids[a];
+          ids[a] = ids[c];
+          ids[c] = t;
+        }
+    for (int a = 0; a < np; ++a) {
+      first[a] = stride * ids[a];
+      uint64_t end = stride * (ids[a] + 1);
+      if (end > num_nodes) end = num_nodes;
+      count[a] = end - first[a];
+    }
+    for (uint64_t off = 0; off < m; off += batch_size) { /* pipeline.cpp:303-312 */
+      const uint64_t cnt = (m - off) < batch_size ? (m - off) : batch_size;
+      rc = lo_sample_negatives_rng(first, count, np, k, cnt, &rng, negs);
+      if (rc) goto done;
+      if (neg_dump) memcpy(neg_dump + neg_pos, negs, cnt * k * sizeof(uint32_t));
+      neg_pos += cnt * k;
+      double l = 0.0;
+      uint64_t un = 0, ur = 0;
+      rc = lo_batch(kind, d, E, S, num_nodes, relE, relS, num_rels, bucket + 3 * off, cnt, negs,
+                    k, lr, eps, 1, &l, &un, NULL, NULL, &ur, NULL, NULL);
+      if (rc) goto done;
+      if (nb < max_batches) {
+        if (batch_loss) batch_loss[nb] = l;
+        if (batch_nodes) batch_nodes[nb] = un;
+        if (batch_rels) batch_rels[nb] = ur;
+      }
+      ++nb;
+      loss_sum += l;
+    }
+    edges_trained += m;
+    ++buckets_trained;
+  }
+done:
+  free(bucket), free(pos), free(negs), free(batch_edges);
+  if (loss_sum_out) *loss_sum_out = loss_sum;
+  if (edges_trained_out) *edges_trained_out = edges_trained;
+  if (buckets_trained_out) *buckets_trained_out = buckets_trained;
+  if (num_batches_out) *num_batches_out = nb;
+  (void)num_edges;
+  return rc;
+}
+
+/* ---------------------------------------------------------- evaluate --- */
+
+/* train.cpp:375-412 evaluate over an all-resident table (train.cpp:414-421
+ * loads every partition in order, so resident_node_at(i) == i). */
+int lo_evaluate(int kind, uint32_t d, const float* E, uint64_t num_nodes, const float* relE,
+                uint64_t num_rels, const uint32_t* test_edges, uint64_t T,
+                uint32_t num_candidates, uint32_t hits_k, uint64_t seed, double* mrr_out,
+                double* hits_out) {
+  int rc = check_model(kind, d);
+  if (rc) return rc;
+  if (T == 0) return LO_INVALID;
+  if (num_candidates == 0) return LO_INVALID;
+  const int typed = kind != LO_KIND_DOT;
+  double* ir1 = (double*)malloc(d * sizeof(double));
+  double mrr = 0.0, hits = 0.0;
+  for (uint64_t t = 0; t < T; ++t) {
+    const uint32_t s = test_edges[3 * t], r = test_edges[3 * t + 1], dd = test_edges[3 * t + 2];
+    if (typed && r == LO_NO_REL) {
+      free(ir1);
+      return LO_INVALID;
+    }
+    if (typed && r >= num_rels) {
+      free(ir1);
+      return LO_RANGE;
+    }
+    if (s >= num_nodes || dd >= num_nodes) {
+      free(ir1);
+      return LO_RANGE;
+    }
+    combine(kind, d, E + (uint64_t)s * d, typed ? relE + (uint64_t)r * d : NULL, ir1);
+    double truth = 0.0;
+    for (uint32_t i = 0; i < d; ++i) truth += ir1[i] * E[(uint64_t)dd * d + i];
+    lo_rng rng;
+    lo_rng_init(&rng, lo_derive_seed(seed, 0x65766179ull, t, 0));
+    uint64_t beaten = 0;
+    for (uint32_t c = 0; c < num_candidates; ++c) {
+      const uint64_t cand = lo_rng_below(&rng, num_nodes);
+      double f = 0.0;
+      for (uint32_t i = 0; i < d; ++i) f += ir1[i] * E[cand * d + i];
+      if (f >= truth) ++beaten;
+    }
+    const uint64_t rank = 1 + beaten;
+    mrr += 1.0 / (double)rank;
+    hits += rank <= hits_k ? 1.0 : 0.0;
+  }
+  free(ir1);
+  *mrr_out = mrr / (double)T;
+  *hits_out = hits / (double)T;
+  return LO_OK;
+}
