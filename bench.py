@@ -1,0 +1,354 @@
+"""Benchmark of the partitioned graph-embedding training hot path on B200.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on at
+1/2/4/8 GPUs): Twitter-shaped synthetic power-law graph -- 41.6M nodes, 1.3B
+edges, 16 relations -- DistMult d=100, 16 partitions, k=16 negatives per
+positive, batch 100,000, lr 0.1, Adagrad eps 1e-10, seed 42.
+
+A step is one bucket of the reference iteration plan (seeded shuffle,
+negative draws and every batch of the bucket: score, sort, sparse Adagrad).
+`value` is edges trained per second of device time (CUDA events), inputs
+resident in HBM; `e2e` runs the same buckets through the C ABI with each
+bucket's edges copied from pinned host memory and its losses read back, per
+step.  `--impl reference` times the reference CPU trainer (oracle/_ref, or
+the C restatement when _ref is absent) on a bounded sample of the same
+workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training edges/sec per epoch (1/2/4/8 B200) and % HBM roofline vs CPU ref"
+CONFIGS = {
+    "tw": dict(workload="Twitter-shaped synthetic power-law graph, DistMult d=100, 16 partitions",
+               nodes=41_600_000, edges=1_300_000_000, rels=16, model="distmult", dim=100, n=16),
+    "lj": dict(workload="LiveJournal-shaped synthetic power-law graph, Dot d=100, 8 partitions",
+               nodes=4_800_000, edges=68_000_000, rels=0, model="dot", dim=100, n=8),
+    "fb15k": dict(workload="FB15k-shaped synthetic KG, DistMult d=100, 1 partition",
+                  nodes=15_000, edges=592_000, rels=1345, model="distmult", dim=100, n=1),
+}
+K_NEG, BATCH, LR, SEED, ALPHA, GRAPH_SEED = 16, 100_000, 0.1, 42, 2.1, 20250509
+REF_SAMPLE_POSITIVES = 25_000  # positives per reference step (bounded CPU sample)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return rank, world, local, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def max_over_ranks(pg, value, local):
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(pg, value, local):
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ CPU reference
+def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
+    """Time the reference CPU trainer on a bounded sample: the first state's
+    resident partitions {0,1,2} (initialised exactly like the store), bucket
+    (0,1)'s edges, `steps` consecutive batches of `batch` positives."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if (which != "port" and available("reference")) else "restatement"
+    o = Oracle(kind)
+    lo = Oracle("restatement")
+    d, R = cfg["dim"], cfg["rels"]
+    V_loc = min(3 * stride, cfg["nodes"])
+    E = np.zeros((V_loc, d), np.float32)
+    for p in range(3):
+        a, b = p * stride, min((p + 1) * stride, V_loc)
+        if b > a:
+            lo.init_rows(lo.derive_seed(SEED, p), b - a, d, E[a:b])
+    S = np.zeros_like(E)
+    rE = np.zeros((max(R, 1), d), np.float32)
+    if R:
+        lo.init_rows(lo.derive_seed(SEED, 0x52454C53), R, d, rE)
+    rS = np.zeros_like(rE)
+    first = [0, stride, 2 * stride]
+    count = [min(stride, V_loc - f) for f in first]
+    stream = lo.derive_seed(SEED, 0x62756B74, 0, 0)
+    m = min(len(bucket_edges), steps * batch)
+    t0 = time.perf_counter()
+    _, done = o.bucket_sample(cfg["model"], bucket_edges[:m], first, count, stream, E, S,
+                              rE if R else None, rS if R else None, batch_size=batch, k=K_NEG,
+                              max_batches=steps, lr=LR)
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "edges/s", "cores": 1,
+            "kind": "reference" if kind == "reference" else "port",
+            "sample": (f"state {{0,1,2}} resident ({V_loc:,} rows), bucket (0,1): shuffle of "
+                       f"{m:,} edges then {steps} batch(es) of {batch:,} positives, "
+                       f"{cfg['model']} d={d} k={K_NEG}; {done:,} edges in {dt:.1f} s"),
+            "seconds": dt, "edges": done}
+
+
+def setup_trainer(cfg, device):
+    import paper_2505_09258_b200 as lgd
+    opts = lgd.TrainOptions(learning_rate=LR, batch_size=BATCH, negatives=K_NEG, shuffle=True,
+                            seed=SEED)
+    t = lgd.Trainer(lgd.ScoreModel(cfg["model"], cfg["dim"]), opts, device=device)
+    t.generate_graph(cfg["nodes"], cfg["rels"], cfg["edges"], ALPHA, GRAPH_SEED)
+    t.make_partition_plan(cfg["n"])
+    t.init_store(SEED)
+    return t
+
+
+def reference_arm(args, cfg, rank):
+    if rank != 0:
+        return
+    import paper_2505_09258_b200 as lgd
+    # bucket (0,1) of the same synthetic graph: generated on the GPU (the
+    # generator is part of the workload definition, not of the timed path)
+    t = lgd.Trainer(lgd.ScoreModel(cfg["model"], cfg["dim"]),
+                    lgd.TrainOptions(batch_size=BATCH, negatives=K_NEG, seed=SEED))
+    t.generate_graph(cfg["nodes"], cfg["rels"], cfg["edges"], ALPHA, GRAPH_SEED)
+    offsets, _ = t.make_partition_plan(cfg["n"])
+    stride = t.stride()
+    b = 0 * cfg["n"] + 1 if cfg["n"] > 1 else 0
+    a0, a1 = int(offsets[b]), int(offsets[b + 1])
+    need = min(a1 - a0, (args.steps + args.warmup) * REF_SAMPLE_POSITIVES)
+    allb = t.bucketed_edges()
+    bucket = np.ascontiguousarray(allb[a0:a0 + max(need, 1)])
+    del allb
+    t.close()
+    # warmup steps run first (untimed) on the leading batches, then K timed
+    res = cpu_sample(cfg, bucket, stride, args.steps + args.warmup, REF_SAMPLE_POSITIVES,
+                     "reference")
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "edges/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * res["seconds"] / (args.steps + args.warmup),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["workload"], "step": (
+                f"{REF_SAMPLE_POSITIVES:,} positives of bucket (0,1)"), "storage": "f32"},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def traffic_from_profiles():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="tw", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank, world, local, pg = dist_setup(args.gpus)
+    if args.impl == "reference":
+        reference_arm(args, cfg, rank)
+        return
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+
+    import paper_2505_09258_b200 as lgd
+    t_setup = time.perf_counter()
+    t = setup_trainer(cfg, local)
+    G = cfg["n"] ** 2
+    # weak scaling: rank r trains its own K consecutive buckets of the plan
+    # (tables replicated per GPU)
+    g0 = args.warmup + rank * args.steps
+    if g0 + args.steps > G:
+        g0 = max(0, G - args.steps)
+    warm_lo = max(0, g0 - args.warmup)
+    setup_s = time.perf_counter() - t_setup
+
+    t.train_buckets(0, warm_lo, g0)  # warm-up buckets (untimed)
+    t.reset_kernel_stats()
+    t.set_profiling(True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(pg)
+    t.synchronize()
+    res = t.train_buckets(0, g0, g0 + args.steps)
+    t.synchronize()
+    barrier(pg)
+    clk = clocks.stop()
+    launches = t.launch_count()
+    stats = t.kernel_stats()
+    t.set_profiling(False)
+
+    dev_s = max_over_ranks(pg, res.device_ms / 1e3, local)
+    edges_all = sum_over_ranks(pg, res.edges_trained, local)
+    value = edges_all / dev_s
+
+    # roofline of the dominant HBM-bound kernel class (per launch averages)
+    hbm, peak_kind = peaks()
+    cand = {k: v for k, v in stats.items() if k in ("score", "update") and v["launches"]}
+    dom = max(cand, key=lambda k: cand[k]["total_ms"])
+    dstat = stats[dom]
+    achieved = dstat["algorithmic_bytes"] / (dstat["total_ms"] / 1e3) / 1e9
+    traffic = traffic_from_profiles()
+    roofline = {"bound": "hbm", "kernel": {"score": "score_kernel (K3)",
+                                           "update": "segment_pass1+2 (K4)"}[dom],
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": peak_kind,
+                "traffic": (traffic or {}).get(dom),
+                "algorithmic_bytes_per_launch": dstat["algorithmic_bytes"] / dstat["launches"],
+                "avg_launch_ms": dstat["total_ms"] / dstat["launches"],
+                "step_achieved": res.algorithmic_bytes / (res.device_ms / 1e3) / 1e9,
+                "step_frac": res.algorithmic_bytes / (res.device_ms / 1e3) / 1e9 / hbm,
+                "phase_ms": {k: round(v["total_ms"], 3) for k, v in stats.items()}}
+
+    e2e = None
+    if not args.no_e2e:
+        host = lgd.PinnedArray((t.num_edges, 3), np.uint32)
+        t.bucketed_edges(host.array)
+        barrier(pg)
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for g in range(g0, g0 + args.steps):  # per step: H2D edges, train, D2H losses
+            r = t.train_buckets_from_host(1, g, g + 1, host.array)
+            h2d += r.h2d_bytes
+            d2h += r.d2h_bytes
+        wall = time.perf_counter() - t0
+        barrier(pg)
+        wall = max_over_ranks(pg, wall, local)
+        host.free()
+        e2e = {"value": edges_all / wall, "unit": "edges/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        offsets = t.bucket_offsets
+        b = 1 if cfg["n"] > 1 else 0
+        a0, a1 = int(offsets[b]), int(offsets[b + 1])
+        allb = t.bucketed_edges()
+        bucket = np.ascontiguousarray(allb[a0:a0 + min(a1 - a0, 4 * REF_SAMPLE_POSITIVES)])
+        del allb
+        cpu = cpu_sample(cfg, bucket, t.stride(), 4, REF_SAMPLE_POSITIVES, "reference")
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "num_nodes": cfg["nodes"],
+                       "num_edges": cfg["edges"], "num_relations": cfg["rels"],
+                       "dim": cfg["dim"], "partitions": cfg["n"], "negatives": K_NEG,
+                       "batch_size": BATCH, "storage": "f32 (E||S), FP64 arithmetic",
+                       "graph": f"power-law alpha={ALPHA}, generator seed {GRAPH_SEED}",
+                       "step": "one bucket of the reference iteration plan",
+                       "buckets_timed": [g0, g0 + args.steps],
+                       "edges_per_rank": res.edges_trained, "batches": res.batches,
+                       "unique_rows_per_batch": res.unique_nodes / max(res.batches, 1),
+                       "l2": "inputs larger than L2 (33 GB table, 15.6 GB edges)",
+                       "parallelism": "bucket slices per GPU" if world > 1 else "single GPU",
+                       "setup_s": round(setup_s, 1)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    t.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -661,3 +661,74 @@ int lo_evaluate(int kind, uint32_t d, const float* E, uint64_t num_nodes, const 
   *hits_out = hits / (double)T;
   return LO_OK;
 }
+
+/* The bucket shuffle of pipeline.cpp:297-301 applied to positions: perm[i] is
+ * the original in-bucket index that ends at position i; consumed = raw draws. */
+void lo_shuffle_perm(uint64_t seed, uint64_t m, uint32_t* perm, uint64_t* consumed) {
+  lo_rng r;
+  lo_rng_init(&r, seed);
+  for (uint64_t i = 0; i < m; ++i) perm[i] = (uint32_t)i;
+  uint64_t used = 0;
+  for (uint64_t i = m; i > 1; --i) {
+    const uint64_t bound = i;
+    const uint64_t threshold = (0 - bound) % bound;
+    uint64_t x;
+    do {
+      x = lo_rng_next(&r);
+      ++used;
+    } while (x < threshold);
+    const uint64_t j = x % bound;
+    const uint32_t t = perm[i - 1];
+    perm[i - 1] = perm[j];
+    perm[j] = t;
+  }
+  if (consumed) *consumed = used;
+}
+
+/* Bounded CPU-baseline sample of the real-train loop (pipeline.cpp:289-312)
+ * for ONE bucket: copy, seeded Fisher-Yates shuffle, then up to max_batches
+ * batches of sample_negatives + batch_loss + batch_gradients + adagrad_step.
+ * The table holds rows [0, num_nodes); the pool lists the resident ranges. */
+int lo_bucket_sample(const uint32_t* bucket_edges, uint64_t m, const uint64_t* first,
+                     const uint64_t* count, int nparts, uint64_t stream_seed, int shuffle,
+                     uint32_t batch_size, uint32_t k, uint64_t max_batches, int kind, uint32_t d,
+                     float* E, float* S, uint64_t num_nodes, float* relE, float* relS,
+                     uint64_t num_rels, double lr, double eps, double* loss_sum,
+                     uint64_t* edges_trained) {
+  uint32_t* edges = (uint32_t*)malloc((m ? m : 1) * 3 * sizeof(uint32_t));
+  uint32_t* negs = (uint32_t*)malloc((uint64_t)batch_size * k * sizeof(uint32_t));
+  if (!edges || !negs) {
+    free(edges), free(negs);
+    return LO_NOMEM;
+  }
+  memcpy(edges, bucket_edges, m * 3 * sizeof(uint32_t));
+  lo_rng rng;
+  lo_rng_init(&rng, stream_seed);
+  if (shuffle) {
+    for (uint64_t i = m; i > 1; --i) {
+      const uint64_t j = lo_rng_below(&rng, i);
+      uint32_t t[3];
+      memcpy(t, edges + 3 * (i - 1), sizeof t);
+      memcpy(edges + 3 * (i - 1), edges + 3 * j, sizeof t);
+      memcpy(edges + 3 * j, t, sizeof t);
+    }
+  }
+  double total = 0.0;
+  uint64_t done = 0, nb = 0;
+  int rc = LO_OK;
+  for (uint64_t off = 0; off < m && nb < max_batches; off += batch_size, ++nb) {
+    const uint64_t cnt = (m - off) < batch_size ? (m - off) : batch_size;
+    rc = lo_sample_negatives_rng(first, count, nparts, k, cnt, &rng, negs);
+    if (rc) break;
+    double l = 0.0;
+    rc = lo_batch(kind, d, E, S, num_nodes, relE, relS, num_rels, edges + 3 * off, cnt, negs, k,
+                  lr, eps, 1, &l, NULL, NULL, NULL, NULL, NULL, NULL);
+    if (rc) break;
+    total += l;
+    done += cnt;
+  }
+  free(edges), free(negs);
+  *loss_sum = total;
+  *edges_trained = done;
+  return rc;
+}

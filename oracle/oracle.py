@@ -65,7 +65,10 @@ class Oracle:
         bind("batch", i32, [i32, u32, vp, vp, u64, vp, vp, u64, vp, u64, vp, u32, f64, f64, i32,
                             vp, vp, vp, vp, vp, vp, vp])
         bind("evaluate", i32, [i32, u32, vp, u64, vp, u64, vp, u64, u32, u32, u64, vp, vp])
+        bind("bucket_sample", i32, [vp, u64, vp, vp, i32, u64, i32, u32, u32, u64, i32, u32, vp,
+                                    vp, u64, vp, vp, u64, f64, f64, vp, vp])
         if which == "restatement":
+            bind("shuffle_perm", None, [u64, u64, vp, vp])
             bind("store_init", None, [u32, u64, u32, u64, u64, vp, vp, vp, vp])
             bind("run_epoch", i32, [vp, u64, u64, u64, u32, u64, vp, vp, u64, vp, vp, vp, i32,
                                     u32, f64, f64, u32, u32, i32, u64, u32, vp, vp, vp, vp, vp,
@@ -139,6 +142,13 @@ class Oracle:
         self._check(self._fn["sample_negatives"](_ptr(first), _ptr(count), len(first), k,
                                                  num_positives, seed, skip, _ptr(out)))
         return out[:num_positives * k]
+
+    def shuffle_perm(self, seed, m):
+        """pipeline.cpp:297-301 on positions (restatement only)."""
+        perm = np.zeros(max(m, 1), np.uint32)
+        used = np.zeros(1, np.uint64)
+        self._fn["shuffle_perm"](seed, m, _ptr(perm), _ptr(used))
+        return perm[:m], int(used[0])
 
     # ---------------------------------------------------------- training
     def batch(self, kind, E, S, relE, relS, edges, negs, k, lr=0.1, eps=1e-10, apply=True,
@@ -218,6 +228,31 @@ class Oracle:
                        batch_rels=br[:b].copy(), perm=pd[:Ecount].copy(),
                        negs=nd[:out["edges_trained"] * k].copy())
         return out
+
+    def bucket_sample(self, kind, bucket_edges, first, count, stream_seed, E, S, relE, relS, *,
+                      batch_size, k, max_batches, shuffle=True, lr=0.1, eps=1e-10):
+        """One bucket of the real-train loop, at most max_batches batches, in place."""
+        kind = KINDS.get(kind, kind)
+        V, d = E.shape
+        R = relE.shape[0] if relE is not None else 0
+        if relE is None:
+            relE = np.zeros((1, d), np.float32)
+            relS = np.zeros((1, d), np.float32)
+        be = np.ascontiguousarray(bucket_edges, np.uint32).reshape(-1, 3)
+        first = np.ascontiguousarray(first, np.uint64)
+        count = np.ascontiguousarray(count, np.uint64)
+        loss = np.zeros(1, np.float64)
+        done = np.zeros(1, np.uint64)
+        self._check(self._fn["bucket_sample"](
+            _ptr(be), len(be), _ptr(first), _ptr(count), len(first), stream_seed, int(shuffle),
+            batch_size, k, max_batches, kind, d, _ptr(E), _ptr(S), V, _ptr(relE), _ptr(relS), R,
+            lr, eps, _ptr(loss), _ptr(done)))
+        return float(loss[0]), int(done[0])
+
+    def init_rows(self, stream_seed, rows, dim, out):
+        """fill_uniform_rows (store.cpp:19-25) into a float32 slice (restatement)."""
+        self.lib.lo_init_rows.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p]
+        self.lib.lo_init_rows(stream_seed, rows, dim, _ptr(out))
 
     def evaluate(self, kind, E, relE, test_edges, num_candidates=999, hits_k=10, seed=0):
         kind = KINDS.get(kind, kind)

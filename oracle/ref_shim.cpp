@@ -429,6 +429,52 @@ int ref_run_epoch_inmem(const std::uint32_t* edges, std::uint64_t num_edges,
   });
 }
 
+// Bounded CPU-baseline sample through the reference primitives: one bucket's
+// copy + shuffle (pipeline.cpp:293-301) and up to max_batches batches of
+// sample_negatives + batch_loss + batch_gradients + adagrad_step
+// (pipeline.cpp:303-312).  The table holds rows [0, num_nodes).
+int ref_bucket_sample(const std::uint32_t* bucket_edges, std::uint64_t m,
+                      const std::uint64_t* first, const std::uint64_t* count, int nparts,
+                      std::uint64_t stream_seed, int shuffle, std::uint32_t batch_size,
+                      std::uint32_t k, std::uint64_t max_batches, int kind, std::uint32_t d,
+                      float* E, float* S, std::uint64_t num_nodes, float* relE, float* relS,
+                      std::uint64_t num_rels, double lr, double eps, double* loss_sum,
+                      std::uint64_t* edges_trained) {
+  return guarded([&] {
+    const ScoreModel model = model_of(kind, d);
+    ResidentTable table = table_of(d, E, S, num_nodes, relE, relS, num_rels);
+    ResidentTable pool(1);
+    for (int i = 0; i < nparts; ++i) {
+      EmbeddingPartition p;
+      p.id = static_cast<PartitionId>(i);
+      p.dim = 1;
+      p.node_count = count[i];
+      p.embeddings.assign(count[i], 0.0f);
+      p.opt_states.assign(count[i], 0.0f);
+      pool.add_partition(std::move(p), first[i]);
+    }
+    std::vector<Edge> edges = edges_of(bucket_edges, m);
+    Rng rng(stream_seed);
+    if (shuffle)
+      for (std::size_t i = edges.size(); i > 1; --i) std::swap(edges[i - 1], edges[rng.next_below(i)]);
+    const AdagradHyper hyper{lr, eps};
+    double total = 0.0;
+    std::uint64_t done = 0, nb = 0;
+    for (std::size_t off = 0; off < edges.size() && nb < max_batches; off += batch_size, ++nb) {
+      const std::size_t cnt = std::min<std::size_t>(batch_size, edges.size() - off);
+      TrainBatch batch;
+      batch.positives.assign(edges.begin() + off, edges.begin() + off + cnt);
+      batch.negatives_per_positive = k;
+      batch.negative_dst = sample_negatives(pool, k, cnt, rng);
+      total += batch_loss(model, batch, table);
+      adagrad_step(table, batch_gradients(model, batch, table), hyper);
+      done += cnt;
+    }
+    *loss_sum = total;
+    *edges_trained = done;
+  });
+}
+
 // evaluate (train.cpp:375-412) over an all-resident table
 int ref_evaluate(int kind, std::uint32_t d, const float* E, std::uint64_t num_nodes,
                  const float* relE, std::uint64_t num_rels, const std::uint32_t* test_edges,

@@ -1,0 +1,63 @@
+// common.cuh -- error plumbing shared by the CUDA sources.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace lgd {
+
+// Exceptions mirror the reference's classes; the C ABI maps them to codes
+// (include/legend_b200.h).
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    throw cuda_error(std::string("CUDA error in ") + what + " (" + file + ":" +
+                     std::to_string(line) + "): " + cudaGetErrorString(e));
+  }
+}
+
+#define LGD_CUDA(expr) ::lgd::cuda_check((expr), #expr, __FILE__, __LINE__)
+#define LGD_LAUNCH_CHECK() ::lgd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr uint32_t kNone32 = 0xffffffffu;
+constexpr int kWarp = 32;
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+inline int bits_for(uint64_t max_value) {  // bits needed to represent values <= max_value
+  int b = 0;
+  while (b < 64 && (max_value >> b)) ++b;
+  return b < 1 ? 1 : b;
+}
+
+// Device buffer with RAII; grows but never shrinks.
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+  void reserve(size_t count) {
+    if (count <= n) return;
+    release();
+    if (count) LGD_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    n = count;
+  }
+  T* get() const { return ptr; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+}  // namespace lgd

@@ -1,0 +1,60 @@
+// train.cuh -- launch interface of the per-batch training kernels (train.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lgd {
+
+struct BatchArgs {
+  int kind;
+  uint32_t dim;
+  uint32_t k;
+  uint64_t P;                 // positives in this batch
+  const uint32_t* edges;      // P x 3 (src, rel, dst), device
+  const uint32_t* negs;       // P x k, device
+  float* theta;               // V x d embeddings
+  float* state;               // V x d Adagrad accumulators
+  float* rel_theta;           // R x d
+  float* rel_state;           // R x d
+  double lr;
+  double eps;
+  // scratch (sized for the largest batch)
+  double* w;                  // P x k softmax weights
+  double* mix;                // P x d  sum_j w_j neg_j - dst
+  float* snap;                // P x d  pre-update source rows
+  double* loss;               // P per-positive loss
+  uint32_t* node_keys;        // P x (k+2) contribution node ids (dst, negs, src)
+  uint32_t* rel_keys;         // P relation ids
+  const uint32_t* iota;       // 0..P*(k+2)-1
+  uint32_t* skeys;            // sorted keys
+  uint32_t* svals;            // sorted contribution indices
+  void* sort_temp;
+  size_t sort_temp_bytes;
+  double* part_first;         // chunks x d
+  double* part_last;          // chunks x d
+  uint8_t* chunk_flags;       // chunks
+  unsigned long long* counters;  // [0] unique nodes, [1] unique rels (accumulated)
+  double* batch_loss_out;     // one double: this batch's loss
+  int node_key_bits;
+  int rel_key_bits;
+  // gradient-only mode (operator-level batch_gradients): dense V x d / R x d
+  double* grad_nodes;
+  uint8_t* grad_node_flag;
+  double* grad_rels;
+  uint8_t* grad_rel_flag;
+  int sm_count;
+};
+
+struct BatchEvents {  // optional per-phase timing (profiling mode)
+  cudaEvent_t ev[5];
+  bool enabled;
+};
+
+size_t batch_sort_temp_bytes(uint64_t max_items);
+size_t score_smem_bytes(uint32_t dim, uint32_t k);
+// K3 -> loss reduce -> sort -> K4 (pass 1, 2) -> relation path.
+void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev);
+
+}  // namespace lgd

@@ -1,0 +1,47 @@
+"""The drop-in boundary: liblegend_b200.so loads, exports every entry point
+include/legend_b200.h declares, and refuses to run without a GPU (no CPU
+fallback).  CPU only."""
+import ctypes
+import os
+import re
+
+import pytest
+from conftest import ROOT
+
+import paper_2505_09258_b200 as lgd
+from paper_2505_09258_b200 import legend
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "legend_b200.h")).read()
+    return sorted(set(re.findall(r"\b(lgd_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(legend.LIB_PATH)
+    names = declared_symbols()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    blob = open(legend.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(lgd.RuntimeFailure):
+        lgd.Trainer(lgd.ScoreModel("distmult", 16))
+    with pytest.raises(lgd.RuntimeFailure):
+        lgd.rng_below(1, 10, 5)
+
+
+def test_argument_validation_before_device():
+    with pytest.raises(lgd.InvalidArgument):
+        lgd.Trainer(lgd.ScoreModel("complex", 7))
+    with pytest.raises(lgd.InvalidArgument):
+        lgd.Trainer(lgd.ScoreModel("dot", 0))

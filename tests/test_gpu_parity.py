@@ -1,0 +1,262 @@
+"""CUDA path vs the oracle (C restatement of the reference) and the golden
+vectors generated from the reference library.  Runs on a B200 (-m gpu).
+
+Tolerances (stated here):
+  * indices -- shuffled order, negative ids, partition plan, eval candidates,
+    unique-row counts: bit-exact;
+  * store init: bit-exact (integer-seeded f32);
+  * per-batch loss / epoch loss_sum: |rel| <= 1e-12 (the kernels compute in
+    FP64 like the reference; only the dot-product summation order and
+    exp/log ulps differ);
+  * gradients: |rel| <= 1e-10 per row norm;
+  * embeddings / Adagrad state after training: relative Frobenius <= 1e-7
+    per partition and >= 99% of elements bit-identical.
+"""
+import numpy as np
+import pytest
+from conftest import golden
+
+import paper_2505_09258_b200 as lgd
+
+pytestmark = pytest.mark.gpu
+KINDS = ["dot", "distmult", "complex"]
+
+
+def frob(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def assert_tables_close(got, want, what):
+    assert got.shape == want.shape, what
+    assert frob(got, want) <= 1e-7, (what, frob(got, want))
+    same = np.mean(got == want)
+    assert same >= 0.99, (what, same)
+
+
+def make_trainer(kind, d, V, R, edges, n, k=16, batch=100000, seed=42, shuffle=True, lr=0.1):
+    opts = lgd.TrainOptions(learning_rate=lr, batch_size=batch, negatives=k, shuffle=shuffle,
+                            seed=seed)
+    t = lgd.Trainer(lgd.ScoreModel(kind, d), opts)
+    t.set_graph(edges, V, R)
+    t.make_partition_plan(n)
+    return t
+
+
+# ------------------------------------------------------------------ K2 / K1
+def test_rng_below_rejection_path_matches_golden():
+    g = golden("rng")
+    vals, used = lgd.rng_below(int(g["reject_seed"]), 2**63 + 1, 5000, skip=int(g["reject_skip"]))
+    assert np.array_equal(vals, g["reject_vals"])
+    assert used == int(g["reject_used"])
+
+
+@pytest.mark.parametrize("bound", [1, 2, 7, 1000, 7_800_000, 2**32 - 1, 2**40 + 3])
+def test_rng_below_matches_oracle(oracle, bound):
+    for count, skip in ((1, 0), (1000, 3), (300_000, 12345)):
+        vals, used = lgd.rng_below(77, bound, count, skip=skip)
+        want, wused = oracle.rng_below(77, np.full(count, bound, np.uint64), skip=skip)
+        assert np.array_equal(vals, want)
+        assert used == wused
+
+
+def test_sample_negatives_match_golden():
+    g = golden("sampler")
+    s2, _ = lgd.sample_negatives(g["first2"], g["count2"], 4, 2500, 4242)
+    assert np.array_equal(s2, g["s2"])
+    s3, used = lgd.sample_negatives(g["first3"], g["count3"], 16, 5000, 99, skip=12345)
+    assert np.array_equal(s3, g["s3"])
+    assert used == 16 * 5000
+
+
+def test_sample_negatives_large_matches_oracle(oracle):
+    # a Twitter-shaped pool (3 x 2.6M resident rows), one bucket's worth of draws
+    first = [2_600_000 * 2, 2_600_000 * 7, 2_600_000 * 11]
+    count = [2_600_000, 2_600_000, 2_600_000]
+    got, used = lgd.sample_negatives(first, count, 16, 1_000_000, 123456789, skip=5_099_999)
+    want = oracle.sample_negatives(first, count, 16, 1_000_000, 123456789, skip=5_099_999)
+    assert used == 16_000_000
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 10, 1000, 65_537, 1_000_000])
+def test_shuffle_permutation_matches_oracle(oracle, m):
+    seed = 0x1234567 + m
+    got, used = lgd.shuffle_permutation(seed, m)
+    want, wused = oracle.shuffle_perm(seed, m)
+    assert np.array_equal(got, want)
+    assert used == wused
+
+
+def test_shuffle_permutation_twitter_bucket(oracle):
+    m = 5_100_000  # mean Twitter bucket (1.3B edges / 256 buckets)
+    got, used = lgd.shuffle_permutation(987654321, m)
+    want, _ = oracle.shuffle_perm(987654321, m)
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.sort(got), np.arange(m, dtype=np.uint32))
+
+
+# ----------------------------------------------------- loader / store init
+def test_partition_plan_matches_golden():
+    g = golden("partition")
+    t = make_trainer("dot", 4, int(g["V"]), 3, g["edges"], int(g["n"]))
+    offsets, order = t.make_partition_plan(int(g["n"]), want_edge_order=True)
+    assert np.array_equal(offsets, g["offsets"])
+    assert np.array_equal(order, g["edge_order"])
+
+
+def test_store_init_matches_golden():
+    g = golden("store")
+    V, R, n, d = int(g["V"]), int(g["R"]), int(g["n"]), int(g["dim"])
+    edges = np.array([[0, 0, 1]], np.uint32)
+    t = make_trainer("distmult", d, V, R, edges, n)
+    t.init_store(int(g["seed"]))
+    E, S = t.tables()
+    rE, rS = t.get_relations()
+    assert np.array_equal(E, g["E"]) and not S.any()
+    assert np.array_equal(rE, g["relE"]) and not rS.any()
+
+
+# ------------------------------------------------------ K3 / K4 one batch
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("d", [6, 12])
+def test_batch_matches_golden(kind, d):
+    g = golden(f"batch_{kind}_d{d}")
+    V, R, k = g["E0"].shape[0], g["rE0"].shape[0], int(g["k"])
+    t = make_trainer(kind, d, V, R if kind != "dot" else 0, g["edges"], 1, k=k)
+    t.load_tables(g["E0"], g["S0"])
+    if kind != "dot":
+        t.set_relations(g["rE0"], g["rS0"])
+    gr = t.batch_gradients(g["edges"], g["negs"])
+    assert gr["loss"] == pytest.approx(float(g["loss"]), rel=1e-12)
+    assert np.array_equal(gr["node_ids"], g["node_ids"])
+    np.testing.assert_allclose(gr["node_grads"], g["node_grads"], rtol=1e-10, atol=1e-14)
+    if kind != "dot":
+        assert np.array_equal(gr["rel_ids"], g["rel_ids"])
+        np.testing.assert_allclose(gr["rel_grads"], g["rel_grads"], rtol=1e-10, atol=1e-14)
+    res = t.train_batch(g["edges"], g["negs"])
+    assert res["loss"] == pytest.approx(float(g["loss"]), rel=1e-12)
+    assert res["nodes"] == len(g["node_ids"])
+    E, S = t.tables()
+    assert_tables_close(E, g["E1"], "E")
+    assert_tables_close(S, g["S1"], "S")
+    if kind != "dot":
+        rE, rS = t.get_relations()
+        assert_tables_close(rE, g["rE1"], "relE")
+        assert_tables_close(rS, g["rS1"], "relS")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("d,k,P", [(100, 16, 3000), (64, 5, 777), (128, 40, 500), (32, 1, 64)])
+def test_batch_matches_oracle_wide(oracle, kind, d, k, P):
+    rng = np.random.default_rng(d * 1000 + k)
+    V, R = 5000, 17
+    E0 = rng.uniform(-0.05, 0.05, (V, d)).astype(np.float32)
+    S0 = rng.uniform(0, 0.01, (V, d)).astype(np.float32)
+    rE0 = rng.uniform(-0.05, 0.05, (R, d)).astype(np.float32)
+    rS0 = np.zeros((R, d), np.float32)
+    rels = rng.integers(0, R, P) if kind != "dot" else np.full(P, 0xFFFFFFFF)
+    # a hub node to exercise long segments (chunk-spanning reductions)
+    src = np.where(rng.random(P) < 0.3, 17, rng.integers(0, V, P))
+    edges = np.stack([src, rels, rng.integers(0, V, P)], 1).astype(np.uint32)
+    negs = rng.integers(0, V, P * k).astype(np.uint32)
+    t = make_trainer(kind, d, V, R if kind != "dot" else 0, edges, 1, k=k)
+    t.load_tables(E0, S0)
+    if kind != "dot":
+        t.set_relations(rE0, rS0)
+    E, S, rE, rS = E0.copy(), S0.copy(), rE0.copy(), rS0.copy()
+    want = oracle.batch(kind, E, S, rE if kind != "dot" else None, rS if kind != "dot" else None,
+                        edges, negs, k)
+    got = t.train_batch(edges, negs)
+    assert got["loss"] == pytest.approx(want["loss"], rel=1e-12)
+    assert got["nodes"] == want["nodes"] and got["rels"] == want["rels"]
+    Eg, Sg = t.tables()
+    assert_tables_close(Eg, E, "E")
+    assert_tables_close(Sg, S, "S")
+    if kind != "dot":
+        rEg, rSg = t.get_relations()
+        assert_tables_close(rEg, rE, "relE")
+
+
+# ------------------------------------------------------------ full epochs
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n", [1, 4])
+def test_epoch_matches_golden(kind, n):
+    g = golden(f"epoch_{kind}_n{n}")
+    V, R, d = int(g["V"]), int(g["R"]), int(g["d"])
+    t = make_trainer(kind, d, V, R if kind != "dot" else 0, g["edges"], n, k=int(g["k"]),
+                     batch=int(g["batch"]), seed=int(g["seed"]))
+    t.init_store(int(g["store_seed"]))
+    res = t.run_epoch(0)
+    assert res.edges_trained == int(g["edges_trained"])
+    assert res.buckets_trained == int(g["buckets_trained"])
+    assert res.batches == len(g["batch_loss"])
+    assert res.unique_nodes == int(g["batch_nodes"].sum())  # bit-exact index work
+    assert res.unique_rels == int(g["batch_rels"].sum())
+    assert res.loss_sum == pytest.approx(float(g["loss_sum"]), rel=1e-12)
+    E, S = t.tables()
+    assert_tables_close(E, g["E"], "E")
+    assert_tables_close(S, g["S"], "S")
+    if kind != "dot":
+        rE, rS = t.get_relations()
+        assert_tables_close(rE, g["relE"], "relE")
+        assert_tables_close(rS, g["relS"], "relS")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_evaluate_matches_golden(kind):
+    g = golden(f"eval_{kind}")
+    E, rE, test = g["E"], g["relE"], g["test"]
+    R = rE.shape[0] if kind != "dot" else 0
+    t = make_trainer(kind, E.shape[1], E.shape[0], R, test, 1)
+    t.load_tables(E, np.zeros_like(E))
+    if R:
+        t.set_relations(rE, np.zeros_like(rE))
+    mrr, hits = t.evaluate(test, lgd.EvalOptions(hits_k=10, num_candidates=999,
+                                                 seed=int(g["seed"])))
+    assert mrr == pytest.approx(float(g["mrr"]), rel=1e-12)
+    assert hits == pytest.approx(float(g["hits"]), abs=1e-12)
+
+
+# ------------------------------------------- configs[0]: FB15k-shaped KG
+def test_fb15k_shaped_distmult_epoch_matches_oracle(oracle):
+    """BASELINE configs[0]: 15k nodes, 1,345 relations, 592k edges, DistMult
+    d=100, 1 partition, k=16, P=1e5 -- full epoch vs the restatement."""
+    rng = np.random.default_rng(15)
+    V, R, Ecnt, d = 15000, 1345, 592_000, 100
+    edges = np.stack([rng.integers(0, V, Ecnt), rng.integers(0, R, Ecnt),
+                      rng.integers(0, V, Ecnt)], 1).astype(np.uint32)
+    t = make_trainer("distmult", d, V, R, edges, 1, k=16, batch=100000, seed=42)
+    t.init_store(42)
+    res = t.run_epoch(0)
+    E, S, rE, rS = oracle.store_init(1, V, d, R, 42)
+    from oracle.oracle import single_state_plan
+    want = oracle.run_epoch(edges, V, R, 1, single_state_plan(1), "distmult", E, S, rE, rS,
+                            dim=d, batch_size=100000, k=16, seed=42, dumps=True)
+    assert res.edges_trained == want["edges_trained"] == Ecnt
+    assert res.unique_nodes == int(want["batch_nodes"].sum())
+    assert res.loss_sum == pytest.approx(want["loss_sum"], rel=1e-12)
+    Eg, Sg = t.tables()
+    assert_tables_close(Eg, E, "E")
+    assert_tables_close(Sg, S, "S")
+    rEg, rSg = t.get_relations()
+    assert_tables_close(rEg, rE, "relE")
+    assert_tables_close(rSg, rS, "relS")
+
+
+# ------------------------------------------------------- error behaviour
+def test_errors_follow_reference_classes():
+    edges = np.array([[0, 0, 1], [1, 0, 2]], np.uint32)
+    t = make_trainer("distmult", 8, 10, 0, np.array([[0, 0xFFFFFFFF, 1]], np.uint32), 1)
+    t.init_store(1)
+    with pytest.raises(lgd.InvalidArgument):  # typed model, no relations (pipeline.cpp:228)
+        t.run_epoch(0)
+    t2 = make_trainer("distmult", 8, 10, 2, edges, 1, k=2)
+    t2.init_store(1)
+    with pytest.raises(lgd.OutOfRange):  # node not resident (train.cpp:157)
+        t2.train_batch(np.array([[0, 0, 99]], np.uint32), np.array([1, 2], np.uint32))
+    with pytest.raises(lgd.InvalidArgument):  # missing relation id (train.cpp:209-211)
+        t2.train_batch(np.array([[0, 0xFFFFFFFF, 1]], np.uint32), np.array([1, 2], np.uint32))
+    with pytest.raises(lgd.InvalidArgument):
+        make_trainer("dot", 8, 10, 0, edges, 11)  # n > V (graph.cpp:122)
