@@ -4,11 +4,11 @@ Hot path: hand-written sm_100a CUDA in liblegend_b200.so behind the C ABI of
 include/legend_b200.h; this package is the thin Python face of that ABI.
 """
 from .legend import (EpochResult, EvalOptions, InvalidArgument, IterationPlan, LogicError,
-                     OutOfRange, RuntimeFailure, ScoreModel, Trainer, TrainOptions, library,
+                     OutOfRange, PinnedArray, RuntimeFailure, ScoreModel, Trainer, TrainOptions, library,
                      plan_iteration_order, plan_to_json, rng_below, sample_negatives,
                      shuffle_permutation, single_state_plan)
 
 __all__ = ["EpochResult", "EvalOptions", "InvalidArgument", "IterationPlan", "LogicError",
-           "OutOfRange", "RuntimeFailure", "ScoreModel", "Trainer", "TrainOptions", "library",
+           "OutOfRange", "PinnedArray", "RuntimeFailure", "ScoreModel", "Trainer", "TrainOptions", "library",
            "plan_iteration_order", "plan_to_json", "rng_below", "sample_negatives",
            "shuffle_permutation", "single_state_plan"]
