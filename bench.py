@@ -37,7 +37,7 @@ CONFIGS = {
     "fb15k": dict(workload="FB15k-shaped synthetic KG, DistMult d=100, 1 partition",
                   nodes=15_000, edges=592_000, rels=1345, model="distmult", dim=100, n=1),
 }
-K_NEG, BATCH, LR, SEED, ALPHA, GRAPH_SEED = 16, 100_000, 0.1, 42, 2.1, 20250509
+K_NEG, BATCH, LR, SEED, ALPHA, GRAPH_SEED = 16, 100_000, 0.1, 42, 2.3, 20250509
 REF_SAMPLE_POSITIVES = 25_000  # positives per reference step (bounded CPU sample)
 
 

@@ -106,8 +106,10 @@ struct lgd_context {
   uint32_t k_cap = 0;
   DevBuf<double> w, mix, loss, part_first, part_last;
   DevBuf<float> snap;
-  DevBuf<uint32_t> node_keys, rel_keys, iota, skeys, svals;
+  DevBuf<uint32_t> node_keys, node_vals, rel_keys, iota, skeys, svals;
   DevBuf<uint8_t> chunk_flags;
+  DevBuf<uint32_t> span_list;
+  DevBuf<unsigned int> span_count;
   DevBuf<unsigned char> sort_temp;
   DevBuf<unsigned long long> counters;
   DevBuf<double> batch_losses;
@@ -172,6 +174,7 @@ struct lgd_context {
     snap.reserve(P * dim);
     loss.reserve(P);
     node_keys.reserve(items);
+    node_vals.reserve(items);
     rel_keys.reserve(P);
     skeys.reserve(items);
     svals.reserve(items);
@@ -179,6 +182,8 @@ struct lgd_context {
     part_first.reserve(chunks * dim);
     part_last.reserve(chunks * dim);
     chunk_flags.reserve(chunks);
+    span_list.reserve(chunks);
+    span_count.reserve(1);
     sort_temp.reserve(batch_sort_temp_bytes(items));
     if (iota.n < items) {
       iota.reserve(items);
@@ -210,6 +215,9 @@ struct lgd_context {
     a.snap = snap.get();
     a.loss = loss.get();
     a.node_keys = node_keys.get();
+    a.node_vals = node_vals.get();
+    a.slot_bits = bits_for(a.k + 1);
+    if ((P << a.slot_bits) >> 32) throw std::invalid_argument("batch too large for 32-bit payloads");
     a.rel_keys = rel_keys.get();
     a.iota = iota.get();
     a.skeys = skeys.get();
@@ -219,6 +227,8 @@ struct lgd_context {
     a.part_first = part_first.get();
     a.part_last = part_last.get();
     a.chunk_flags = chunk_flags.get();
+    a.span_list = span_list.get();
+    a.span_count = span_count.get();
     a.counters = counters.get();
     a.batch_loss_out = loss_out;
     a.node_key_bits = bits_for(V ? V - 1 : 0);

@@ -1,24 +1,31 @@
 // train.cu -- the per-batch hot path: batch_loss + batch_gradients +
 // adagrad_step (train.cpp:217-363) as
-//   K3 score_kernel    warp per positive; the 2+k+t embedding rows are pulled
-//                      into shared memory by TMA bulk copies
-//                      (cp.async.bulk, one per row, mbarrier-tracked, double
-//                      buffered across the warp's positives); FP64 math
-//                      exactly as the reference orders it per element,
-//                      warp-shuffle reductions for the dot products.
+//
+//   K3 score_kernel    warp per positive.  The 2+k+t embedding rows land in
+//                      shared memory by TMA bulk copies (cp.async.bulk, one
+//                      per row, mbarrier-tracked), double buffered, with the
+//                      row ids fetched two positives ahead.  Lane j computes
+//                      the dot product of negative j (lane k: the positive)
+//                      sequentially over the dimension -- the reference's
+//                      own FP64 summation order (train.cpp:246-264) -- then
+//                      the softmax weights, the loss and mix = sum_j w_j neg_j
+//                      - dst (train.cpp:306-323) in the reference order.
 //   sort               CUB onesweep radix sort of the P(k+2) contribution
-//                      node ids (stable, so each node's contributions stay in
-//                      the reference's std::map visit order: positive
-//                      ascending, then dst, negatives j ascending, src).
-//   K4 segment passes  warp per 32 sorted contributions: sum each node's
-//                      contributions in order (FP64), then one Adagrad row
-//                      update (train.cpp:342-354) per unique node -- a
-//                      sort-by-node segmented reduction, no atomics on rows.
-//                      Segments that cross a 32-item chunk are finished by a
-//                      second pass from per-chunk partial sums.
+//                      node ids.  Stable, so every node's contributions stay
+//                      in the reference's std::map visit order (positive
+//                      ascending; dst, negatives j ascending, src).
+//   K4 segment_pass1   warp per 32 sorted contributions.  The chunk's pieces
+//                      (node segments cut at chunk edges) are processed four
+//                      at a time, one 8-lane group each, in lockstep: the
+//                      contributions are summed in order in FP64 and complete
+//                      segments get their Adagrad row update (train.cpp:
+//                      342-354) right away -- a sort-by-node segmented
+//                      reduction, no atomics on rows.
+//   K4 segment_pass2   segments that cross chunks (hubs) are finished by one
+//                      block each from the per-chunk partial sums.
 //   relation path      the same segmented reduction over relation ids.
-// All FP64 expressions are compiled with -fmad=false so products and sums
-// round exactly like the reference's unfused x86-64 double arithmetic.
+// FP64 expressions are compiled with -fmad=false so products and sums round
+// exactly like the reference's unfused x86-64 double arithmetic.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -30,8 +37,10 @@ namespace {
 
 constexpr int kScoreWarps = 4;
 constexpr int kSegThreads = 256;
+constexpr int kPass2Threads = 256;
 constexpr uint8_t kNoHead = 1;
 constexpr uint8_t kContOut = 2;
+constexpr int kGroup = 8;  // lanes per segment group in K4
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -71,244 +80,189 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  return v;
-}
-
-// --------------------------------------------------- lane element mapping
-// Dot / DistMult: lane owns elements lane + 32c (c < NC).
-// ComplEx (half-split encoding, train.hpp:17-18): lane owns real index
-// j = lane + 32c and its imaginary partner j + h; slots c (re) and NC + c (im).
-template <int KIND, int NC>
-struct Map {
-  static constexpr int NE = KIND == 2 ? 2 * NC : NC;
-  __device__ __forceinline__ static int idx(int e, int lane, uint32_t h) {
-    if (KIND == 2) return e < NC ? lane + 32 * e : lane + 32 * (e - NC) + (int)h;
-    return lane + 32 * e;
+// ---------------------------------------------------------------- K3 score
+// Shared memory per warp: ids[32] u32, rows[(k+3) x dpad] f32 (src, rel,
+// dst, negatives), ir1[dpad] f64, f[k+1] f64, e[k] f64.  One row buffer per
+// warp keeps the footprint at ~9 KB so 24 warps share an SM; the next
+// positive's row ids are fetched while the current one computes.
+struct ScoreSmem {
+  uint32_t dpad, k, nrows;
+  size_t ids_off, rows_off, ir1_off, f_off, e_off, warp_bytes;
+  __host__ __device__ ScoreSmem(uint32_t d, uint32_t kk) {
+    dpad = (d + 3) & ~3u;
+    k = kk;
+    nrows = kk + 3;
+    const uint32_t nid = (nrows + 31) & ~31u;
+    ids_off = 0;
+    rows_off = (nid * 4 + 15) & ~size_t(15);
+    ir1_off = rows_off + size_t(nrows) * dpad * 4;
+    f_off = ir1_off + size_t(dpad) * 8;
+    e_off = f_off + size_t(kk + 1) * 8;
+    warp_bytes = (e_off + size_t(kk) * 8 + 15) & ~size_t(15);
   }
-  __device__ __forceinline__ static bool ok(int e, int lane, uint32_t d, uint32_t h) {
-    if (KIND == 2) return lane + 32 * (e < NC ? e : e - NC) < (int)h;
-    return lane + 32 * e < (int)d;
-  }
+  __host__ __device__ size_t block_bytes() const { return 16 * kScoreWarps + kScoreWarps * warp_bytes; }
 };
 
-// IR1 = s (x) r (combine_src_rel, train.cpp:39-60) for the lane's elements.
-template <int KIND, int NC>
-__device__ __forceinline__ void combine(const float* s, const float* r, int lane, uint32_t d,
-                                        uint32_t h, double* x) {
-  using M = Map<KIND, NC>;
-  if (KIND == 2) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      x[c] = 0.0;
-      x[c + NC] = 0.0;
-      if (M::ok(c, lane, d, h)) {
-        const int j = lane + 32 * c;
-        const double sr = s[j], si = s[j + h];
-        const double rr = r[j], ri = r[j + h];
-        x[c] = sr * rr - si * ri;
-        x[c + NC] = sr * ri + si * rr;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < NC; ++e) {
-      x[e] = 0.0;
-      if (M::ok(e, lane, d, h)) {
-        const int i = lane + 32 * e;
-        x[e] = KIND == 0 ? (double)s[i] : (double)s[i] * (double)r[i];
-      }
-    }
-  }
-}
-
-// g += adj_other(mix) (adjoint_combine, train.cpp:65-85) for the lane's elements.
-template <int KIND, int NC>
-__device__ __forceinline__ void adjoint_add(const float* other, const double* mixrow, int lane,
-                                            uint32_t d, uint32_t h, double* g) {
-  using M = Map<KIND, NC>;
-  if (KIND == 2) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      if (M::ok(c, lane, d, h)) {
-        const int j = lane + 32 * c;
-        const double orr = other[j], ori = other[j + h];
-        const double mr = mixrow[j], mi = mixrow[j + h];
-        g[c] += orr * mr + ori * mi;
-        g[c + NC] += orr * mi - ori * mr;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < NC; ++e) {
-      if (M::ok(e, lane, d, h)) {
-        const int i = lane + 32 * e;
-        if (KIND == 0) {
-          g[e] += mixrow[i];
-        } else {
-          g[e] += (double)other[i] * mixrow[i];
-        }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------- K3 score
-// Shared memory per warp: 2 row buffers of (k+3) x dpad floats (src, rel,
-// dst, k negatives), then f_j and e_j scratch (k doubles each).
-template <int KIND, int NC, bool TMA>
-__global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, uint32_t dpad) {
+template <int KIND>
+__global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, int use_tma) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using M = Map<KIND, NC>;
-  constexpr int NE = M::NE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t k = a.k, d = a.dim, h = d / 2;
   const bool typed = KIND != 0;
-  const uint32_t nrows = k + 3;
-  const size_t buf_floats = (size_t)nrows * dpad;
-  const size_t warp_bytes = 2 * buf_floats * sizeof(float) + 2 * (size_t)k * sizeof(double);
+  const ScoreSmem L(d, k);
+  const uint32_t dpad = L.dpad, nrows = L.nrows;
+  const uint32_t nid = (nrows + 31) & ~31u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-  float* rows = reinterpret_cast<float*>(smem + 16 * kScoreWarps + warp * warp_bytes);
-  double* fj = reinterpret_cast<double*>(rows + 2 * buf_floats);
-  double* ej = fj + k;
+  unsigned char* wbase = smem + 16 * kScoreWarps + warp * L.warp_bytes;
+  uint32_t* ids = reinterpret_cast<uint32_t*>(wbase + L.ids_off);
+  float* rows = reinterpret_cast<float*>(wbase + L.rows_off);
+  double* ir1 = reinterpret_cast<double*>(wbase + L.ir1_off);
+  double* fbuf = reinterpret_cast<double*>(wbase + L.f_off);
+  double* ebuf = reinterpret_cast<double*>(wbase + L.e_off);
+  const size_t buf_floats = size_t(nrows) * dpad;
+  const bool tma = use_tma && nrows <= 32;
 
-  if (TMA) {
+  if (tma) {
     if (lane == 0) {
       mbar_init(bars, 1);
-      mbar_init(bars + 1, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
   }
-  const uint32_t row_bytes = d * sizeof(float);
+  const uint32_t row_bytes = d * 4;
   const uint32_t tx_bytes = (typed ? nrows : nrows - 1) * row_bytes;
 
-  auto issue = [&](uint64_t p, int b) {
+  // row r of positive p: 0 src, 1 rel, 2 dst, 3+j negative j
+  auto row_id = [&](uint64_t p, uint32_t r) -> uint32_t {
+    if (r < 3) return a.edges[3 * p + r];
+    return a.negs[p * k + (r - 3)];
+  };
+  auto row_src = [&](uint32_t r, uint32_t id) -> const float* {
+    return (r == 1 ? a.rel_theta : a.theta) + size_t(id) * d;
+  };
+  auto issue = [&](uint32_t my_id, int b) {  // TMA path: lane r owns row r's id
+    if (lane < (int)nrows) ids[b * nid + lane] = my_id;
+    if (lane == 0) mbar_arrive_expect_tx(bars + b, tx_bytes);
+    __syncwarp();
+    if (lane < (int)nrows && (typed || lane != 1))
+      bulk_g2s(rows + b * buf_floats + lane * dpad, row_src(lane, my_id), row_bytes, bars + b);
+  };
+  auto load_sync = [&](uint64_t p, int b) {  // generic path: plain loads
+    for (uint32_t r = lane; r < nrows; r += 32) ids[b * nid + r] = row_id(p, r);
+    __syncwarp();
     float* base = rows + b * buf_floats;
-    const uint32_t s = a.edges[3 * p], r = a.edges[3 * p + 1], t = a.edges[3 * p + 2];
-    if (TMA) {
-      if (lane == 0) mbar_arrive_expect_tx(bars + b, tx_bytes);
-      __syncwarp();
-      for (uint32_t row = lane; row < nrows; row += 32) {
-        const float* src;
-        if (row == 0) {
-          src = a.theta + (size_t)s * d;
-        } else if (row == 1) {
-          if (!typed) continue;
-          src = a.rel_theta + (size_t)r * d;
-        } else if (row == 2) {
-          src = a.theta + (size_t)t * d;
-        } else {
-          src = a.theta + (size_t)a.negs[p * k + (row - 3)] * d;
-        }
-        bulk_g2s(base + row * dpad, src, row_bytes, bars + b);
-      }
-    } else {
-      for (uint32_t row = 0; row < nrows; ++row) {
-        const float* src;
-        if (row == 0) {
-          src = a.theta + (size_t)s * d;
-        } else if (row == 1) {
-          if (!typed) continue;
-          src = a.rel_theta + (size_t)r * d;
-        } else if (row == 2) {
-          src = a.theta + (size_t)t * d;
-        } else {
-          src = a.theta + (size_t)a.negs[p * k + (row - 3)] * d;
-        }
-        for (uint32_t i = lane; i < d; i += 32) base[row * dpad + i] = src[i];
-      }
+    for (uint32_t r = 0; r < nrows; ++r) {
+      if (r == 1 && !typed) continue;
+      const float* src = row_src(r, ids[b * nid + r]);
+      for (uint32_t i = lane; i < d; i += 32) base[r * dpad + i] = src[i];
     }
+    __syncwarp();
   };
 
   const uint64_t nwarps = (uint64_t)gridDim.x * kScoreWarps;
   uint64_t p = (uint64_t)blockIdx.x * kScoreWarps + warp;
-  uint32_t phase0 = 0, phase1 = 0;
-  int b = 0;
-  if (p < a.P) issue(p, 0);
-  for (; p < a.P; p += nwarps, b ^= 1) {
-    const uint64_t pn = p + nwarps;
-    if (pn < a.P) issue(pn, b ^ 1);
-    if (TMA) {
-      uint64_t* bar = bars + b;
-      const uint32_t ph = b ? phase1 : phase0;
-      while (!mbar_try_wait(bar, ph)) {
+  uint32_t phase = 0;
+  uint32_t id_next = 0;
+  const int b = 0;
+  if (tma && p < a.P) {
+    const uint32_t id0 = lane < (int)nrows ? row_id(p, lane) : 0;
+    issue(id0, 0);
+    const uint64_t p1 = p + nwarps;
+    if (p1 < a.P && lane < (int)nrows) id_next = row_id(p1, lane);
+  }
+  for (; p < a.P; p += nwarps) {
+    const uint64_t pn = p + nwarps, pnn = pn + nwarps;
+    if (tma) {
+      while (!mbar_try_wait(bars, phase)) {
       }
-      if (b) {
-        phase1 ^= 1;
-      } else {
-        phase0 ^= 1;
-      }
+      phase ^= 1;
+    } else {
+      load_sync(p, b);
     }
     __syncwarp();
     const float* R = rows + b * buf_floats;
     const float* srow = R;
     const float* rrow = R + dpad;
     const float* drow = R + 2 * dpad;
+    const uint32_t* pid = ids + b * nid;
 
-    double x[NE];
-    combine<KIND, NC>(srow, rrow, lane, d, h, x);
-    // positive score (train.cpp:246-252)
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < NE; ++e)
-      if (M::ok(e, lane, d, h)) acc += x[e] * (double)drow[M::idx(e, lane, h)];
-    const double pos = warp_sum(acc);
-    // negative scores (train.cpp:256-264)
-    for (uint32_t j = 0; j < k; ++j) {
-      const float* nrow = R + (3 + j) * dpad;
+    // IR1 = s (x) r (combine_src_rel, train.cpp:39-60) into shared memory
+    if (KIND == 2) {
+      for (uint32_t j = lane; j < h; j += 32) {
+        const double sr = srow[j], si = srow[j + h];
+        const double rr = rrow[j], ri = rrow[j + h];
+        ir1[j] = sr * rr - si * ri;
+        ir1[j + h] = sr * ri + si * rr;
+      }
+    } else {
+      for (uint32_t i = lane; i < d; i += 32)
+        ir1[i] = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
+    }
+    for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
+    __syncwarp();
+    // scores: lane q < k -> negative q, lane k -> the positive; sequential
+    // over the dimension exactly as train.cpp:246-264
+    for (uint32_t q = lane; q <= k; q += 32) {
+      const float* row = q < k ? R + (3 + q) * dpad : drow;
       double f = 0.0;
-#pragma unroll
-      for (int e = 0; e < NE; ++e)
-        if (M::ok(e, lane, d, h)) f += x[e] * (double)nrow[M::idx(e, lane, h)];
-      f = warp_sum(f);
-      if (lane == (int)(j & 31)) fj[j] = f;
+      if ((d & 3) == 0) {
+        for (uint32_t i = 0; i < d; i += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + i);
+          const double2 x0 = *reinterpret_cast<const double2*>(ir1 + i);
+          const double2 x1 = *reinterpret_cast<const double2*>(ir1 + i + 2);
+          f += x0.x * (double)v.x;
+          f += x0.y * (double)v.y;
+          f += x1.x * (double)v.z;
+          f += x1.y * (double)v.w;
+        }
+      } else {
+        for (uint32_t i = 0; i < d; ++i) f += ir1[i] * (double)row[i];
+      }
+      fbuf[q] = f;
     }
     __syncwarp();
     double row_max = -INFINITY;
     for (uint32_t j = 0; j < k; ++j) {
-      const double f = fj[j];
+      const double f = fbuf[j];
       row_max = row_max < f ? f : row_max;  // std::max(row_max, f)
     }
-    for (uint32_t j = lane; j < k; j += 32) ej[j] = exp(fj[j] - row_max);  // IR3
+    for (uint32_t j = lane; j < k; j += 32) ebuf[j] = exp(fbuf[j] - row_max);  // IR3
     __syncwarp();
     double sum = 0.0;
-    for (uint32_t j = 0; j < k; ++j) sum += ej[j];  // sequential j, every lane
+    for (uint32_t j = 0; j < k; ++j) sum += ebuf[j];  // sequential j (train.cpp:266-270)
     const double inv_sum = 1.0 / sum;
-    for (uint32_t j = lane; j < k; j += 32) a.w[p * k + j] = ej[j] * inv_sum;
-    if (lane == 0) a.loss[p] = -(pos - (row_max + log(sum)));  // train.cpp:274
+    for (uint32_t j = lane; j < k; j += 32) a.w[p * k + j] = ebuf[j] * inv_sum;
+    if (lane == 0) a.loss[p] = -(fbuf[k] - (row_max + log(sum)));  // train.cpp:274
 
-    // mix = sum_j w_j neg_j - dst (train.cpp:306-323)
-    double mx[NE];
-#pragma unroll
-    for (int e = 0; e < NE; ++e)
-      mx[e] = M::ok(e, lane, d, h) ? -(double)drow[M::idx(e, lane, h)] : 0.0;
-    for (uint32_t j = 0; j < k; ++j) {
-      const float* nrow = R + (3 + j) * dpad;
-      const double w = ej[j] * inv_sum;
-#pragma unroll
-      for (int e = 0; e < NE; ++e)
-        if (M::ok(e, lane, d, h)) mx[e] += w * (double)nrow[M::idx(e, lane, h)];
+    // mix = sum_j w_j neg_j - dst, j ascending (train.cpp:306-323)
+    for (uint32_t i = lane; i < d; i += 32) {
+      double mx = -(double)drow[i];
+      for (uint32_t j = 0; j < k; ++j) mx += (ebuf[j] * inv_sum) * (double)R[(3 + j) * dpad + i];
+      a.mix[p * d + i] = mx;
     }
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      if (M::ok(e, lane, d, h)) {
-        const int i = M::idx(e, lane, h);
-        a.mix[p * d + i] = mx[e];
-        a.snap[p * d + i] = srow[i];
+    // contribution keys in the reference's visit order: dst, negatives, src
+    const uint64_t kb = p * (k + 2);
+    for (uint32_t r = lane; r < nrows; r += 32) {
+      const uint32_t id = pid[r];
+      const uint32_t pv = (uint32_t)p << a.slot_bits;  // payload: positive, slot
+      if (r == 0) {
+        a.node_keys[kb + k + 1] = id;
+        a.node_vals[kb + k + 1] = pv | (k + 1);
+      } else if (r == 1) {
+        if (typed) a.rel_keys[p] = id;
+      } else if (r == 2) {
+        a.node_keys[kb] = id;
+        a.node_vals[kb] = pv;
+      } else {
+        a.node_keys[kb + (r - 2)] = id;
+        a.node_vals[kb + (r - 2)] = pv | (r - 2);
       }
     }
-    // contribution keys in the reference's visit order: dst, negs, src
-    const uint64_t kb = p * (k + 2);
-    if (lane == 0) {
-      a.node_keys[kb] = a.edges[3 * p + 2];
-      a.node_keys[kb + k + 1] = a.edges[3 * p];
-      if (typed) a.rel_keys[p] = a.edges[3 * p + 1];
-    }
-    for (uint32_t j = lane; j < k; j += 32) a.node_keys[kb + 1 + j] = a.negs[p * k + j];
     __syncwarp();
+    if (tma && pn < a.P) {  // the buffer is free again: fetch the next positive
+      issue(id_next, 0);
+      if (pnn < a.P && lane < (int)nrows) id_next = row_id(pnn, lane);
+    }
   }
 }
 
@@ -328,157 +282,697 @@ __global__ void __launch_bounds__(1024) loss_reduce_kernel(const double* __restr
 }
 
 // ------------------------------------------------- K4 segmented reduction
-// One item of the sorted contribution list, added to the lane's elements.
+// Element ownership inside an 8-lane group: Dot / DistMult lane g owns
+// i = g + 8c; ComplEx lane g owns real index j = g + 8c (< h) and its
+// imaginary partner j + h (slots c and NC + c).
+template <int KIND, int NC>
+struct GMap {
+  static constexpr int NE = KIND == 2 ? 2 * NC : NC;
+  __device__ __forceinline__ static int idx(int e, int g, uint32_t h) {
+    if (KIND == 2) return e < NC ? g + kGroup * e : g + kGroup * (e - NC) + (int)h;
+    return g + kGroup * e;
+  }
+  __device__ __forceinline__ static bool ok(int e, int g, uint32_t d, uint32_t h) {
+    if (KIND == 2) return g + kGroup * (e < NC ? e : e - NC) < (int)h;
+    return g + kGroup * e < (int)d;
+  }
+};
+
+// One sorted contribution added to the group lane's elements.  All loads are
+// issued first (predicated, no branches) so a lane keeps every element of the
+// item in flight at once; the FP64 arithmetic follows in the reference order.
 template <int KIND, int NC, bool REL>
-__device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int lane, double* g) {
-  using M = Map<KIND, NC>;
+__device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g, double* acc) {
+  using M = GMap<KIND, NC>;
+  constexpr int NE = M::NE;
   const uint32_t d = a.dim, h = d / 2, k = a.k;
   if (REL) {  // relation gradient: adj_src(mix) (train.cpp:328-332)
-    const uint64_t p = val;
-    adjoint_add<KIND, NC>(a.snap + p * d, a.mix + p * d, lane, d, h, g);
+    const float* s = a.snap + (uint64_t)val * d;
+    const double* mx = a.mix + (uint64_t)val * d;
+    float sv[NE];
+    double mv[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const bool ok = M::ok(e, g, d, h);
+      const int i = M::idx(e, g, h);
+      sv[e] = ok ? __ldg(s + i) : 0.f;
+      mv[e] = ok ? __ldg(mx + i) : 0.0;
+    }
+    if (KIND == 2) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double orr = sv[c], ori = sv[c + NC], mr = mv[c], mi = mv[c + NC];
+        acc[c] += orr * mr + ori * mi;
+        acc[c + NC] += orr * mi - ori * mr;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] += (double)sv[e] * mv[e];
+    }
     return;
   }
-  const uint64_t p = val / (k + 2);
-  const uint32_t slot = val - (uint32_t)(p * (k + 2));
-  const float* rel = KIND != 0 ? a.rel_theta + (size_t)a.edges[3 * p + 1] * d : nullptr;
-  if (slot <= k) {
-    double x[M::NE];
-    combine<KIND, NC>(a.snap + p * d, rel, lane, d, h, x);
-    if (slot == 0) {  // dst: g -= IR1 (train.cpp:310)
+  const uint64_t p = val >> a.slot_bits;
+  const uint32_t slot = val & ((1u << a.slot_bits) - 1u);
+  const bool is_src = slot > k;
+  const float* rel = KIND != 0 ? a.rel_theta + (size_t)__ldg(a.rel_keys + p) * d : nullptr;
+  const float* s = a.snap + p * d;
+  const double* mx = a.mix + p * d;
+  const double w = (slot >= 1 && !is_src) ? __ldg(a.w + p * k + (slot - 1)) : 0.0;
+  float rv[NE], sv[NE];
+  double mv[NE];
 #pragma unroll
-      for (int e = 0; e < M::NE; ++e) g[e] -= x[e];
-    } else {  // negative j: g += w_j IR1 (train.cpp:320)
-      const double w = a.w[p * k + (slot - 1)];
+  for (int e = 0; e < NE; ++e) {
+    const bool ok = M::ok(e, g, d, h);
+    const int i = M::idx(e, g, h);
+    rv[e] = (KIND != 0 && ok) ? __ldg(rel + i) : 0.f;
+    sv[e] = (!is_src && ok) ? __ldg(s + i) : 0.f;
+    mv[e] = (is_src && ok) ? __ldg(mx + i) : 0.0;
+  }
+  if (!is_src) {  // dst: g -= IR1 (train.cpp:310); negative j: g += w_j IR1 (:320)
+    if (KIND == 2) {
 #pragma unroll
-      for (int e = 0; e < M::NE; ++e) g[e] += w * x[e];
+      for (int c = 0; c < NC; ++c) {
+        const double sr = sv[c], si = sv[c + NC], rr = rv[c], ri = rv[c + NC];
+        const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
+        acc[c] = slot == 0 ? acc[c] - xr : acc[c] + w * xr;
+        acc[c + NC] = slot == 0 ? acc[c + NC] - xi : acc[c + NC] + w * xi;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const double x = KIND == 0 ? (double)sv[e] : (double)sv[e] * (double)rv[e];
+        acc[e] = slot == 0 ? acc[e] - x : acc[e] + w * x;
+      }
     }
-  } else {  // src: g += adj_rel(mix) (train.cpp:327)
-    adjoint_add<KIND, NC>(rel, a.mix + p * d, lane, d, h, g);
+  } else {  // src: g += adj_rel(mix) (train.cpp:327, adjoint_combine :65-85)
+    if (KIND == 2) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double orr = rv[c], ori = rv[c + NC], mr = mv[c], mi = mv[c + NC];
+        acc[c] += orr * mr + ori * mi;
+        acc[c + NC] += orr * mi - ori * mr;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] += KIND == 0 ? mv[e] : (double)rv[e] * mv[e];
+    }
   }
 }
 
-// adagrad_update (train.cpp:342-354) on one row, or the gradient itself in
-// gradient-only mode.
-template <int KIND, int NC, bool REL>
-__device__ __forceinline__ void finish_row(const BatchArgs& a, uint32_t row, const double* g,
-                                           int lane) {
-  using M = Map<KIND, NC>;
-  const uint32_t d = a.dim, h = d / 2;
-  double* gout = REL ? a.grad_rels : a.grad_nodes;
-  if (gout) {
-#pragma unroll
-    for (int e = 0; e < M::NE; ++e)
-      if (M::ok(e, lane, d, h)) gout[(size_t)row * d + M::idx(e, lane, h)] = g[e];
-    if (lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[row] = 1;
-    return;
-  }
-  float* th = (REL ? a.rel_theta : a.theta) + (size_t)row * d;
-  float* st = (REL ? a.rel_state : a.state) + (size_t)row * d;
-  float tv[M::NE], sv[M::NE];
-#pragma unroll
-  for (int e = 0; e < M::NE; ++e) {
-    if (M::ok(e, lane, d, h)) {
-      const int i = M::idx(e, lane, h);
-      tv[e] = th[i];
-      sv[e] = st[i];
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < M::NE; ++e) {
-    if (M::ok(e, lane, d, h)) {
-      const int i = M::idx(e, lane, h);
-      const double gi = g[e];
-      const double acc = (double)sv[e] + gi * gi;
-      st[i] = (float)acc;
-      th[i] = (float)((double)tv[e] - a.lr * gi / (sqrt(acc) + a.eps));
-    }
-  }
+template <bool REL>
+__device__ __forceinline__ float* row_theta(const BatchArgs& a, uint32_t r) {
+  return (REL ? a.rel_theta : a.theta) + (size_t)r * a.dim;
+}
+template <bool REL>
+__device__ __forceinline__ float* row_state(const BatchArgs& a, uint32_t r) {
+  return (REL ? a.rel_state : a.state) + (size_t)r * a.dim;
+}
+
+// adagrad_update (train.cpp:342-354): a = acc + g^2 (FP64), acc = f32(a),
+// theta = f32(theta - lr g / (sqrt(a) + eps)).  When lr*g is a (signed) zero
+// the quotient is that same signed zero, so it is used directly: IEEE double
+// division and sqrt of zero take CUDA's slow path, and idle lanes (d < 32
+// vectors) would otherwise send every warp through it.  Bit-identical to the
+// reference for all inputs.
+__device__ __forceinline__ double opaque_sel(bool p, double a, double b);
+__device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr, double eps);
+__device__ __forceinline__ void adagrad_elem(double gi, float& th, float& st, double lr,
+                                             double eps) {
+  adagrad_fast(gi, th, st, lr, eps);
 }
 
 template <int KIND, int NC, bool REL>
 __global__ void __launch_bounds__(kSegThreads) segment_pass1(BatchArgs a, uint64_t n,
                                                              const uint32_t* __restrict__ skeys,
-                                                             const uint32_t* __restrict__ svals) {
-  using M = Map<KIND, NC>;
+                                                             const uint32_t* __restrict__ svals,
+                                                             uint32_t* __restrict__ span_list,
+                                                             unsigned int* __restrict__ span_count) {
+  using M = GMap<KIND, NC>;
+  constexpr int NE = M::NE;
   const int lane = threadIdx.x & 31;
+  const int g = lane & (kGroup - 1);
+  const int grp = lane >> 3;
   const uint64_t c = ((uint64_t)blockIdx.x * kSegThreads + threadIdx.x) >> 5;
   const uint64_t base = c * 32;
   if (base >= n) return;
+  const uint32_t d = a.dim, h = d / 2;
   const uint64_t end = min(base + 32, n);
   const uint64_t i = base + lane;
   const uint32_t key = i < n ? skeys[i] : 0;
   const bool head = i < n && (i == 0 || skeys[i - 1] != key);
-  uint32_t mask = __ballot_sync(0xffffffffu, head);
+  const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+  const bool cont_in = !(hmask & 1u);
   const bool cont_out = end < n && skeys[end] == skeys[end - 1];
-  double* first_out = a.part_first + c * a.dim;
-  double* last_out = a.part_last + c * a.dim;
-  const uint32_t d = a.dim, h = d / 2;
-
-  auto accumulate = [&](uint64_t from, uint64_t to, double* g) {
-#pragma unroll
-    for (int e = 0; e < M::NE; ++e) g[e] = 0.0;
-    for (uint64_t q = from; q < to; ++q) add_item<KIND, NC, REL>(a, svals[q], lane, g);
-  };
-  auto store_partial = [&](double* dst, const double* g) {
-#pragma unroll
-    for (int e = 0; e < M::NE; ++e)
-      if (M::ok(e, lane, d, h)) dst[M::idx(e, lane, h)] = g[e];
-  };
-
-  if (!(mask & 1u)) {  // leading piece continues a segment from the previous chunk
-    const uint64_t to = mask ? base + (__ffs(mask) - 1) : end;
-    double g[M::NE];
-    accumulate(base, to, g);
-    store_partial(first_out, g);
+  const uint32_t smask = hmask | 1u;  // piece starts (bit 0 also starts a continuation)
+  const int np = __popc(smask);
+  // lane t < np: start offset of piece t (t-th set bit of smask)
+  int my_start = 32;
+  if (lane < np) {
+    uint32_t m = smask;
+    for (int s2 = 0; s2 < lane; ++s2) m &= m - 1;
+    my_start = __ffs(m) - 1;
   }
-  const uint32_t heads = __popc(mask);
-  while (mask) {
-    const int hb = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const uint64_t from = base + hb;
-    const uint64_t to = mask ? base + (__ffs(mask) - 1) : end;
-    double g[M::NE];
-    accumulate(from, to, g);
-    if (to == end && cont_out) {
-      store_partial(last_out, g);  // finished in pass 2
-    } else {
-      finish_row<KIND, NC, REL>(a, skeys[from], g, lane);
+  const int nlive = (int)(end - base);
+  for (int r0 = 0; r0 < np; r0 += 4) {
+    const int t = r0 + grp;  // this group's piece
+    const bool live = t < np;
+    const int ps = __shfl_sync(0xffffffffu, my_start, t & 31);
+    const int pe_next = __shfl_sync(0xffffffffu, my_start, (t + 1) & 31);
+    const int pstart = live ? ps : 0;
+    const int pend = live ? (t + 1 < np ? pe_next : nlive) : 0;
+    const bool first_piece = live && t == 0 && cont_in;
+    const bool last_piece = live && t == np - 1 && cont_out;
+    const bool finish = live && !first_piece && !last_piece;
+    const uint32_t row = live ? skeys[base + pstart] : 0;
+    float tv[NE], sv[NE];
+    if (finish && !(REL ? a.grad_rels : a.grad_nodes)) {  // prefetch theta / state
+      const float* th = row_theta<REL>(a, row);
+      const float* st = row_state<REL>(a, row);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        if (M::ok(e, g, d, h)) {
+          tv[e] = th[M::idx(e, g, h)];
+          sv[e] = st[M::idx(e, g, h)];
+        }
+      }
+    }
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    // lockstep over the longest piece of this round
+    int len = pend - pstart;
+    int maxlen = len;
+#pragma unroll
+    for (int off = 8; off < 32; off <<= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    for (int q = 0; q < maxlen; ++q) {
+      if (q < len) add_item<KIND, NC, REL>(a, __ldg(svals + base + pstart + q), g, acc);
+    }
+    if (first_piece || last_piece) {
+      double* dst = (first_piece ? a.part_first : a.part_last) + c * d;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (M::ok(e, g, d, h)) dst[M::idx(e, g, h)] = acc[e];
+    } else if (finish) {
+      double* gout = REL ? a.grad_rels : a.grad_nodes;
+      if (gout) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+          if (M::ok(e, g, d, h)) gout[(size_t)row * d + M::idx(e, g, h)] = acc[e];
+        if (g == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[row] = 1;
+      } else {
+        float* th = row_theta<REL>(a, row);
+        float* st = row_state<REL>(a, row);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          if (M::ok(e, g, d, h)) {
+            adagrad_elem(acc[e], tv[e], sv[e], a.lr, a.eps);
+            th[M::idx(e, g, h)] = tv[e];
+            st[M::idx(e, g, h)] = sv[e];
+          }
+        }
+      }
     }
   }
   if (lane == 0) {
+    const int heads = __popc(hmask);
     a.chunk_flags[c] = (heads ? 0 : kNoHead) | (cont_out ? kContOut : 0);
     if (heads) atomicAdd(a.counters + (REL ? 1 : 0), (unsigned long long)heads);
+    if (heads && cont_out) span_list[atomicAdd(span_count, 1u)] = (uint32_t)c;
   }
 }
 
-template <int KIND, int NC, bool REL>
-__global__ void __launch_bounds__(kSegThreads) segment_pass2(BatchArgs a, uint64_t n,
-                                                             const uint32_t* __restrict__ skeys) {
-  using M = Map<KIND, NC>;
+// ---------------------------------------------- K4, vector-lane variant
+// Full warp per piece, lanes own 16-byte vectors: Dot / DistMult lane l owns
+// elements 4q..4q+3 (q = l + 32v, float4); ComplEx lane l owns the real pair
+// 2q, 2q+1 and its imaginary partners h+2q, h+2q+1 (float2 each), stored at
+// e = 4v + {0,1} (re) and 4v + {2,3} (im).  The next piece's theta / state and
+// first contribution are loaded while the current piece computes.
+template <int KIND, int NV>
+struct Lanes {
+  static constexpr int NE = 4 * NV;
+  bool ok[NV];
+  uint32_t off[NV];  // element offset of the lane's (real) vector
+  uint32_t h;
+  __device__ __forceinline__ Lanes(int lane, uint32_t d) {
+    h = d / 2;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t q = lane + 32 * v;
+      ok[v] = KIND == 2 ? 2 * q < h : 4 * q < d;
+      off[v] = KIND == 2 ? 2 * q : 4 * q;
+    }
+  }
+  template <bool RO>
+  __device__ __forceinline__ void ldf(const float* b, bool pred, float* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const bool o = pred && ok[v];
+      if (KIND == 2) {
+        float2 re = make_float2(0.f, 0.f), im = make_float2(0.f, 0.f);
+        if (o) {
+          const float2* pr = reinterpret_cast<const float2*>(b + off[v]);
+          const float2* pi = reinterpret_cast<const float2*>(b + off[v] + h);
+          re = RO ? __ldg(pr) : *pr;
+          im = RO ? __ldg(pi) : *pi;
+        }
+        x[4 * v] = re.x;
+        x[4 * v + 1] = re.y;
+        x[4 * v + 2] = im.x;
+        x[4 * v + 3] = im.y;
+      } else {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (o) {
+          const float4* pt = reinterpret_cast<const float4*>(b + off[v]);
+          t = RO ? __ldg(pt) : *pt;
+        }
+        x[4 * v] = t.x;
+        x[4 * v + 1] = t.y;
+        x[4 * v + 2] = t.z;
+        x[4 * v + 3] = t.w;
+      }
+    }
+  }
+  __device__ __forceinline__ void ldd(const double* b, bool pred, double* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const bool o = pred && ok[v];
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+      if (o) {
+        a0 = __ldg(reinterpret_cast<const double2*>(b + off[v]));
+        a1 = __ldg(reinterpret_cast<const double2*>(b + off[v] + (KIND == 2 ? h : 2)));
+      }
+      x[4 * v] = a0.x;
+      x[4 * v + 1] = a0.y;
+      x[4 * v + 2] = a1.x;
+      x[4 * v + 3] = a1.y;
+    }
+  }
+  __device__ __forceinline__ void stf(float* b, const float* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!ok[v]) continue;
+      if (KIND == 2) {
+        *reinterpret_cast<float2*>(b + off[v]) = make_float2(x[4 * v], x[4 * v + 1]);
+        *reinterpret_cast<float2*>(b + off[v] + h) = make_float2(x[4 * v + 2], x[4 * v + 3]);
+      } else {
+        *reinterpret_cast<float4*>(b + off[v]) =
+            make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+      }
+    }
+  }
+  __device__ __forceinline__ void std_(double* b, const double* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!ok[v]) continue;
+      *reinterpret_cast<double2*>(b + off[v]) = make_double2(x[4 * v], x[4 * v + 1]);
+      *reinterpret_cast<double2*>(b + off[v] + (KIND == 2 ? h : 2)) =
+          make_double2(x[4 * v + 2], x[4 * v + 3]);
+    }
+  }
+};
+
+// A select the compiler cannot see through: keeps "sqrt(z ? 1 : a)" from
+// being rewritten into "z ? 1 : sqrt(a)", which would still run sqrt(0).
+__device__ __forceinline__ double opaque_sel(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"((unsigned)p));
+  return r;
+}
+
+// adagrad_update (train.cpp:342-354) with the inline (fast-path) IEEE
+// division and square root; a zero quotient (lr*g == +-0) is selected, never
+// divided, since zero operands take CUDA's slow path.  Bit-identical.
+__device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr,
+                                             double eps) {
+  const double acc = (double)st + gi * gi;
+  st = (float)acc;
+  const double num = lr * gi;
+  const bool zero = num == 0.0;
+  const double q = opaque_sel(zero, 1.0, num) / (sqrt(opaque_sel(zero, 1.0, acc)) + eps);
+  th = (float)((double)th - (zero ? num : q));
+}
+
+// One contribution's operands: the src snapshot (dst / negative items), the
+// relation row, mix (src items) and the softmax weight.
+template <int NE>
+struct ItemRegs {
+  float sv[NE], rv[NE];
+  double mv[NE];
+  double w;
+  uint32_t slot;
+};
+
+struct SegCtx {  // hoisted kernel arguments
+  const float* snap;
+  const double* mix;
+  const double* w;
+  const float* rel_theta;
+  const uint32_t* rel_keys;
+  uint32_t d, k, sbits, smask;
+};
+
+template <int KIND, int NV, bool REL>
+__device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>& L, uint32_t val,
+                                          bool pred, ItemRegs<4 * NV>& it) {
+  if (REL) {
+    const uint64_t row = (uint64_t)val * x.d;
+    L.template ldf<true>(x.snap + row, pred, it.sv);
+    L.ldd(x.mix + row, pred, it.mv);
+    it.slot = 0;
+    it.w = 0.0;
+    return;
+  }
+  const uint32_t p = val >> x.sbits;
+  const uint32_t slot = val & x.smask;
+  const bool is_src = slot > x.k;
+  it.slot = slot;
+  it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1)) : 0.0;
+  const uint64_t row = (uint64_t)p * x.d;
+  if (KIND != 0) {
+    const uint32_t r = pred ? __ldg(x.rel_keys + p) : 0;
+    L.template ldf<true>(x.rel_theta + (uint64_t)r * x.d, pred, it.rv);
+  }
+  L.template ldf<true>(x.snap + row, pred && !is_src, it.sv);
+  L.ldd(x.mix + row, pred && is_src, it.mv);
+}
+
+template <int KIND, int NV, bool REL>
+__device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t k, double* acc) {
+  constexpr int NE = 4 * NV;
+  if (REL || it.slot > k) {  // adj_other(mix): other = src snapshot (REL) or relation row
+    const float* o = REL ? it.sv : it.rv;
+    if (KIND == 2) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int re = 4 * v + t, im = 4 * v + 2 + t;
+          const double orr = o[re], ori = o[im], mr = it.mv[re], mi = it.mv[im];
+          acc[re] += orr * mr + ori * mi;
+          acc[im] += orr * mi - ori * mr;
+        }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] += KIND == 0 ? it.mv[e] : (double)o[e] * it.mv[e];
+    }
+    return;
+  }
+  const bool dst = it.slot == 0;
+  if (KIND == 2) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int re = 4 * v + t, im = 4 * v + 2 + t;
+        const double sr = it.sv[re], si = it.sv[im], rr = it.rv[re], ri = it.rv[im];
+        const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
+        acc[re] = dst ? acc[re] - xr : acc[re] + it.w * xr;
+        acc[im] = dst ? acc[im] - xi : acc[im] + it.w * xi;
+      }
+  } else {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double x = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * (double)it.rv[e];
+      acc[e] = dst ? acc[e] - x : acc[e] + it.w * x;
+    }
+  }
+}
+
+template <int KIND, int NV, bool REL>
+__global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
+    BatchArgs a, uint64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+    uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
+  constexpr int NE = 4 * NV;
   const int lane = threadIdx.x & 31;
   const uint64_t c = ((uint64_t)blockIdx.x * kSegThreads + threadIdx.x) >> 5;
-  const uint64_t nchunks = (n + 31) / 32;
-  if (c >= nchunks) return;
-  const uint8_t f = a.chunk_flags[c];
-  if ((f & kNoHead) || !(f & kContOut)) return;
-  const uint32_t d = a.dim, h = d / 2;
-  const uint64_t end = min(c * 32 + 32, n);
-  const uint32_t row = skeys[end - 1];
-  double g[M::NE];
-#pragma unroll
-  for (int e = 0; e < M::NE; ++e)
-    g[e] = M::ok(e, lane, d, h) ? a.part_last[c * d + M::idx(e, lane, h)] : 0.0;
-  for (uint64_t c2 = c + 1; c2 < nchunks; ++c2) {
-#pragma unroll
-    for (int e = 0; e < M::NE; ++e)
-      if (M::ok(e, lane, d, h)) g[e] += a.part_first[c2 * d + M::idx(e, lane, h)];
-    const uint8_t f2 = a.chunk_flags[c2];
-    if (!((f2 & kNoHead) && (f2 & kContOut))) break;
+  const uint64_t base = c * 32;
+  if (base >= n) return;
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const SegCtx x{a.snap, a.mix, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u};
+  float* __restrict__ theta = REL ? a.rel_theta : a.theta;
+  float* __restrict__ state = REL ? a.rel_state : a.state;
+  double* gout = REL ? a.grad_rels : a.grad_nodes;
+  const uint64_t d = a.dim;
+  const double lr = a.lr, eps = a.eps;
+  const uint64_t end = min(base + 32, n);
+  const uint64_t i = base + lane;
+  const uint32_t key = i < n ? skeys[i] : 0;
+  const uint32_t val = i < n ? __ldg(svals + i) : 0;
+  const bool head = i < n && (i == 0 || skeys[i - 1] != key);
+  const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+  const bool cont_in = !(hmask & 1u);
+  const bool cont_out = end < n && skeys[end] == skeys[end - 1];
+  // lookahead: keys / values of the next chunk
+  const uint64_t j = end + lane;
+  const uint32_t key2 = (cont_out && j < n) ? skeys[j] : 0;
+  const uint32_t val2 = (cont_out && j < n) ? __ldg(svals + j) : 0;
+  const uint32_t last_key = __shfl_sync(0xffffffffu, key, (int)(end - base - 1));
+  const uint32_t same2 = __ballot_sync(0xffffffffu, cont_out && j < n && key2 == last_key);
+  // A segment whose head is in this chunk is "short" when it ends before
+  // end + 32 (or at n): this warp finishes it.  The next chunk's warp then
+  // skips that leading piece ("lead_done"); both sides use the same rule.
+  const int ext = __popc(same2);
+  const bool ext_short = cont_out && hmask != 0 && (ext < 32 || end + 32 >= n);
+  bool lead_done = false;
+  if (cont_in) {
+    const bool head_in_prev = skeys[base - 32] != __shfl_sync(0xffffffffu, key, 0);
+    lead_done = head_in_prev && (hmask != 0 || end == n);
   }
-  finish_row<KIND, NC, REL>(a, row, g, lane);
+  const uint32_t smask = hmask | 1u;
+  const int np = __popc(smask);
+  const int nlive = (int)(end - base);
+  auto finishing = [&](int t) {
+    return !(t == 0 && cont_in) && !(t == np - 1 && cont_out && !ext_short);
+  };
+  auto item_val = [&](int q) {  // q may run past the chunk into the lookahead
+    const uint32_t v1 = __shfl_sync(0xffffffffu, val, q & 31);
+    const uint32_t v2 = __shfl_sync(0xffffffffu, val2, q & 31);
+    return q < 32 ? v1 : v2;
+  };
+  // remaining piece starts, consumed lowest bit first
+  uint32_t rest = smask;
+  if (lead_done) rest &= rest - 1;
+  int t = lead_done ? 1 : 0;
+  if (t < np) {
+    int cur = __ffs(rest) - 1;
+    rest &= rest - 1;
+    float cth[NE], cst[NE];
+    ItemRegs<NE> cit;
+    {
+      const uint64_t row = (uint64_t)__shfl_sync(0xffffffffu, key, cur) * d;
+      const bool fin = finishing(t) && !gout;
+      L.template ldf<false>(theta + row, fin, cth);
+      L.template ldf<false>(state + row, fin, cst);
+      load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
+    }
+    for (; t < np; ++t) {
+      const int nxt = rest ? __ffs(rest) - 1 : nlive;
+      rest &= rest - 1;
+      const bool has_next = t + 1 < np;
+      const int pend = (t == np - 1 && ext_short) ? nlive + ext : nxt;
+      float nth[NE], nst[NE];
+      ItemRegs<NE> nit;
+      {
+        const int ns = nxt & 31;
+        const uint64_t row = (uint64_t)__shfl_sync(0xffffffffu, key, ns) * d;
+        const bool fin = has_next && finishing(t + 1) && !gout;
+        L.template ldf<false>(theta + row, fin, nth);
+        L.template ldf<false>(state + row, fin, nst);
+        load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, ns), has_next, nit);
+      }
+      double acc[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+      add_loaded<KIND, NV, REL>(cit, x.k, acc);
+      for (int q = cur + 1; q < pend; ++q) {
+        ItemRegs<NE> it;
+        load_item<KIND, NV, REL>(x, L, item_val(q), true, it);
+        add_loaded<KIND, NV, REL>(it, x.k, acc);
+      }
+      const uint32_t rowid = __shfl_sync(0xffffffffu, key, cur);
+      if (t == 0 && cont_in) {
+        L.std_(a.part_first + c * d, acc);
+      } else if (!finishing(t)) {
+        L.std_(a.part_last + c * d, acc);
+      } else if (gout) {
+        L.std_(gout + (uint64_t)rowid * d, acc);
+        if (lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[rowid] = 1;
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) adagrad_fast(acc[e], cth[e], cst[e], lr, eps);
+        L.stf(theta + (uint64_t)rowid * d, cth);
+        L.stf(state + (uint64_t)rowid * d, cst);
+      }
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        cth[e] = nth[e];
+        cst[e] = nst[e];
+      }
+      cit = nit;
+      cur = nxt;
+    }
+  }
+  if (lane == 0) {
+    const int heads = __popc(hmask);
+    // pass 2 sees only long segments: a short one ends the chain at this
+    // chunk (no kContOut) and its continuation chunk starts "done"
+    a.chunk_flags[c] = (heads ? 0 : kNoHead) | ((cont_out && !ext_short) ? kContOut : 0);
+    if (heads) atomicAdd(a.counters + (REL ? 1 : 0), (unsigned long long)heads);
+    if (heads && cont_out && !ext_short) span_list[atomicAdd(span_count, 1u)] = (uint32_t)c;
+  }
+}
+
+// One block per chunk that holds the head of a chunk-spanning segment: sum
+// part_last[c] and the following chunks' part_first in a fixed order (warp w
+// takes chunks w, w + 8, ... in order; warp sums combined in warp order), then
+// one Adagrad row update.
+template <bool REL>
+__global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint64_t n,
+                                                               const uint32_t* __restrict__ skeys,
+                                                               const uint32_t* __restrict__ span_list,
+                                                               const unsigned int* __restrict__ span_count) {
+  __shared__ double wsum[kPass2Threads / 32][512];
+  __shared__ uint32_t s_len;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int W = kPass2Threads / 32;
+  const uint32_t d = a.dim;
+  const uint64_t nchunks = (n + 31) / 32;
+  const unsigned cnt = *span_count;
+  for (unsigned idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
+    const uint64_t c = span_list[idx];
+    if (warp == 0) {  // following chunks covered by the segment, 32 flags per step
+      uint32_t L = 0;
+      for (uint64_t c0 = c + 1; c0 < nchunks; c0 += 32) {
+        const uint64_t c2 = c0 + lane;
+        const uint8_t f2 = c2 < nchunks ? a.chunk_flags[c2] : 0;
+        const uint32_t stop = __ballot_sync(0xffffffffu, !((f2 & kNoHead) && (f2 & kContOut)));
+        if (stop) {
+          L += __ffs(stop);
+          break;
+        }
+        L += 32;
+      }
+      if (lane == 0) s_len = (uint32_t)(L < nchunks - c - 1 ? L : nchunks - c - 1);
+    }
+    __syncthreads();
+    const uint32_t L = s_len;
+    for (uint32_t e = lane; e < d; e += 32) {
+      double s = 0.0;
+      uint32_t q = warp;
+      for (; q + 3 * W < L; q += 4 * W) {  // four loads in flight, added in order
+        const double v0 = a.part_first[(c + 1 + q) * d + e];
+        const double v1 = a.part_first[(c + 1 + q + W) * d + e];
+        const double v2 = a.part_first[(c + 1 + q + 2 * W) * d + e];
+        const double v3 = a.part_first[(c + 1 + q + 3 * W) * d + e];
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+      }
+      for (; q < L; q += W) s += a.part_first[(c + 1 + q) * d + e];
+      wsum[warp][e] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t row = skeys[min(c * 32 + 32, n) - 1];
+      double* gout = REL ? a.grad_rels : a.grad_nodes;
+      float* th = row_theta<REL>(a, row);
+      float* st = row_state<REL>(a, row);
+      for (uint32_t e = lane; e < d; e += 32) {
+        double gsum = a.part_last[c * d + e];
+        for (int w = 0; w < W; ++w) gsum += wsum[w][e];
+        if (gout) {
+          gout[(size_t)row * d + e] = gsum;
+        } else {
+          float tv = th[e], sv = st[e];
+          adagrad_elem(gsum, tv, sv, a.lr, a.eps);
+          th[e] = tv;
+          st[e] = sv;
+        }
+      }
+      if (gout && lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[row] = 1;
+    }
+    __syncthreads();
+  }
 }
 
 // ----------------------------------------------------------- dispatchers
+// score_kernel<KIND> is shared by every (dim, k): its dynamic-smem attribute
+// only grows; occupancy is cached per smem size.  (Host-side, per process.)
+size_t g_score_attr[3] = {0, 0, 0};
+size_t g_score_occ_smem[3] = {0, 0, 0};
+int g_score_occ[3] = {0, 0, 0};
+
+void sort_items(const BatchArgs& a, uint64_t items, const uint32_t* keys, const uint32_t* vals,
+                int key_bits, cudaStream_t st) {
+  size_t bytes = a.sort_temp_bytes;
+  LGD_CUDA(cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, keys, a.skeys, vals, a.svals,
+                                           (int64_t)items, 0, key_bits, st));
+}
+
+// vector-lane pass 1 when the dimension fits one (NV = 1) or two (NV = 2)
+// 16-byte vectors per lane; 0 = use the 8-lane-group kernel
+template <int KIND>
+int vec_width(uint32_t d) {
+  if (KIND == 2) {
+    const uint32_t h = d / 2;
+    if (h % 2) return 0;
+    return h <= 64 ? 1 : (h <= 128 ? 2 : 0);
+  }
+  if (d % 4) return 0;
+  return d <= 128 ? 1 : (d <= 256 ? 2 : 0);
+}
+
+template <int KIND, int NV, bool REL>
+void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
+  segment_pass1_vec<KIND, NV, REL><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
+                                                                 a.span_list, a.span_count);
+}
+
+template <int KIND, int NC>
+void run_segments(const BatchArgs& a, uint64_t items, bool rel, cudaStream_t st) {
+  LGD_CUDA(cudaMemsetAsync(a.span_count, 0, sizeof(unsigned int), st));
+  const unsigned grid = ceil_div(ceil_div(items, 32), kSegThreads / 32);
+  const unsigned grid2 = (unsigned)a.sm_count * 4;
+  const int nv = vec_width<KIND>(a.dim);
+  if (nv) {
+    if (rel) {
+      nv == 1 ? launch_vec_pass1<KIND, 1, true>(a, items, grid, st)
+              : launch_vec_pass1<KIND, 2, true>(a, items, grid, st);
+    } else {
+      nv == 1 ? launch_vec_pass1<KIND, 1, false>(a, items, grid, st)
+              : launch_vec_pass1<KIND, 2, false>(a, items, grid, st);
+    }
+    LGD_LAUNCH_CHECK();
+    if (rel) {
+      segment_pass2<true><<<grid2, kPass2Threads, 0, st>>>(a, items, a.skeys, a.span_list,
+                                                            a.span_count);
+    } else {
+      segment_pass2<false><<<grid2, kPass2Threads, 0, st>>>(a, items, a.skeys, a.span_list,
+                                                             a.span_count);
+    }
+    LGD_LAUNCH_CHECK();
+    return;
+  }
+  if (rel) {
+    segment_pass1<KIND, NC, true><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
+                                                                a.span_list, a.span_count);
+    LGD_LAUNCH_CHECK();
+    segment_pass2<true><<<grid2, kPass2Threads, 0, st>>>(a, items, a.skeys, a.span_list,
+                                                          a.span_count);
+  } else {
+    segment_pass1<KIND, NC, false><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
+                                                                 a.span_list, a.span_count);
+    LGD_LAUNCH_CHECK();
+    segment_pass2<false><<<grid2, kPass2Threads, 0, st>>>(a, items, a.skeys, a.span_list,
+                                                           a.span_count);
+  }
+  LGD_LAUNCH_CHECK();
+}
+
 template <int KIND, int NC>
 void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   auto rec = [&](int i) {
@@ -486,61 +980,44 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   };
   const uint32_t d = a.dim, k = a.k;
   const uint64_t P = a.P;
-  const uint32_t dpad = (d + 3) & ~3u;
-  const size_t smem = score_smem_bytes(d, k);
-  const bool tma = (d % 4) == 0;
+  const ScoreSmem L(d, k);
+  const size_t smem = L.block_bytes();
+  const int tma = ((d % 4) == 0 && L.nrows <= 32) ? 1 : 0;
   rec(0);
   {
-    const uint64_t blocks_needed = (P + kScoreWarps - 1) / kScoreWarps;
-    int per_sm = 1;
-    if (tma) {
-      LGD_CUDA(cudaFuncSetAttribute(score_kernel<KIND, NC, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, score_kernel<KIND, NC, true>, kScoreWarps * 32, smem));
-    } else {
-      LGD_CUDA(cudaFuncSetAttribute(score_kernel<KIND, NC, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, score_kernel<KIND, NC, false>, kScoreWarps * 32, smem));
+    // the dynamic-smem attribute only ever grows (it is shared by every
+    // dimension / k this kernel serves); occupancy is cached per smem size
+    size_t* attr_set = g_score_attr;
+    size_t* occ_smem = g_score_occ_smem;
+    int* occ_val = g_score_occ;
+    if (smem > attr_set[KIND]) {
+      LGD_CUDA(cudaFuncSetAttribute(score_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      attr_set[KIND] = smem;
     }
+    if (occ_smem[KIND] != smem) {
+      LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val[KIND], score_kernel<KIND>,
+                                                             kScoreWarps * 32, smem));
+      occ_smem[KIND] = smem;
+    }
+    const int per_sm = occ_val[KIND];
     if (per_sm < 1) throw std::invalid_argument("batch shape exceeds shared memory (k, dim)");
+    const uint64_t blocks_needed = (P + kScoreWarps - 1) / kScoreWarps;
     const uint64_t cap = (uint64_t)per_sm * a.sm_count;
     const unsigned grid = (unsigned)(blocks_needed < cap ? blocks_needed : cap);
-    if (tma) {
-      score_kernel<KIND, NC, true><<<grid, kScoreWarps * 32, smem, st>>>(a, dpad);
-    } else {
-      score_kernel<KIND, NC, false><<<grid, kScoreWarps * 32, smem, st>>>(a, dpad);
-    }
+    score_kernel<KIND><<<grid, kScoreWarps * 32, smem, st>>>(a, tma);
     LGD_LAUNCH_CHECK();
   }
   loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
   LGD_LAUNCH_CHECK();
   rec(1);
-  const uint64_t items = P * (k + 2);
-  {
-    size_t bytes = a.sort_temp_bytes;
-    LGD_CUDA(cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, a.node_keys, a.skeys, a.iota,
-                                             a.svals, (int64_t)items, 0, a.node_key_bits, st));
-  }
+  sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
   rec(2);
-  {
-    const unsigned grid = ceil_div(ceil_div(items, 32), kSegThreads / 32);
-    segment_pass1<KIND, NC, false><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals);
-    LGD_LAUNCH_CHECK();
-    segment_pass2<KIND, NC, false><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys);
-    LGD_LAUNCH_CHECK();
-  }
+  run_segments<KIND, NC>(a, P * (k + 2), false, st);
   rec(3);
   if (KIND != 0) {
-    size_t bytes = a.sort_temp_bytes;
-    LGD_CUDA(cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, a.rel_keys, a.skeys, a.iota,
-                                             a.svals, (int64_t)P, 0, a.rel_key_bits, st));
-    const unsigned grid = ceil_div(ceil_div(P, 32), kSegThreads / 32);
-    segment_pass1<KIND, NC, true><<<grid, kSegThreads, 0, st>>>(a, P, a.skeys, a.svals);
-    LGD_LAUNCH_CHECK();
-    segment_pass2<KIND, NC, true><<<grid, kSegThreads, 0, st>>>(a, P, a.skeys);
-    LGD_LAUNCH_CHECK();
+    sort_items(a, P, a.rel_keys, a.iota, a.rel_key_bits, st);
+    run_segments<KIND, NC>(a, P, true, st);
   }
   rec(4);
 }
@@ -548,11 +1025,14 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
 template <int KIND>
 void run_kind(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   const uint32_t lanes_elems = KIND == 2 ? a.dim / 2 : a.dim;
-  const uint32_t nc = (lanes_elems + 31) / 32;
+  const uint32_t nc = (lanes_elems + kGroup - 1) / kGroup;
   if (nc <= 1) return run_batch<KIND, 1>(a, st, ev);
   if (nc <= 2) return run_batch<KIND, 2>(a, st, ev);
   if (nc <= 4) return run_batch<KIND, 4>(a, st, ev);
   if (nc <= 8) return run_batch<KIND, 8>(a, st, ev);
+  if (nc <= 13) return run_batch<KIND, 13>(a, st, ev);
+  if (nc <= 16) return run_batch<KIND, 16>(a, st, ev);
+  if (nc <= 32) return run_batch<KIND, 32>(a, st, ev);
   throw std::invalid_argument("embedding dimension too large (max 256, ComplEx 512)");
 }
 
@@ -567,11 +1047,7 @@ size_t batch_sort_temp_bytes(uint64_t max_items) {
   return bytes;
 }
 
-size_t score_smem_bytes(uint32_t dim, uint32_t k) {
-  const size_t dpad = (dim + 3) & ~3u;
-  const size_t warp_bytes = 2 * (size_t)(k + 3) * dpad * sizeof(float) + 2 * (size_t)k * 8;
-  return 16 * kScoreWarps + kScoreWarps * warp_bytes;
-}
+size_t score_smem_bytes(uint32_t dim, uint32_t k) { return ScoreSmem(dim, k).block_bytes(); }
 
 void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   if (a.P == 0) return;

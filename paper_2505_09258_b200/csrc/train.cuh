@@ -26,6 +26,7 @@ struct BatchArgs {
   float* snap;                // P x d  pre-update source rows
   double* loss;               // P per-positive loss
   uint32_t* node_keys;        // P x (k+2) contribution node ids (dst, negs, src)
+  uint32_t* node_vals;        // P x (k+2) payloads (p << slot_bits) | slot
   uint32_t* rel_keys;         // P relation ids
   const uint32_t* iota;       // 0..P*(k+2)-1
   uint32_t* skeys;            // sorted keys
@@ -35,8 +36,11 @@ struct BatchArgs {
   double* part_first;         // chunks x d
   double* part_last;          // chunks x d
   uint8_t* chunk_flags;       // chunks
+  uint32_t* span_list;        // chunks holding the head of a chunk-spanning segment
+  unsigned int* span_count;   // entries in span_list
   unsigned long long* counters;  // [0] unique nodes, [1] unique rels (accumulated)
   double* batch_loss_out;     // one double: this batch's loss
+  int slot_bits;              // bits for a slot in [0, k+1]
   int node_key_bits;
   int rel_key_bits;
   // gradient-only mode (operator-level batch_gradients): dense V x d / R x d

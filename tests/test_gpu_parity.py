@@ -148,10 +148,15 @@ def test_batch_matches_golden(kind, d):
 
 
 @pytest.mark.parametrize("kind", KINDS)
-@pytest.mark.parametrize("d,k,P", [(100, 16, 3000), (64, 5, 777), (128, 40, 500), (32, 1, 64)])
-def test_batch_matches_oracle_wide(oracle, kind, d, k, P):
-    rng = np.random.default_rng(d * 1000 + k)
-    V, R = 5000, 17
+@pytest.mark.parametrize("d,k,P,V", [(100, 16, 3000, 5000), (64, 5, 777, 5000),
+                                     (128, 40, 500, 5000), (32, 1, 64, 5000),
+                                     (100, 16, 3000, 64), (100, 16, 3000, 2000),
+                                     (200, 8, 1000, 3000), (36, 3, 2000, 300)])
+def test_batch_matches_oracle_wide(oracle, kind, d, k, P, V):
+    """Segment lengths from 1 to ~850 contributions (V=64): chunk-boundary
+    crossings, short-segment extension and long (pass-2) segments."""
+    rng = np.random.default_rng(d * 1000 + k + V)
+    R = 17
     E0 = rng.uniform(-0.05, 0.05, (V, d)).astype(np.float32)
     S0 = rng.uniform(0, 0.01, (V, d)).astype(np.float32)
     rE0 = rng.uniform(-0.05, 0.05, (R, d)).astype(np.float32)
