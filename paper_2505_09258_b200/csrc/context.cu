@@ -231,16 +231,20 @@ struct lgd_context {
     a.span_count = span_count.get();
     a.counters = counters.get();
     a.batch_loss_out = loss_out;
+    a.pool_first[0] = 0;
+    a.pool_end[0] = V;
+    a.pool_n = 1;
     a.node_key_bits = bits_for(V ? V - 1 : 0);
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
     return a;
   }
 
-  uint64_t batch_launches() const {
+  uint64_t batch_launches(int node_bits = -1) const {
     // K3 + loss reduce + pass1 + pass2 (+ relation pass1/2) + radix sorts
     // (upsweep histogram + scan + one onesweep pass per 8 key bits)
-    const int nb = bits_for(V ? V - 1 : 0), rb = bits_for(R ? R - 1 : 0);
+    const int nb = node_bits >= 0 ? node_bits : bits_for(V ? V - 1 : 0);
+    const int rb = bits_for(R ? R - 1 : 0);
     uint64_t c = 4 + 2 + (nb + 7) / 8;
     if (typed()) c += 2 + 2 + (rb + 7) / 8;
     return c;
@@ -283,8 +287,17 @@ struct lgd_context {
       if (prof_pending[s]) prof_drain(s);
   }
 
-  void run_batch(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P, double* loss_out) {
-    const BatchArgs a = batch_args(bedges, bnegs, P, loss_out);
+  void run_batch(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P, double* loss_out,
+                 const Pool* pool = nullptr) {
+    BatchArgs a = batch_args(bedges, bnegs, P, loss_out);
+    if (pool) {  // keys are indices into the resident pool of the plan state
+      for (int i = 0; i < 3; ++i) {
+        a.pool_first[i] = pool->first[i];
+        a.pool_end[i] = pool->end_index[i];
+      }
+      a.pool_n = pool->n;
+      a.node_key_bits = bits_for(pool->end_index[pool->n - 1] - 1);
+    }
     if (profiling) {
       const int slot = prof_slot(1);
       BatchEvents ev;
@@ -299,7 +312,7 @@ struct lgd_context {
     } else {
       launch_train_batch(a, stream, nullptr);
     }
-    launches += batch_launches();
+    launches += batch_launches(a.node_key_bits);
   }
 
   Pool pool_of_state(size_t s) const {
@@ -428,7 +441,7 @@ struct lgd_context {
       if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
       for (uint64_t o = 0; o < m; o += opt.batch_size) {
         const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
-        run_batch(shuffled.get() + 3 * o, negs.get() + o * kk, P, batch_losses.get() + nb);
+        run_batch(shuffled.get() + 3 * o, negs.get() + o * kk, P, batch_losses.get() + nb, &pool);
         ++nb;
       }
       edges_trained += m;

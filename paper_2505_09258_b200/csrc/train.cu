@@ -80,6 +80,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ------------------------------------------------------- pool indices
+__device__ __forceinline__ uint32_t to_pool(const BatchArgs& a, uint32_t id) {
+  uint64_t prev = 0;
+  for (int i = 0; i < a.pool_n; ++i) {
+    const uint64_t cnt = a.pool_end[i] - prev;
+    if (id >= a.pool_first[i] && id - a.pool_first[i] < cnt) return (uint32_t)(prev + id - a.pool_first[i]);
+    prev = a.pool_end[i];
+  }
+  return 0xffffffffu;  // not resident (validated on the host)
+}
+__device__ __forceinline__ uint32_t from_pool(const BatchArgs& a, uint32_t idx) {
+  if (idx < a.pool_end[0]) return (uint32_t)(a.pool_first[0] + idx);
+  if (a.pool_n > 1 && idx < a.pool_end[1]) return (uint32_t)(a.pool_first[1] + (idx - a.pool_end[0]));
+  return (uint32_t)(a.pool_first[2] + (idx - a.pool_end[1]));
+}
+
 // ---------------------------------------------------------------- K3 score
 // Shared memory per warp: ids[32] u32, rows[(k+3) x dpad] f32 (src, rel,
 // dst, negatives), ir1[dpad] f64, f[k+1] f64, e[k] f64.  One row buffer per
@@ -246,15 +262,15 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       const uint32_t id = pid[r];
       const uint32_t pv = (uint32_t)p << a.slot_bits;  // payload: positive, slot
       if (r == 0) {
-        a.node_keys[kb + k + 1] = id;
+        a.node_keys[kb + k + 1] = to_pool(a, id);
         a.node_vals[kb + k + 1] = pv | (k + 1);
       } else if (r == 1) {
         if (typed) a.rel_keys[p] = id;
       } else if (r == 2) {
-        a.node_keys[kb] = id;
+        a.node_keys[kb] = to_pool(a, id);
         a.node_vals[kb] = pv;
       } else {
-        a.node_keys[kb + (r - 2)] = id;
+        a.node_keys[kb + (r - 2)] = to_pool(a, id);
         a.node_vals[kb + (r - 2)] = pv | (r - 2);
       }
     }
@@ -443,7 +459,7 @@ __global__ void __launch_bounds__(kSegThreads) segment_pass1(BatchArgs a, uint64
     const bool first_piece = live && t == 0 && cont_in;
     const bool last_piece = live && t == np - 1 && cont_out;
     const bool finish = live && !first_piece && !last_piece;
-    const uint32_t row = live ? skeys[base + pstart] : 0;
+    const uint32_t row = live ? (REL ? skeys[base + pstart] : from_pool(a, skeys[base + pstart])) : 0;
     float tv[NE], sv[NE];
     if (finish && !(REL ? a.grad_rels : a.grad_nodes)) {  // prefetch theta / state
       const float* th = row_theta<REL>(a, row);
@@ -648,7 +664,8 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
   it.slot = slot;
-  it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1)) : 0.0;
+  // dst (slot 0) uses w = -1: g - IR1 == g + (-1 * IR1) in IEEE arithmetic
+  it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1)) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
   if (KIND != 0) {
     const uint32_t r = pred ? __ldg(x.rel_keys + p) : 0;
@@ -679,7 +696,7 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
     }
     return;
   }
-  const bool dst = it.slot == 0;
+  // dst: g -= IR1 (train.cpp:310) as g += (-1) IR1; negative j: g += w_j IR1 (:320)
   if (KIND == 2) {
 #pragma unroll
     for (int v = 0; v < NV; ++v)
@@ -688,16 +705,27 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
         const int re = 4 * v + t, im = 4 * v + 2 + t;
         const double sr = it.sv[re], si = it.sv[im], rr = it.rv[re], ri = it.rv[im];
         const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
-        acc[re] = dst ? acc[re] - xr : acc[re] + it.w * xr;
-        acc[im] = dst ? acc[im] - xi : acc[im] + it.w * xi;
+        acc[re] += it.w * xr;
+        acc[im] += it.w * xi;
       }
   } else {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const double x = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * (double)it.rv[e];
-      acc[e] = dst ? acc[e] - x : acc[e] + it.w * x;
+      acc[e] += it.w * x;
     }
   }
+}
+
+// adagrad_update (train.cpp:342-354) with the compiler's inline IEEE
+// division / square root (bit-identical; zero or denormal operands take the
+// library slow path, which only genuinely-zero gradients of active lanes
+// reach).
+__device__ __forceinline__ void adagrad_plain(double gi, float& th, float& st, double lr,
+                                              double eps) {
+  const double acc = (double)st + gi * gi;
+  st = (float)acc;
+  th = (float)((double)th - lr * gi / (sqrt(acc) + eps));
 }
 
 template <int KIND, int NV, bool REL>
@@ -761,8 +789,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     rest &= rest - 1;
     float cth[NE], cst[NE];
     ItemRegs<NE> cit;
+    auto rowof = [&](uint32_t kk) { return REL ? kk : from_pool(a, kk); };
     {
-      const uint64_t row = (uint64_t)__shfl_sync(0xffffffffu, key, cur) * d;
+      const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, cur)) * d;
       const bool fin = finishing(t) && !gout;
       L.template ldf<false>(theta + row, fin, cth);
       L.template ldf<false>(state + row, fin, cst);
@@ -777,7 +806,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       ItemRegs<NE> nit;
       {
         const int ns = nxt & 31;
-        const uint64_t row = (uint64_t)__shfl_sync(0xffffffffu, key, ns) * d;
+        const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, ns)) * d;
         const bool fin = has_next && finishing(t + 1) && !gout;
         L.template ldf<false>(theta + row, fin, nth);
         L.template ldf<false>(state + row, fin, nst);
@@ -792,7 +821,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         load_item<KIND, NV, REL>(x, L, item_val(q), true, it);
         add_loaded<KIND, NV, REL>(it, x.k, acc);
       }
-      const uint32_t rowid = __shfl_sync(0xffffffffu, key, cur);
+      const uint32_t rowid = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {
         L.std_(a.part_first + c * d, acc);
       } else if (!finishing(t)) {
@@ -877,7 +906,8 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
     }
     __syncthreads();
     if (warp == 0) {
-      const uint32_t row = skeys[min(c * 32 + 32, n) - 1];
+      const uint32_t kk = skeys[min(c * 32 + 32, n) - 1];
+      const uint32_t row = REL ? kk : from_pool(a, kk);
       double* gout = REL ? a.grad_rels : a.grad_nodes;
       float* th = row_theta<REL>(a, row);
       float* st = row_state<REL>(a, row);

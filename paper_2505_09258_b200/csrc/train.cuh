@@ -41,6 +41,11 @@ struct BatchArgs {
   unsigned long long* counters;  // [0] unique nodes, [1] unique rels (accumulated)
   double* batch_loss_out;     // one double: this batch's loss
   int slot_bits;              // bits for a slot in [0, k+1]
+  // resident sampling pool (<= 3 node ranges, ascending): contribution keys
+  // are pool indices, so the radix sort needs bits_for(pool size) bits only
+  uint64_t pool_first[3];
+  uint64_t pool_end[3];       // inclusive prefix of range sizes
+  int pool_n;
   int node_key_bits;
   int rel_key_bits;
   // gradient-only mode (operator-level batch_gradients): dense V x d / R x d
