@@ -128,6 +128,19 @@ int lgd_set_iteration_plan(lgd_context* ctx, uint64_t num_states, const uint32_t
                            const uint32_t* swaps, const uint32_t* bucket_order,
                            const uint64_t* state_offsets, const uint64_t* prefetch_points);
 
+/* Multi-GPU partition-round schedule: rounds of disjoint
+ * partition pairs; every bucket once, numbered in one global order that keys
+ * its RNG stream; the pair is its negative pool; pair j of a round runs on
+ * rank j % num_ranks.  Call with capacity 0 to learn count. */
+typedef struct {
+  uint32_t src_part, dst_part; /* bucket (i, j) */
+  uint64_t g;                  /* RNG stream index (global position) */
+  uint32_t pool[3];            /* negative pool partitions, 0xffffffff = unused */
+  uint32_t round, pair;
+} lgd_bucket_item;
+int lgd_round_schedule(uint32_t n, uint64_t capacity, uint64_t* count, lgd_bucket_item* items,
+                       uint32_t* num_rounds, uint32_t* pairs_per_round);
+
 /* ------------------------------------------------------ embedding store */
 
 /* EmbeddingStore::create initial values (store.cpp:59-86), on the device. */
@@ -160,6 +173,22 @@ int lgd_get_bucketed_edges(lgd_context* ctx, uint32_t* edges_out);
 /* Pinned host memory for the E||S blobs and edge lists. */
 int lgd_host_alloc(uint64_t bytes, void** out);
 int lgd_host_free(void* p);
+
+/* Trains an explicit list of buckets (e.g. this rank's share of a round),
+ * each with its own RNG stream index and negative pool. */
+int lgd_train_items(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* items,
+                    uint64_t count, lgd_epoch_result* out);
+/* Lock-step rounds for typed models on several ranks: after each step the
+ * caller sums the dense relation gradient [R x (dim+1)] (device, last column
+ * = touched flag) across ranks, then applies it on every rank. */
+int lgd_round_begin(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* items,
+                    uint64_t count, uint64_t* my_batches);
+int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device);
+int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device);
+int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out);
+/* Device pointers of the resident tables (partition hand-off between ranks). */
+int lgd_device_tables(lgd_context* ctx, float** theta, float** state, float** rel_theta,
+                      float** rel_state);
 
 /* Operator level: batch_loss + batch_gradients + adagrad_step
  * (train.cpp:217-363) on one batch of host edges / negatives. */

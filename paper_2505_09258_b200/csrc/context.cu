@@ -196,7 +196,7 @@ struct lgd_context {
   }
 
   BatchArgs batch_args(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P,
-                       double* loss_out) const {
+                       double* loss_out, const Pool* pool = nullptr) const {
     BatchArgs a{};
     a.kind = kind;
     a.dim = dim;
@@ -235,6 +235,14 @@ struct lgd_context {
     a.pool_end[0] = V;
     a.pool_n = 1;
     a.node_key_bits = bits_for(V ? V - 1 : 0);
+    if (pool) {  // keys are indices into the resident pool of the plan state
+      for (int i = 0; i < 3; ++i) {
+        a.pool_first[i] = pool->first[i];
+        a.pool_end[i] = pool->end_index[i];
+      }
+      a.pool_n = pool->n;
+      a.node_key_bits = bits_for(pool->end_index[pool->n - 1] - 1);
+    }
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
     return a;
@@ -289,15 +297,7 @@ struct lgd_context {
 
   void run_batch(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P, double* loss_out,
                  const Pool* pool = nullptr) {
-    BatchArgs a = batch_args(bedges, bnegs, P, loss_out);
-    if (pool) {  // keys are indices into the resident pool of the plan state
-      for (int i = 0; i < 3; ++i) {
-        a.pool_first[i] = pool->first[i];
-        a.pool_end[i] = pool->end_index[i];
-      }
-      a.pool_n = pool->n;
-      a.node_key_bits = bits_for(pool->end_index[pool->n - 1] - 1);
-    }
+    BatchArgs a = batch_args(bedges, bnegs, P, loss_out, pool);
     if (profiling) {
       const int slot = prof_slot(1);
       BatchEvents ev;
@@ -344,109 +344,99 @@ struct lgd_context {
       throw std::invalid_argument("at least one negative per positive required");
   }
 
-  // host_bucketed: optional host copy (pinned for full speed) of the edges in
-  // bucket order; each bucket is then streamed H2D on a side stream, one
-  // bucket ahead of the compute (double-buffered staging).
-  void train_range(uint32_t epoch, uint64_t g_begin, uint64_t g_end, lgd_epoch_result* out,
-                   const uint32_t* host_bucketed = nullptr) {
-    check_ready();
-    const auto t0 = std::chrono::steady_clock::now();
+  // One bucket of work: bucket (bi, bj), its RNG stream index g (the
+  // position in the schedule, pipeline.cpp:296) and its negative pool.
+  struct WorkItem {
+    uint32_t bi, bj;
+    uint64_t g;
+    Pool pool;
+  };
+
+  Pool pool_of_parts(const uint32_t* parts, int count) const {
+    uint32_t ids[3];
+    int np = 0;
+    for (int i = 0; i < count; ++i)
+      if (parts[i] != kNoPartition) {
+        if (parts[i] >= n) throw std::invalid_argument("pool partition out of range");
+        ids[np++] = parts[i];
+      }
+    if (np == 0) throw std::invalid_argument("empty negative pool");
+    std::sort(ids, ids + np);
+    Pool pool{};
+    uint64_t acc = 0;
+    for (int i = 0; i < np; ++i) {
+      pool.first[i] = part_begin(ids[i]);
+      acc += part_rows(ids[i]);
+      pool.end_index[i] = acc;
+    }
+    pool.n = np;
+    return pool;
+  }
+
+  std::vector<WorkItem> plan_items(uint64_t g_begin, uint64_t g_end) const {
+    std::vector<WorkItem> items;
     const uint64_t G = plan.bucket_order.size();
     g_end = std::min(g_end, G);
-    uint64_t max_m = 0, total_batches = 0;
-    for (uint64_t g = g_begin; g < g_end; ++g) {
-      const auto [bi, bj] = plan.bucket_order[g];
-      const uint64_t b = uint64_t(bi) * n + bj;
-      const uint64_t m = offsets[b + 1] - offsets[b];
-      max_m = std::max(max_m, m);
-      total_batches += (m + opt.batch_size - 1) / opt.batch_size;
-    }
-    ensure_bucket(max_m);
-    ensure_batch(std::min<uint64_t>(opt.batch_size, std::max<uint64_t>(max_m, 1)));
-    batch_losses.reserve(std::max<uint64_t>(total_batches, 1));
-    auto bucket_span = [&](uint64_t g, uint64_t& off) {
-      const auto [bi, bj] = plan.bucket_order[g];
-      const uint64_t b = uint64_t(bi) * n + bj;
-      off = offsets[b];
-      return offsets[b + 1] - off;
-    };
-    auto next_nonempty = [&](uint64_t g) {
-      uint64_t off;
-      while (g < g_end && bucket_span(g, off) == 0) ++g;
-      return g;
-    };
-    int stage = 0;
-    uint64_t h2d_bytes = 0;
-    auto issue_copy = [&](uint64_t g, int slot) {
-      uint64_t off;
-      const uint64_t m = bucket_span(g, off);
-      LGD_CUDA(cudaStreamWaitEvent(copy_stream, stage_free[slot], 0));
-      LGD_CUDA(cudaMemcpyAsync(staging[slot].get(), host_bucketed + 3 * off, m * 12,
-                               cudaMemcpyHostToDevice, copy_stream));
-      LGD_CUDA(cudaEventRecord(copy_done[slot], copy_stream));
-      h2d_bytes += m * 12;
-    };
-    LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
-    LGD_CUDA(cudaEventRecord(ev_begin, stream));
-    if (host_bucketed) {
-      staging[0].reserve(max_m * 3);
-      staging[1].reserve(max_m * 3);
-      const uint64_t g0 = next_nonempty(g_begin);
-      LGD_CUDA(cudaEventRecord(stage_free[0], stream));
-      LGD_CUDA(cudaEventRecord(stage_free[1], stream));
-      if (g0 < g_end) issue_copy(g0, 0);
-    }
-
-    uint64_t nb = 0, edges_trained = 0, buckets = 0;
     size_t st = 0;
-    const uint32_t kk = k();
     for (uint64_t g = g_begin; g < g_end; ++g) {
       while (st + 1 < plan.seq.states.size() && g >= plan.state_offsets[st + 1]) ++st;
       const auto [bi, bj] = plan.bucket_order[g];
-      const uint64_t b = uint64_t(bi) * n + bj;
-      const uint64_t off = offsets[b];
-      const uint64_t m = offsets[b + 1] - off;
-      if (m == 0) continue;  // pipeline.cpp:291, before the RNG is created
-      const Pool pool = pool_of_state(st);
-      StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, g)), pos.get(),
-                      reject.get()};
-      cudaEvent_t* bev = profiling ? prof_ev(prof_slot(2)) : nullptr;
-      if (bev) LGD_CUDA(cudaEventRecord(bev[0], stream));
-      LGD_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(uint64_t), stream));
-      const uint32_t* bucket_edges = edges_bucketed.get() + 3 * off;
-      if (host_bucketed) {
-        LGD_CUDA(cudaStreamWaitEvent(stream, copy_done[stage], 0));
-        bucket_edges = staging[stage].get();
-        const uint64_t gn = next_nonempty(g + 1);
-        if (gn < g_end) issue_copy(gn, stage ^ 1);
-      }
-      if (opt.shuffle) {
-        launch_shuffle_draws(slot, m, H.get(), stream);
-        ShuffleScratch s{sh_keys_in.get(), sh_vals_in.get(), sh_keys_out.get(), sh_vals_out.get(),
-                         sh_ptr.get(),     sh_G.get(),       sh_temp.get(),     sh_temp.bytes()};
-        launch_shuffle_permutation(H.get(), m, s, perm.get(), stream);
-        launch_gather_edges(bucket_edges, perm.get(), m, shuffled.get(), stream);
-        launches += 2 + 5 + 2 + (bits_for(m) + 7) / 8 + 1;
-      } else {
-        launch_gather_edges(bucket_edges, nullptr, m, shuffled.get(), stream);
-        launches += 1;
-      }
-      if (host_bucketed) {
-        LGD_CUDA(cudaEventRecord(stage_free[stage], stream));
-        stage ^= 1;
-      }
-      if (bev) LGD_CUDA(cudaEventRecord(bev[1], stream));
-      launch_sample_nodes(slot, m * kk, pool, negs.get(), stream);
-      launches += 2;
-      if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
-      for (uint64_t o = 0; o < m; o += opt.batch_size) {
-        const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
-        run_batch(shuffled.get() + 3 * o, negs.get() + o * kk, P, batch_losses.get() + nb, &pool);
-        ++nb;
-      }
-      edges_trained += m;
-      ++buckets;
+      items.push_back({bi, bj, g, pool_of_state(st)});
     }
+    return items;
+  }
+
+  uint64_t bucket_size(const WorkItem& it, uint64_t* off = nullptr) const {
+    const uint64_t b = uint64_t(it.bi) * n + it.bj;
+    if (off) *off = offsets[b];
+    return offsets[b + 1] - offsets[b];
+  }
+
+  // Shuffle draws + permutation + gather, then the bucket's m*k negative
+  // draws, all from the bucket's stream (pipeline.cpp:296-308).
+  void prepare_bucket(const WorkItem& it, uint32_t epoch, const uint32_t* bucket_edges, uint64_t m,
+                      cudaEvent_t* bev) {
+    StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, it.g)), pos.get(),
+                    reject.get()};
+    if (bev) LGD_CUDA(cudaEventRecord(bev[0], stream));
+    LGD_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(uint64_t), stream));
+    if (opt.shuffle) {
+      launch_shuffle_draws(slot, m, H.get(), stream);
+      ShuffleScratch s{sh_keys_in.get(), sh_vals_in.get(), sh_keys_out.get(), sh_vals_out.get(),
+                       sh_ptr.get(),     sh_G.get(),       sh_temp.get(),     sh_temp.bytes()};
+      launch_shuffle_permutation(H.get(), m, s, perm.get(), stream);
+      launch_gather_edges(bucket_edges, perm.get(), m, shuffled.get(), stream);
+      launches += 2 + 5 + 2 + (bits_for(m) + 7) / 8 + 1;
+    } else {
+      launch_gather_edges(bucket_edges, nullptr, m, shuffled.get(), stream);
+      launches += 1;
+    }
+  }
+  void sample_bucket(const WorkItem& it, uint32_t epoch, uint64_t m, cudaEvent_t* bev) {
+    (void)epoch;
+    StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, it.g)), pos.get(),
+                    reject.get()};
+    if (bev) LGD_CUDA(cudaEventRecord(bev[1], stream));
+    launch_sample_nodes(slot, m * k(), it.pool, negs.get(), stream);
+    launches += 2;
+    if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
+  }
+
+  void reserve_for(const std::vector<WorkItem>& items, uint64_t* total_batches) {
+    uint64_t max_m = 0, tb = 0;
+    for (const auto& it : items) {
+      const uint64_t m = bucket_size(it);
+      max_m = std::max(max_m, m);
+      tb += (m + opt.batch_size - 1) / opt.batch_size;
+    }
+    ensure_bucket(max_m);
+    ensure_batch(std::min<uint64_t>(opt.batch_size, std::max<uint64_t>(max_m, 1)));
+    batch_losses.reserve(std::max<uint64_t>(tb, 1));
+    if (total_batches) *total_batches = tb;
+  }
+
+  void fill_result(lgd_epoch_result* out, uint64_t nb, uint64_t edges_trained, uint64_t buckets,
+                   uint64_t h2d_bytes, std::chrono::steady_clock::time_point t0) {
     LGD_CUDA(cudaEventRecord(ev_end, stream));
     LGD_CUDA(cudaStreamSynchronize(stream));
     prof_flush();
@@ -464,6 +454,7 @@ struct lgd_context {
       kstats[LGD_KSTAT_REL].algorithmic_bytes += 16.0 * dim * double(cnt[1]);
     }
     if (out) {
+      const uint32_t kk = k();
       std::memset(out, 0, sizeof *out);
       out->loss_sum = loss_sum;
       out->edges_trained = edges_trained;
@@ -481,6 +472,161 @@ struct lgd_context {
           double(edges_trained) * (12.0 + 4.0 * dim * (2 + kk + (typed() ? 1 : 0))) +
           16.0 * dim * double(cnt[0] + cnt[1]);
     }
+  }
+
+  // Trains a list of buckets in order.  host_bucketed: optional host copy
+  // (pinned for full speed) of the edges in bucket order; each bucket is then
+  // streamed H2D on a side stream, one bucket ahead of the compute.
+  void train_items(uint32_t epoch, const std::vector<WorkItem>& items, lgd_epoch_result* out,
+                   const uint32_t* host_bucketed = nullptr) {
+    check_ready();
+    const auto t0 = std::chrono::steady_clock::now();
+    reserve_for(items, nullptr);
+    uint64_t max_m = 0;
+    for (const auto& it : items) max_m = std::max(max_m, bucket_size(it));
+    auto next_nonempty = [&](size_t i) {
+      while (i < items.size() && bucket_size(items[i]) == 0) ++i;
+      return i;
+    };
+    int stage = 0;
+    uint64_t h2d_bytes = 0;
+    auto issue_copy = [&](size_t i, int slot) {
+      uint64_t off;
+      const uint64_t m = bucket_size(items[i], &off);
+      LGD_CUDA(cudaStreamWaitEvent(copy_stream, stage_free[slot], 0));
+      LGD_CUDA(cudaMemcpyAsync(staging[slot].get(), host_bucketed + 3 * off, m * 12,
+                               cudaMemcpyHostToDevice, copy_stream));
+      LGD_CUDA(cudaEventRecord(copy_done[slot], copy_stream));
+      h2d_bytes += m * 12;
+    };
+    LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
+    LGD_CUDA(cudaEventRecord(ev_begin, stream));
+    if (host_bucketed) {
+      staging[0].reserve(max_m * 3);
+      staging[1].reserve(max_m * 3);
+      const size_t i0 = next_nonempty(0);
+      LGD_CUDA(cudaEventRecord(stage_free[0], stream));
+      LGD_CUDA(cudaEventRecord(stage_free[1], stream));
+      if (i0 < items.size()) issue_copy(i0, 0);
+    }
+    uint64_t nb = 0, edges_trained = 0, buckets = 0;
+    const uint32_t kk = k();
+    for (size_t idx = 0; idx < items.size(); ++idx) {
+      const WorkItem& it = items[idx];
+      uint64_t off;
+      const uint64_t m = bucket_size(it, &off);
+      if (m == 0) continue;  // pipeline.cpp:291, before the RNG is created
+      cudaEvent_t* bev = profiling ? prof_ev(prof_slot(2)) : nullptr;
+      const uint32_t* bucket_edges = edges_bucketed.get() + 3 * off;
+      if (host_bucketed) {
+        LGD_CUDA(cudaStreamWaitEvent(stream, copy_done[stage], 0));
+        bucket_edges = staging[stage].get();
+        const size_t in = next_nonempty(idx + 1);
+        if (in < items.size()) issue_copy(in, stage ^ 1);
+      }
+      prepare_bucket(it, epoch, bucket_edges, m, bev);
+      if (host_bucketed) {
+        LGD_CUDA(cudaEventRecord(stage_free[stage], stream));
+        stage ^= 1;
+      }
+      sample_bucket(it, epoch, m, bev);
+      for (uint64_t o = 0; o < m; o += opt.batch_size) {
+        const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
+        run_batch(shuffled.get() + 3 * o, negs.get() + o * kk, P, batch_losses.get() + nb,
+                  &it.pool);
+        ++nb;
+      }
+      edges_trained += m;
+      ++buckets;
+    }
+    fill_result(out, nb, edges_trained, buckets, h2d_bytes, t0);
+  }
+
+  void train_range(uint32_t epoch, uint64_t g_begin, uint64_t g_end, lgd_epoch_result* out,
+                   const uint32_t* host_bucketed = nullptr) {
+    check_ready();
+    train_items(epoch, plan_items(g_begin, g_end), out, host_bucketed);
+  }
+
+  // ---- lock-step rounds (multi-GPU, typed models): this rank's batches are
+  // run one at a time; after each, the caller sums the dense relation
+  // gradient [R x (d+1)] (last column: touched flag) across ranks and hands
+  // the sum back for one identical relation Adagrad step on every rank.
+  std::vector<WorkItem> round_items;
+  std::vector<uint64_t> round_first_batch;  // per item, prefix of batch counts
+  uint64_t round_batches = 0, round_nb = 0, round_edges = 0, round_buckets = 0;
+  uint32_t round_epoch = 0;
+  size_t round_prepared = ~size_t(0);
+  std::chrono::steady_clock::time_point round_t0;
+  DevBuf<double> rel_grad;
+  DevBuf<uint8_t> rel_flag;
+
+  uint64_t round_begin(uint32_t epoch, std::vector<WorkItem> items) {
+    check_ready();
+    round_t0 = std::chrono::steady_clock::now();
+    round_items = std::move(items);
+    round_first_batch.assign(round_items.size() + 1, 0);
+    for (size_t i = 0; i < round_items.size(); ++i) {
+      const uint64_t m = bucket_size(round_items[i]);
+      round_first_batch[i + 1] = round_first_batch[i] + (m + opt.batch_size - 1) / opt.batch_size;
+    }
+    round_batches = round_first_batch.back();
+    reserve_for(round_items, nullptr);
+    rel_grad.reserve(std::max<uint64_t>(R, 1) * dim);
+    rel_flag.reserve(std::max<uint64_t>(R, 1));
+    round_epoch = epoch;
+    round_prepared = ~size_t(0);
+    round_nb = round_edges = round_buckets = 0;
+    LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
+    LGD_CUDA(cudaEventRecord(ev_begin, stream));
+    return round_batches;
+  }
+
+  // Lock-step batch `step` of this rank (a no-op past its last batch); the
+  // dense relation gradient lands in rel_out [R x (d+1)] (device).
+  void round_step(uint64_t step, double* rel_out) {
+    const uint64_t rows = std::max<uint64_t>(R, 1);
+    LGD_CUDA(cudaMemsetAsync(rel_grad.get(), 0, rows * dim * 8, stream));
+    LGD_CUDA(cudaMemsetAsync(rel_flag.get(), 0, rows, stream));
+    if (step < round_batches) {
+      const size_t i = std::upper_bound(round_first_batch.begin(), round_first_batch.end(), step) -
+                       round_first_batch.begin() - 1;
+      const WorkItem& it = round_items[i];
+      uint64_t off;
+      const uint64_t m = bucket_size(it, &off);
+      if (round_prepared != i) {
+        prepare_bucket(it, round_epoch, edges_bucketed.get() + 3 * off, m, nullptr);
+        sample_bucket(it, round_epoch, m, nullptr);
+        round_prepared = i;
+        round_edges += m;
+        ++round_buckets;
+      }
+      const uint64_t o = (step - round_first_batch[i]) * opt.batch_size;
+      const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
+      BatchArgs a = batch_args(shuffled.get() + 3 * o, negs.get() + o * k(), P,
+                               batch_losses.get() + round_nb, &it.pool);
+      if (typed()) {
+        a.grad_rels = rel_grad.get();
+        a.grad_rel_flag = rel_flag.get();
+      }
+      launch_train_batch(a, stream, nullptr);
+      launches += batch_launches(a.node_key_bits);
+      ++round_nb;
+    }
+    if (rel_out) launch_rel_pack(rel_grad.get(), rel_flag.get(), R, dim, rel_out, stream);
+    LGD_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  void round_apply_relations(const double* summed) {
+    if (typed() && R) {
+      launch_rel_apply(summed, rel_theta.get(), rel_state.get(), R, dim, opt.learning_rate,
+                       opt.adagrad_epsilon, stream);
+      LGD_CUDA(cudaStreamSynchronize(stream));
+    }
+  }
+
+  void round_end(lgd_epoch_result* out) {
+    fill_result(out, round_nb, round_edges, round_buckets, 0, round_t0);
   }
 
   // Operator-level batch on host inputs (validated like batch_loss,
@@ -906,6 +1052,97 @@ int lgd_train_buckets(lgd_context* ctx, uint32_t epoch, uint64_t g_begin, uint64
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
     ctx->train_range(epoch, g_begin, g_end, out);
+  });
+}
+
+int lgd_round_schedule(uint32_t n, uint64_t capacity, uint64_t* count, lgd_bucket_item* items,
+                       uint32_t* num_rounds, uint32_t* pairs_per_round) {
+  return guarded([&] {
+    const RoundSchedule rs = make_round_schedule(n);
+    if (count) *count = rs.buckets.size();
+    if (num_rounds) *num_rounds = rs.num_rounds;
+    if (pairs_per_round) *pairs_per_round = rs.pairs_per_round;
+    if (capacity < rs.buckets.size() || !items) return;
+    for (size_t i = 0; i < rs.buckets.size(); ++i) {
+      const auto& b = rs.buckets[i];
+      items[i] = lgd_bucket_item{b.src, b.dst, b.g, {b.pool[0], b.pool[1], kNoPartition},
+                                 b.round, b.pair};
+    }
+  });
+}
+
+static std::vector<lgd_context::WorkItem> work_items(const lgd_context* ctx,
+                                                     const lgd_bucket_item* items, uint64_t count) {
+  std::vector<lgd_context::WorkItem> out;
+  for (uint64_t i = 0; i < count; ++i) {
+    const auto& it = items[i];
+    if (it.src_part >= ctx->n || it.dst_part >= ctx->n)
+      throw std::invalid_argument("bucket partition out of range");
+    const Pool pool = ctx->pool_of_parts(it.pool, 3);
+    // both endpoints of the bucket must be in its pool (resident)
+    auto in_pool = [&](uint32_t p) {
+      return it.pool[0] == p || it.pool[1] == p || it.pool[2] == p;
+    };
+    if (!in_pool(it.src_part) || !in_pool(it.dst_part))
+      throw std::invalid_argument("bucket scheduled while a partition is not resident");
+    out.push_back({it.src_part, it.dst_part, it.g, pool});
+  }
+  return out;
+}
+
+int lgd_train_items(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* items,
+                    uint64_t count, lgd_epoch_result* out) {
+  return guarded([&] {
+    if (!ctx || (!items && count)) throw std::invalid_argument("null argument");
+    if (!ctx->partitioned) throw std::invalid_argument("no partition plan");
+    DeviceGuard g(ctx->device);
+    ctx->train_items(epoch, work_items(ctx, items, count), out);
+  });
+}
+
+int lgd_round_begin(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* items,
+                    uint64_t count, uint64_t* my_batches) {
+  return guarded([&] {
+    if (!ctx || (!items && count)) throw std::invalid_argument("null argument");
+    if (!ctx->partitioned) throw std::invalid_argument("no partition plan");
+    DeviceGuard g(ctx->device);
+    const uint64_t b = ctx->round_begin(epoch, work_items(ctx, items, count));
+    if (my_batches) *my_batches = b;
+  });
+}
+
+int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard g(ctx->device);
+    ctx->round_step(step, rel_grad_device);
+  });
+}
+
+int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device) {
+  return guarded([&] {
+    if (!ctx || !summed_device) throw std::invalid_argument("null argument");
+    DeviceGuard g(ctx->device);
+    ctx->round_apply_relations(summed_device);
+  });
+}
+
+int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard g(ctx->device);
+    ctx->round_end(out);
+  });
+}
+
+int lgd_device_tables(lgd_context* ctx, float** theta, float** state, float** rel_theta,
+                      float** rel_state) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (theta) *theta = ctx->theta.get();
+    if (state) *state = ctx->state.get();
+    if (rel_theta) *rel_theta = ctx->rel_theta.get();
+    if (rel_state) *rel_state = ctx->rel_state.get();
   });
 }
 

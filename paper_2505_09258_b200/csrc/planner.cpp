@@ -276,6 +276,53 @@ IterationPlan make_iteration_plan(const LoadingOrder& seq, uint32_t n) {
   return plan;
 }
 
+RoundSchedule make_round_schedule(uint32_t n) {
+  if (n < 1) throw std::invalid_argument("partition count must be >= 1");
+  RoundSchedule rs;
+  rs.n = n;
+  if (n == 1) {
+    rs.num_rounds = 1;
+    rs.pairs_per_round = 1;
+    rs.buckets.push_back({0, 0, 0, {0, kNoPartition}, 0, 0});
+    return rs;
+  }
+  const uint32_t m = n + (n & 1);  // even player count; player n (odd n) is the bye
+  rs.num_rounds = m - 1;
+  rs.pairs_per_round = m / 2;
+  std::vector<uint8_t> diag_done(n, 0);
+  uint64_t g = 0;
+  for (uint32_t r = 0; r < m - 1; ++r) {
+    // circle method: player m-1 fixed, the others rotate
+    std::vector<std::pair<uint32_t, uint32_t>> pairs;
+    pairs.push_back({r, m - 1});
+    for (uint32_t i = 1; i < m / 2; ++i)
+      pairs.push_back({(r + i) % (m - 1), (r + m - 1 - i) % (m - 1)});
+    uint32_t j = 0;
+    for (auto [x, y] : pairs) {
+      const uint32_t a = std::min(x, y), b = std::max(x, y);
+      if (b >= n) {  // bye: a still gets its diagonal when first seen
+        if (!diag_done[a]) {
+          diag_done[a] = 1;
+          rs.buckets.push_back({a, a, g++, {a, kNoPartition}, r, j});
+        }
+        ++j;
+        continue;
+      }
+      const uint32_t pool[2] = {a, b};
+      for (uint32_t q : {a, b}) {
+        if (!diag_done[q]) {
+          diag_done[q] = 1;
+          rs.buckets.push_back({q, q, g++, {pool[0], pool[1]}, r, j});
+        }
+      }
+      rs.buckets.push_back({a, b, g++, {pool[0], pool[1]}, r, j});
+      rs.buckets.push_back({b, a, g++, {pool[0], pool[1]}, r, j});
+      ++j;
+    }
+  }
+  return rs;
+}
+
 IterationPlan single_state_plan(uint32_t n) {
   if (n < 1 || n > 3) throw std::invalid_argument("single-state plan is for n <= 3");
   IterationPlan plan;

@@ -29,6 +29,28 @@ struct IterationPlan {
   std::vector<uint64_t> prefetch_points;                    // states - 1
 };
 
+// Multi-GPU partition-round schedule: rounds of disjoint
+// partition pairs (circle method; odd n gets a bye per round).  Every bucket
+// appears exactly once: (a,b) and (b,a) in the round pairing a and b, the
+// diagonal (a,a) in the first round that holds a.  Buckets are numbered in
+// one global order (round, pair, [diagonals], (a,b), (b,a)); that position
+// keys the bucket's RNG stream, and the pair {a,b} is its negative pool, so
+// the epoch is the same for any number of GPUs.  Pair j of a round runs on
+// rank j % num_ranks.
+struct RoundBucket {
+  uint32_t src, dst;     // bucket (i, j)
+  uint64_t g;            // global position (RNG stream index)
+  uint32_t pool[2];      // the pair {a, b}, ascending (pool[1] = none for n = 1)
+  uint32_t round, pair;
+};
+struct RoundSchedule {
+  uint32_t n = 0;
+  uint32_t num_rounds = 0;
+  uint32_t pairs_per_round = 0;
+  std::vector<RoundBucket> buckets;  // global order
+};
+RoundSchedule make_round_schedule(uint32_t n);
+
 LoadingOrder make_loading_order(uint32_t n);
 IterationPlan make_iteration_plan(const LoadingOrder& seq, uint32_t n);
 IterationPlan single_state_plan(uint32_t n);

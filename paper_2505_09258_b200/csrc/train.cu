@@ -1066,7 +1066,44 @@ void run_kind(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   throw std::invalid_argument("embedding dimension too large (max 256, ComplEx 512)");
 }
 
+__global__ void rel_pack_kernel(const double* __restrict__ grad, const uint8_t* __restrict__ flag,
+                                uint64_t R, uint32_t d, double* __restrict__ out) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R * (d + 1)) return;
+  const uint64_t r = t / (d + 1), i = t - r * (d + 1);
+  out[t] = i < d ? grad[r * d + i] : (flag[r] ? 1.0 : 0.0);
+}
+
+__global__ void rel_apply_kernel(const double* __restrict__ summed, float* __restrict__ th,
+                                 float* __restrict__ st, uint64_t R, uint32_t d, double lr,
+                                 double eps) {
+  const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= R || summed[r * (d + 1) + d] <= 0.0) return;  // row untouched by every rank
+  for (uint32_t i = lane; i < d; i += 32) {
+    float tv = th[r * d + i], sv = st[r * d + i];
+    adagrad_fast(summed[r * (d + 1) + i], tv, sv, lr, eps);
+    th[r * d + i] = tv;
+    st[r * d + i] = sv;
+  }
+}
+
 }  // namespace
+
+void launch_rel_pack(const double* grad, const uint8_t* flag, uint64_t R, uint32_t d, double* out,
+                     cudaStream_t st) {
+  if (!R) return;
+  rel_pack_kernel<<<ceil_div(R * (d + 1), 256), 256, 0, st>>>(grad, flag, R, d, out);
+  LGD_LAUNCH_CHECK();
+}
+
+void launch_rel_apply(const double* summed, float* rel_theta, float* rel_state, uint64_t R,
+                      uint32_t d, double lr, double eps, cudaStream_t st) {
+  if (!R) return;
+  rel_apply_kernel<<<ceil_div(R * 32, 256), 256, 0, st>>>(summed, rel_theta, rel_state, R, d, lr,
+                                                           eps);
+  LGD_LAUNCH_CHECK();
+}
 
 size_t batch_sort_temp_bytes(uint64_t max_items) {
   size_t bytes = 0;

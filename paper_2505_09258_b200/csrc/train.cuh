@@ -65,5 +65,12 @@ size_t batch_sort_temp_bytes(uint64_t max_items);
 size_t score_smem_bytes(uint32_t dim, uint32_t k);
 // K3 -> loss reduce -> sort -> K4 (pass 1, 2) -> relation path.
 void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev);
+// Multi-GPU lock-step relations: pack a dense gradient [R x d] + touched
+// flags into [R x (d+1)] (the buffer the ranks sum), and apply one Adagrad
+// step to every touched row from a summed buffer.
+void launch_rel_pack(const double* grad, const uint8_t* flag, uint64_t R, uint32_t d, double* out,
+                     cudaStream_t st);
+void launch_rel_apply(const double* summed, float* rel_theta, float* rel_state, uint64_t R,
+                      uint32_t d, double lr, double eps, cudaStream_t st);
 
 }  // namespace lgd

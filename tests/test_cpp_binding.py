@@ -1,0 +1,35 @@
+"""The header-only C++ binding (include/legend_b200.hpp) compiles against the
+C ABI, maps error codes onto the reference's exception classes, and refuses to
+run without a GPU.  The GPU variant trains one epoch through it."""
+import os
+import subprocess
+
+import pytest
+from conftest import ROOT
+
+
+def build(tmp_path):
+    exe = tmp_path / "binding_smoke"
+    libdir = os.path.join(ROOT, "paper_2505_09258_b200")
+    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "binding_smoke.cpp"), "-L", libdir,
+                           "-llegend_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    return exe
+
+
+def test_cpp_binding_without_gpu(tmp_path):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    exe = build(tmp_path)
+    out = subprocess.run([str(exe), "0"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "runtime_error" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_binding_epoch(tmp_path):
+    exe = build(tmp_path)
+    out = subprocess.run([str(exe), "1"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "epoch ok: 500 edges" in out.stdout
