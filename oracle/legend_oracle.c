@@ -306,11 +306,29 @@ static int check_model(int kind, uint32_t dim) {
  * positive dst, negatives j ascending, then src.  Optional outputs: the sorted
  * unique node / relation ids and their FP64 gradients.
  */
+static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes,
+                       float* relE, float* relS, uint64_t num_rels, const uint32_t* edges,
+                       uint64_t P, const uint32_t* negs, uint32_t k, double lr, double eps,
+                       int apply_nodes, int apply_rels, double* loss_out, uint64_t* n_nodes_out,
+                       uint32_t* node_ids, double* node_grads, uint64_t* n_rels_out,
+                       uint32_t* rel_ids, double* rel_grads);
+
 int lo_batch(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes, float* relE,
              float* relS, uint64_t num_rels, const uint32_t* edges, uint64_t P,
              const uint32_t* negs, uint32_t k, double lr, double eps, int apply, double* loss_out,
              uint64_t* n_nodes_out, uint32_t* node_ids, double* node_grads, uint64_t* n_rels_out,
              uint32_t* rel_ids, double* rel_grads) {
+  return lo_batch_ex(kind, d, E, S, num_nodes, relE, relS, num_rels, edges, P, negs, k, lr, eps,
+                     apply, apply, loss_out, n_nodes_out, node_ids, node_grads, n_rels_out,
+                     rel_ids, rel_grads);
+}
+
+static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes,
+                       float* relE, float* relS, uint64_t num_rels, const uint32_t* edges,
+                       uint64_t P, const uint32_t* negs, uint32_t k, double lr, double eps,
+                       int apply_nodes, int apply_rels, double* loss_out, uint64_t* n_nodes_out,
+                       uint32_t* node_ids, double* node_grads, uint64_t* n_rels_out,
+                       uint32_t* rel_ids, double* rel_grads) {
   int rc = check_model(kind, d);
   if (rc) return rc;
   if (k == 0) return LO_INVALID; /* train.cpp:219-221 */
@@ -463,13 +481,14 @@ int lo_batch(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes, float
   if (rel_ids && n_rels) memcpy(rel_ids, rid, n_rels * sizeof(uint32_t));
   if (rel_grads && n_rels) memcpy(rel_grads, rall, n_rels * d * sizeof(double));
 
-  if (apply) { /* train.cpp:356-363: nodes ascending, then relations */
+  /* train.cpp:356-363: nodes ascending, then relations */
+  if (apply_nodes)
     for (uint64_t u = 0; u < n_nodes; ++u)
       adagrad_row(E + (uint64_t)gid[u] * d, S + (uint64_t)gid[u] * d, gall + u * d, d, lr, eps);
+  if (apply_rels)
     for (uint64_t u = 0; u < n_rels; ++u)
       adagrad_row(relE + (uint64_t)rid[u] * d, relS + (uint64_t)rid[u] * d, rall + u * d, d, lr,
                   eps);
-  }
   if (loss_out) *loss_out = loss;
   free(ir1), free(w), free(f), free(con), free(mixes), free(rowsum), free(g), free(gall),
       free(gid);
@@ -731,4 +750,168 @@ int lo_bucket_sample(const uint32_t* bucket_edges, uint64_t m, const uint64_t* f
   *loss_sum = total;
   *edges_trained = done;
   return rc;
+}
+
+/*
+ * Serialized restatement of the multi-GPU partition-round schedule
+ * (SURVEY.md 8(e)).  items: count buckets in global order with
+ * (src_part, dst_part, g, pool[3], round, pair) flattened as 8 u64 each;
+ * bucket g uses the stream Rng(derive_seed(seed, "bukt", epoch, g)) and
+ * samples negatives from its pool.  Pair j of a round runs on rank
+ * j % num_ranks; a rank's batches (its buckets in order, shuffled, sliced)
+ * run in lock step with the other ranks': at step k every rank's batch k
+ * applies its node gradients (ranks own disjoint partitions) and the ranks'
+ * relation gradients are summed in rank order, then one Adagrad step updates
+ * every relation row any rank touched.
+ */
+typedef struct {
+  uint64_t m, off;          /* bucket size and offset in edge_order */
+  uint32_t* edges;          /* shuffled copy */
+  uint32_t* negs;           /* m * k negative ids */
+} lo_prepared;
+
+int lo_run_rounds(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
+                  uint64_t num_rels, uint32_t n, const uint64_t* items, uint64_t count,
+                  uint32_t num_ranks, int kind, uint32_t d, double lr, double eps,
+                  uint32_t batch_size, uint32_t k, int shuffle, uint64_t seed, uint32_t epoch,
+                  float* E, float* S, float* relE, float* relS, double* loss_sum_out,
+                  uint64_t* edges_trained_out) {
+  int rc = check_model(kind, d);
+  if (rc) return rc;
+  if (kind != LO_KIND_DOT && num_rels == 0) return LO_INVALID;
+  uint64_t stride = 0;
+  uint64_t* offsets = (uint64_t*)malloc(((uint64_t)n * n + 1) * sizeof(uint64_t));
+  uint64_t* order = (uint64_t*)malloc((num_edges ? num_edges : 1) * sizeof(uint64_t));
+  rc = lo_partition_plan(edges, num_edges, num_nodes, n, &stride, offsets, order);
+  if (rc) {
+    free(offsets), free(order);
+    return rc;
+  }
+  const int typed = kind != LO_KIND_DOT;
+  double* rsum = typed ? (double*)malloc(num_rels * d * sizeof(double)) : NULL;
+  uint8_t* rtouch = typed ? (uint8_t*)malloc(num_rels) : NULL;
+  uint32_t* rid = typed ? (uint32_t*)malloc(((uint64_t)batch_size + 1) * sizeof(uint32_t)) : NULL;
+  double* rg = typed ? (double*)malloc(((uint64_t)batch_size + 1) * d * sizeof(double)) : NULL;
+  double loss_sum = 0.0;
+  uint64_t edges_trained = 0;
+  uint64_t i0 = 0;
+  while (i0 < count && rc == 0) {
+    const uint64_t round = items[8 * i0 + 6];
+    uint64_t i1 = i0;
+    while (i1 < count && items[8 * i1 + 6] == round) ++i1;
+    /* per rank: prepare its buckets (shuffle + all negatives, stream order) */
+    lo_prepared* prep = (lo_prepared*)calloc(i1 - i0, sizeof(lo_prepared));
+    uint64_t* nbat = (uint64_t*)calloc(num_ranks, sizeof(uint64_t));
+    for (uint64_t it = i0; it < i1; ++it) {
+      const uint64_t* I = items + 8 * it;
+      const uint64_t b = I[0] * n + I[1];
+      lo_prepared* P = prep + (it - i0);
+      P->off = offsets[b];
+      P->m = offsets[b + 1] - offsets[b];
+      nbat[I[7] % num_ranks] += (P->m + batch_size - 1) / batch_size;
+      if (!P->m) continue;
+      P->edges = (uint32_t*)malloc(P->m * 3 * sizeof(uint32_t));
+      P->negs = (uint32_t*)malloc(P->m * k * sizeof(uint32_t));
+      for (uint64_t e = 0; e < P->m; ++e)
+        memcpy(P->edges + 3 * e, edges + 3 * order[P->off + e], 3 * sizeof(uint32_t));
+      lo_rng rng;
+      lo_rng_init(&rng, lo_derive_seed(seed, 0x62756b74ull, epoch, I[2]));
+      if (shuffle)
+        for (uint64_t i = P->m; i > 1; --i) {
+          const uint64_t j = lo_rng_below(&rng, i);
+          uint32_t t[3];
+          memcpy(t, P->edges + 3 * (i - 1), sizeof t);
+          memcpy(P->edges + 3 * (i - 1), P->edges + 3 * j, sizeof t);
+          memcpy(P->edges + 3 * j, t, sizeof t);
+        }
+      uint64_t first[3], cnt[3];
+      int np = 0;
+      uint32_t ids[3];
+      for (int q = 0; q < 3; ++q)
+        if ((uint32_t)I[3 + q] != 0xffffffffu) ids[np++] = (uint32_t)I[3 + q];
+      for (int a = 0; a < np; ++a)
+        for (int c = a + 1; c < np; ++c)
+          if (ids[c] < ids[a]) {
+            uint32_t t = ids[a];
+            ids[a] = ids[c];
+            ids[c] = t;
+          }
+      for (int a = 0; a < np; ++a) {
+        first[a] = stride * ids[a];
+        uint64_t end = stride * (ids[a] + 1);
+        if (end > num_nodes) end = num_nodes;
+        cnt[a] = end - first[a];
+      }
+      rc = lo_sample_negatives_rng(first, cnt, np, k, P->m, &rng, P->negs);
+      if (rc) break;
+    }
+    uint64_t steps = 0;
+    for (uint32_t r = 0; r < num_ranks; ++r) steps = nbat[r] > steps ? nbat[r] : steps;
+    for (uint64_t st = 0; st < steps && rc == 0; ++st) {
+      if (typed) {
+        memset(rsum, 0, num_rels * d * sizeof(double));
+        memset(rtouch, 0, num_rels);
+      }
+      for (uint32_t r = 0; r < num_ranks && rc == 0; ++r) {
+        /* this rank's batch st: walk its buckets in global order */
+        uint64_t seen = 0;
+        for (uint64_t it = i0; it < i1; ++it) {
+          if (items[8 * it + 7] % num_ranks != r) continue;
+          lo_prepared* P = prep + (it - i0);
+          const uint64_t nb = (P->m + batch_size - 1) / batch_size;
+          if (st < seen + nb) {
+            const uint64_t off = (st - seen) * batch_size;
+            const uint64_t cntp = (P->m - off) < batch_size ? (P->m - off) : batch_size;
+            double l = 0.0;
+            uint64_t nr = 0;
+            rc = lo_batch_ex(kind, d, E, S, num_nodes, relE, relS, num_rels, P->edges + 3 * off,
+                             cntp, P->negs + off * k, k, lr, eps, 1, 0, &l, NULL, NULL, NULL,
+                             &nr, rid, rg);
+            loss_sum += l;
+            edges_trained += cntp;
+            for (uint64_t u = 0; typed && u < nr; ++u) {
+              rtouch[rid[u]] = 1;
+              for (uint32_t e = 0; e < d; ++e) rsum[(uint64_t)rid[u] * d + e] += rg[u * d + e];
+            }
+            break;
+          }
+          seen += nb;
+        }
+      }
+      for (uint64_t q = 0; typed && q < num_rels; ++q)
+        if (rtouch[q])
+          adagrad_row(relE + q * d, relS + q * d, rsum + q * d, d, lr, eps);
+    }
+    for (uint64_t it = i0; it < i1; ++it) free(prep[it - i0].edges), free(prep[it - i0].negs);
+    free(prep), free(nbat);
+    i0 = i1;
+  }
+  free(offsets), free(order), free(rsum), free(rtouch), free(rid), free(rg);
+  *loss_sum_out = loss_sum;
+  *edges_trained_out = edges_trained;
+  return rc;
+}
+
+/* Exported pieces of the round restatement, for the CPU multi-rank tests:
+ * one batch with node and relation updates applied separately, and the
+ * relation Adagrad step over rows flagged as touched. */
+int lo_batch_split(int kind, uint32_t d, float* E, float* S, uint64_t num_nodes, float* relE,
+                   float* relS, uint64_t num_rels, const uint32_t* edges, uint64_t P,
+                   const uint32_t* negs, uint32_t k, double lr, double eps, int apply_nodes,
+                   int apply_rels, double* loss_out, uint64_t* n_rels_out, uint32_t* rel_ids,
+                   double* rel_grads) {
+  return lo_batch_ex(kind, d, E, S, num_nodes, relE, relS, num_rels, edges, P, negs, k, lr, eps,
+                     apply_nodes, apply_rels, loss_out, NULL, NULL, NULL, n_rels_out, rel_ids,
+                     rel_grads);
+}
+
+void lo_adagrad_touched(float* relE, float* relS, const double* summed, uint64_t R, uint32_t d,
+                        double lr, double eps) {
+  /* summed: R x (d+1), last column = touched flag (summed across ranks) */
+  for (uint64_t r = 0; r < R; ++r)
+    if (summed[r * (d + 1) + d] > 0.0) {
+      double g[4096];
+      for (uint32_t i = 0; i < d; ++i) g[i] = summed[r * (d + 1) + i];
+      adagrad_row(relE + r * d, relS + r * d, g, d, lr, eps);
+    }
 }

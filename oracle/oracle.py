@@ -69,6 +69,11 @@ class Oracle:
                                     vp, u64, vp, vp, u64, f64, f64, vp, vp])
         if which == "restatement":
             bind("shuffle_perm", None, [u64, u64, vp, vp])
+            bind("batch_split", i32, [i32, u32, vp, vp, u64, vp, vp, u64, vp, u64, vp, u32, f64,
+                                      f64, i32, i32, vp, vp, vp, vp])
+            bind("adagrad_touched", None, [vp, vp, vp, u64, u32, f64, f64])
+            bind("run_rounds", i32, [vp, u64, u64, u64, u32, vp, u64, u32, i32, u32, f64, f64,
+                                     u32, u32, i32, u64, u32, vp, vp, vp, vp, vp, vp])
             bind("store_init", None, [u32, u64, u32, u64, u64, vp, vp, vp, vp])
             bind("run_epoch", i32, [vp, u64, u64, u64, u32, u64, vp, vp, u64, vp, vp, vp, i32,
                                     u32, f64, f64, u32, u32, i32, u64, u32, vp, vp, vp, vp, vp,
@@ -253,6 +258,55 @@ class Oracle:
         """fill_uniform_rows (store.cpp:19-25) into a float32 slice (restatement)."""
         self.lib.lo_init_rows.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p]
         self.lib.lo_init_rows(stream_seed, rows, dim, _ptr(out))
+
+    def batch_nodes_only(self, kind, E, S, relE, relS, edges, negs, k, lr=0.1, eps=1e-10):
+        """batch_loss + batch_gradients; node Adagrad applied, relation
+        gradients returned as a dense [R x (d+1)] array (last column: touched)."""
+        kind = KINDS.get(kind, kind)
+        V, d = E.shape
+        R = relE.shape[0] if relE is not None else 0
+        edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
+        negs = np.ascontiguousarray(negs, np.uint32)
+        P = len(edges)
+        loss = np.zeros(1, np.float64)
+        nr = np.zeros(1, np.uint64)
+        rids = np.zeros(P + 1, np.uint32)
+        rg = np.zeros((P + 1, d), np.float64)
+        if relE is None:
+            relE = np.zeros((1, d), np.float32)
+            relS = np.zeros((1, d), np.float32)
+        self._check(self._fn["batch_split"](kind, d, _ptr(E), _ptr(S), V, _ptr(relE), _ptr(relS),
+                                            R, _ptr(edges), P, _ptr(negs), k, lr, eps, 1, 0,
+                                            _ptr(loss), _ptr(nr), _ptr(rids), _ptr(rg)))
+        dense = np.zeros((max(R, 1), d + 1), np.float64)
+        n = int(nr[0])
+        dense[rids[:n], :d] = rg[:n]
+        dense[rids[:n], d] = 1.0
+        return float(loss[0]), dense
+
+    def adagrad_touched(self, relE, relS, summed, lr=0.1, eps=1e-10):
+        R, d = relE.shape
+        summed = np.ascontiguousarray(summed, np.float64)
+        self._fn["adagrad_touched"](_ptr(relE), _ptr(relS), _ptr(summed), R, d, lr, eps)
+
+    def run_rounds(self, edges, num_nodes, num_rels, n, items, num_ranks, kind, E, S, relE, relS,
+                   *, dim, lr=0.1, eps=1e-10, batch_size=100000, k=16, shuffle=True, seed=42,
+                   epoch=0):
+        """Serialized multi-GPU round schedule (lock-step relation sums), in place.
+        items: (count, 8) u64 rows (src, dst, g, pool0, pool1, pool2, round, pair)."""
+        kind = KINDS.get(kind, kind)
+        edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
+        items = np.ascontiguousarray(items, np.uint64).reshape(-1, 8)
+        if relE is None or len(relE) == 0:
+            relE = np.zeros((1, dim), np.float32)
+            relS = np.zeros((1, dim), np.float32)
+        loss = np.zeros(1, np.float64)
+        et = np.zeros(1, np.uint64)
+        self._check(self._fn["run_rounds"](_ptr(edges), len(edges), num_nodes, num_rels, n,
+                                           _ptr(items), len(items), num_ranks, kind, dim, lr, eps,
+                                           batch_size, k, int(shuffle), seed, epoch, _ptr(E),
+                                           _ptr(S), _ptr(relE), _ptr(relS), _ptr(loss), _ptr(et)))
+        return {"loss_sum": float(loss[0]), "edges_trained": int(et[0])}
 
     def evaluate(self, kind, E, relE, test_edges, num_candidates=999, hits_k=10, seed=0):
         kind = KINDS.get(kind, kind)

@@ -296,8 +296,13 @@ struct lgd_context {
   }
 
   void run_batch(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P, double* loss_out,
-                 const Pool* pool = nullptr) {
+                 const Pool* pool = nullptr, double* rel_grad_out = nullptr,
+                 uint8_t* rel_flag_out = nullptr) {
     BatchArgs a = batch_args(bedges, bnegs, P, loss_out, pool);
+    if (rel_grad_out) {  // lock-step rounds: relation gradient only, applied later
+      a.grad_rels = rel_grad_out;
+      a.grad_rel_flag = rel_flag_out;
+    }
     if (profiling) {
       const int slot = prof_slot(1);
       BatchEvents ev;
@@ -603,14 +608,8 @@ struct lgd_context {
       }
       const uint64_t o = (step - round_first_batch[i]) * opt.batch_size;
       const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
-      BatchArgs a = batch_args(shuffled.get() + 3 * o, negs.get() + o * k(), P,
-                               batch_losses.get() + round_nb, &it.pool);
-      if (typed()) {
-        a.grad_rels = rel_grad.get();
-        a.grad_rel_flag = rel_flag.get();
-      }
-      launch_train_batch(a, stream, nullptr);
-      launches += batch_launches(a.node_key_bits);
+      run_batch(shuffled.get() + 3 * o, negs.get() + o * k(), P, batch_losses.get() + round_nb,
+                &it.pool, typed() ? rel_grad.get() : nullptr, typed() ? rel_flag.get() : nullptr);
       ++round_nb;
     }
     if (rel_out) launch_rel_pack(rel_grad.get(), rel_flag.get(), R, dim, rel_out, stream);

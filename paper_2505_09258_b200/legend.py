@@ -97,6 +97,13 @@ def library():
         "lgd_train_epoch": (i32, [vp, u32, vp]),
         "lgd_train_buckets": (i32, [vp, u32, u64, u64, vp]),
         "lgd_train_buckets_from_host": (i32, [vp, u32, u64, u64, vp, vp]),
+        "lgd_round_schedule": (i32, [u32, u64, vp, vp, vp, vp]),
+        "lgd_train_items": (i32, [vp, u32, vp, u64, vp]),
+        "lgd_round_begin": (i32, [vp, u32, vp, u64, vp]),
+        "lgd_round_step": (i32, [vp, u64, vp]),
+        "lgd_round_apply_relations": (i32, [vp, vp]),
+        "lgd_round_end": (i32, [vp, vp]),
+        "lgd_device_tables": (i32, [vp, vp, vp, vp, vp]),
         "lgd_get_bucketed_edges": (i32, [vp, vp]),
         "lgd_host_alloc": (i32, [u64, vp]),
         "lgd_host_free": (i32, [vp]),
@@ -286,6 +293,14 @@ def shuffle_permutation(seed, m, device=0):
     return perm[:m], int(used[0])
 
 
+class _CudaArray:
+    """__cuda_array_interface__ shim: wraps a device pointer of f32 values."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 class PinnedArray:
     """Page-locked host memory (cudaHostAlloc) viewed as a numpy array."""
 
@@ -472,6 +487,55 @@ class Trainer:
             out = np.zeros((self.num_edges, 3), np.uint32)
         _check(library().lgd_get_bucketed_edges(self._h, _p(out)))
         return out
+
+    # ---- multi-GPU round schedule (paper_2505_09258_b200/multigpu.py) ------
+    @property
+    def typed(self):
+        return self.model.uses_relations()
+
+    def train_items(self, epoch, items) -> EpochResult:
+        """Train an explicit bucket list (structured lgd_bucket_item array)."""
+        items = np.ascontiguousarray(items)
+        r = _EpochResult()
+        _check(library().lgd_train_items(self._h, epoch, items.ctypes.data_as(C.c_void_p),
+                                         len(items), C.byref(r)))
+        return EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
+
+    def round_begin(self, epoch, items) -> int:
+        items = np.ascontiguousarray(items)
+        self._round_items = items  # keep alive
+        nb = np.zeros(1, np.uint64)
+        _check(library().lgd_round_begin(self._h, epoch, items.ctypes.data_as(C.c_void_p),
+                                         len(items), _p(nb)))
+        return int(nb[0])
+
+    def round_step(self, step, rel_buf):
+        """rel_buf: device tensor [R x (d+1)] f64 (torch) or None."""
+        ptr = None if rel_buf is None else C.c_void_p(rel_buf.data_ptr())
+        _check(library().lgd_round_step(self._h, step, ptr))
+
+    def round_apply(self, summed):
+        _check(library().lgd_round_apply_relations(self._h, C.c_void_p(summed.data_ptr())))
+
+    def round_end(self) -> EpochResult:
+        r = _EpochResult()
+        _check(library().lgd_round_end(self._h, C.byref(r)))
+        return EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
+
+    def device_tables(self):
+        ptrs = [C.c_void_p() for _ in range(4)]
+        _check(library().lgd_device_tables(self._h, *[C.byref(x) for x in ptrs]))
+        return [x.value for x in ptrs]
+
+    def partition_views(self, p):
+        """Zero-copy torch views (CUDA) of partition p's theta and state rows."""
+        import torch
+        th, st, _, _ = self.device_tables()
+        s = self.stride()
+        a, b = s * p, min(s * (p + 1), self.num_nodes)
+        d = self.model.dim
+        return [torch.as_tensor(_CudaArray(ptr + a * d * 4, ((b - a) * d,)), device="cuda")
+                for ptr in (th, st)]
 
     def train_batch(self, edges, negatives, apply=True):
         """batch_loss + batch_gradients + adagrad_step on one batch."""

@@ -1,0 +1,238 @@
+"""Multi-GPU partition-round scheduler.
+
+Exact reference semantics do not shard: batches are sequentially dependent
+and every batch samples negatives from all three resident partitions.  The
+multi-GPU epoch is therefore a *schedule* with its own, stated semantics,
+rebuilt from the reference primitives and checked against a serialised CPU
+restatement (oracle ``run_rounds``):
+
+* rounds of disjoint partition pairs (circle method), every bucket once, in
+  one global order whose position keys the bucket's RNG stream
+  (``derive_seed(seed, "bukt", epoch, g)``, pipeline.cpp:296);
+* a bucket's negative pool is its pair {a, b};
+* pair j of a round runs on rank ``j % world``; ranks own disjoint
+  partitions within a round, so node updates never conflict;
+* typed models share the relation table: ranks run their batches in lock
+  step, the dense relation gradients [R x (d+1)] are summed across ranks
+  (NCCL all-reduce) and every rank applies the same Adagrad step;
+* between rounds each partition moves from its previous owner to its next
+  one (NCCL send/recv over NVLink); tables are allocated on every rank so a
+  hand-off is a plain row-range copy.
+
+The driver below is communicator-agnostic: ``DistComm`` wraps
+``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests) and
+``run_epoch_virtual`` steps several trainers in one process (the 1-GPU
+parity test).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import legend as L
+
+ITEM_DTYPE = np.dtype([("src", "<u4"), ("dst", "<u4"), ("g", "<u8"), ("pool", "<u4", (3,)),
+                       ("round", "<u4"), ("pair", "<u4"), ("_pad", "<u4")])
+assert ITEM_DTYPE.itemsize == 40
+
+
+def round_schedule(n: int) -> np.ndarray:
+    """The global bucket schedule (lgd_round_schedule) as a structured array."""
+    lib = L.library()
+    cnt = np.zeros(1, np.uint64)
+    L._check(lib.lgd_round_schedule(n, 0, L._p(cnt), None, None, None))
+    items = np.zeros(int(cnt[0]), ITEM_DTYPE)
+    L._check(lib.lgd_round_schedule(n, len(items), L._p(cnt), items.ctypes.data_as(C.c_void_p),
+                                    None, None))
+    return items
+
+
+def items_as_u64(items: np.ndarray) -> np.ndarray:
+    """(count, 8) rows for the oracle: src, dst, g, pool0..2, round, pair."""
+    out = np.zeros((len(items), 8), np.uint64)
+    out[:, 0] = items["src"]
+    out[:, 1] = items["dst"]
+    out[:, 2] = items["g"]
+    out[:, 3:6] = items["pool"]
+    out[:, 6] = items["round"]
+    out[:, 7] = items["pair"]
+    return out
+
+
+@dataclass
+class Schedule:
+    n: int
+    world: int
+    items: np.ndarray
+
+    @classmethod
+    def build(cls, n: int, world: int) -> "Schedule":
+        return cls(n, world, round_schedule(n))
+
+    @property
+    def num_rounds(self) -> int:
+        return int(self.items["round"].max()) + 1 if len(self.items) else 0
+
+    def rank_items(self, r: int, rank: int) -> np.ndarray:
+        it = self.items
+        sel = (it["round"] == r) & (it["pair"] % self.world == rank)
+        return np.ascontiguousarray(it[sel])
+
+    def users(self, r: int) -> dict:
+        """partition -> rank that trains on it in round r"""
+        it = self.items[self.items["round"] == r]
+        out = {}
+        for row in it:
+            for p in row["pool"]:
+                if p != 0xFFFFFFFF:
+                    out[int(p)] = int(row["pair"]) % self.world
+        return out
+
+    def handoffs(self):
+        """Per round: [(partition, from_rank, to_rank)] moves before it runs.
+        Every rank starts with an identical copy of every partition."""
+        owner = {p: None for p in range(self.n)}
+        plan = []
+        for r in range(self.num_rounds):
+            moves = []
+            for p, dst in sorted(self.users(r).items()):
+                src = owner[p]
+                if src is not None and src != dst:
+                    moves.append((p, src, dst))
+                owner[p] = dst
+            plan.append(moves)
+        return plan, owner
+
+
+class DistComm:
+    """torch.distributed communicator (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, dist, device):
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = device
+
+    def all_reduce_sum(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+
+    def all_reduce_max_int(self, v: int) -> int:
+        import torch
+        t = torch.tensor([v], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return int(t.item())
+
+    def exchange(self, moves, views):
+        """moves: [(p, src, dst)]; views(p) -> list of tensors of partition p"""
+        ops = []
+        for p, src, dst in moves:
+            if self.rank == src:
+                ops += [self.dist.P2POp(self.dist.isend, t, dst) for t in views(p)]
+            elif self.rank == dst:
+                ops += [self.dist.P2POp(self.dist.irecv, t, src) for t in views(p)]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+def run_epoch_distributed(trainer, sched: Schedule, epoch: int, comm, rel_buf=None):
+    """One epoch of the round schedule on this rank.  `trainer` provides
+    train_items / round_begin / round_step / round_apply / round_end /
+    partition_views; `rel_buf` is a [R x (d+1)] f64 tensor on the comm device
+    (typed models).  Returns this rank's summed EpochResult fields."""
+    plan, _ = sched.handoffs()
+    totals = {"loss_sum": 0.0, "edges_trained": 0, "batches": 0, "device_ms": 0.0}
+    for r in range(sched.num_rounds):
+        comm.exchange(plan[r], trainer.partition_views)
+        mine = sched.rank_items(r, comm.rank)
+        if not trainer.typed:
+            res = trainer.train_items(epoch, mine)
+        else:
+            nb = trainer.round_begin(epoch, mine)
+            steps = comm.all_reduce_max_int(nb)
+            for s in range(steps):
+                trainer.round_step(s, rel_buf)
+                comm.all_reduce_sum(rel_buf)
+                trainer.round_apply(rel_buf)
+            res = trainer.round_end()
+        for key in totals:
+            totals[key] += getattr(res, key) if hasattr(res, key) else res[key]
+    return totals
+
+
+def gather_final(trainer, sched: Schedule, comm):
+    """Move every partition from its final owner to rank 0."""
+    _, owner = sched.handoffs()
+    moves = [(p, o, 0) for p, o in sorted(owner.items()) if o not in (None, 0)]
+    comm.exchange(moves, trainer.partition_views)
+
+
+def run_epoch_virtual(trainers, sched: Schedule, epoch: int, copy_partition, rel_bufs=None,
+                      sum_into=None):
+    """All ranks of the schedule in one process (one trainer per rank, e.g.
+    several contexts on one GPU): the 1-GPU parity harness."""
+    plan, owner = sched.handoffs()
+    world = len(trainers)
+    typed = trainers[0].typed
+    for r in range(sched.num_rounds):
+        for p, src, dst in plan[r]:
+            copy_partition(trainers[dst], trainers[src], p)
+        mines = [sched.rank_items(r, q) for q in range(world)]
+        if not typed:
+            for q in range(world):
+                trainers[q].train_items(epoch, mines[q])
+            continue
+        nbs = [trainers[q].round_begin(epoch, mines[q]) for q in range(world)]
+        for s in range(max(nbs) if nbs else 0):
+            for q in range(world):
+                trainers[q].round_step(s, rel_bufs[q])
+            total = sum_into(rel_bufs)
+            for q in range(world):
+                trainers[q].round_apply(total)
+        for q in range(world):
+            trainers[q].round_end()
+    for p, o in sorted(owner.items()):
+        if o not in (None, 0):
+            copy_partition(trainers[0], trainers[o], p)
+
+
+class RoundCursor:
+    """Walks the schedule round after round (wrapping into the next epoch)
+    and keeps partition ownership across rounds and epochs; every rank starts
+    with an identical copy of every partition."""
+
+    def __init__(self, sched: Schedule):
+        self.sched = sched
+        self.owner = {p: None for p in range(sched.n)}
+        self.step = 0
+
+    def next(self):
+        """-> (epoch, round, moves) for the next round; ownership advances."""
+        r = self.step % self.sched.num_rounds
+        epoch = self.step // self.sched.num_rounds
+        moves = []
+        for p, dst in sorted(self.sched.users(r).items()):
+            src = self.owner[p]
+            if src is not None and src != dst:
+                moves.append((p, src, dst))
+            self.owner[p] = dst
+        self.step += 1
+        return epoch, r, moves
+
+
+def run_round(trainer, sched: Schedule, epoch: int, r: int, moves, comm, rel_buf=None):
+    """One round on this rank: hand-offs, then this rank's buckets (lock-step
+    relation sums for typed models).  Returns the trainer's EpochResult."""
+    comm.exchange(moves, trainer.partition_views)
+    mine = sched.rank_items(r, comm.rank)
+    if not trainer.typed:
+        return trainer.train_items(epoch, mine)
+    nb = trainer.round_begin(epoch, mine)
+    steps = comm.all_reduce_max_int(nb)
+    for s in range(steps):
+        trainer.round_step(s, rel_buf)
+        comm.all_reduce_sum(rel_buf)
+        trainer.round_apply(rel_buf)
+    return trainer.round_end()

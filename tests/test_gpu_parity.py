@@ -265,3 +265,51 @@ def test_errors_follow_reference_classes():
         t2.train_batch(np.array([[0, 0xFFFFFFFF, 1]], np.uint32), np.array([1, 2], np.uint32))
     with pytest.raises(lgd.InvalidArgument):
         make_trainer("dot", 8, 10, 0, edges, 11)  # n > V (graph.cpp:122)
+
+
+# ------------------------------------------- multi-GPU round schedule (1 GPU)
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world):
+    """`world` trainer contexts on one GPU run the partition-round schedule
+    exactly as `world` GPUs would (hand-offs as device copies, lock-step
+    relation sums); the result must match the serialised restatement."""
+    import torch
+    from paper_2505_09258_b200 import multigpu as mg
+    rng = np.random.default_rng(21)
+    V, R, d, Ecnt, n, k, B = 500, 5, 12, 8000, 6, 4, 300
+    rels = rng.integers(0, R, Ecnt) if kind != "dot" else np.full(Ecnt, 0xFFFFFFFF)
+    edges = np.stack([rng.integers(0, V, Ecnt), rels, rng.integers(0, V, Ecnt)],
+                     1).astype(np.uint32)
+    Rm = R if kind != "dot" else 0
+    trainers = [make_trainer(kind, d, V, Rm, edges, n, k=k, batch=B, seed=7) for _ in range(world)]
+    for t in trainers:
+        t.init_store(42)
+    sched = mg.Schedule.build(n, world)
+
+    def copy_partition(dst, src, p):
+        for a, b in zip(dst.partition_views(p), src.partition_views(p)):
+            a.copy_(b)
+
+    bufs = [torch.zeros((max(Rm, 1), d + 1), dtype=torch.float64, device="cuda")
+            for _ in range(world)]
+
+    def sum_into(bs):
+        total = bs[0].clone()
+        for b in bs[1:]:
+            total += b
+        return total
+
+    mg.run_epoch_virtual(trainers, sched, 0, copy_partition, bufs, sum_into)
+    torch.cuda.synchronize()
+    E, S = trainers[0].tables()
+    E0, S0, rE, rS = oracle.store_init(n, V, d, max(Rm, 1), 42)
+    want = oracle.run_rounds(edges, V, Rm, n, mg.items_as_u64(sched.items), world, kind, E0, S0,
+                             rE if Rm else None, rS if Rm else None, dim=d, batch_size=B, k=k,
+                             seed=7)
+    assert want["edges_trained"] == Ecnt
+    assert_tables_close(E, E0, "E")
+    assert_tables_close(S, S0, "S")
+    if Rm:
+        rEg, rSg = trainers[0].get_relations()
+        assert_tables_close(rEg, rE, "relE")
