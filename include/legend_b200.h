@@ -36,6 +36,7 @@ extern "C" {
 #define LGD_MODEL_DOT 0
 #define LGD_MODEL_DISTMULT 1
 #define LGD_MODEL_COMPLEX 2
+#define LGD_MODEL_TRANSE 3 /* -||s + r - t||; not in the reference */
 
 #define LGD_NO_RELATION 0xffffffffu /* kNoRelation, graph.hpp:17 */
 

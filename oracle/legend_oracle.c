@@ -31,6 +31,7 @@
 #define LO_KIND_DOT 0              /* train.hpp:13 ScoreKind */
 #define LO_KIND_DISTMULT 1
 #define LO_KIND_COMPLEX 2
+#define LO_KIND_TRANSE 3           /* not in the reference (train.hpp:13): defined below */
 
 /* ------------------------------------------------------------------ RNG --- */
 
@@ -233,6 +234,9 @@ static void combine(int kind, uint32_t d, const float* src, const float* rel, do
     case LO_KIND_DISTMULT:
       for (uint32_t i = 0; i < d; ++i) out[i] = (double)src[i] * rel[i];
       break;
+    case LO_KIND_TRANSE:
+      for (uint32_t i = 0; i < d; ++i) out[i] = (double)src[i] + (double)rel[i];
+      break;
     default: {
       const uint32_t h = d / 2;
       for (uint32_t i = 0; i < h; ++i) {
@@ -249,6 +253,7 @@ static void combine(int kind, uint32_t d, const float* src, const float* rel, do
 static void adjoint(int kind, uint32_t d, const float* other, const double* mix, double* out) {
   switch (kind) {
     case LO_KIND_DOT:
+    case LO_KIND_TRANSE:
       for (uint32_t i = 0; i < d; ++i) out[i] += mix[i];
       break;
     case LO_KIND_DISTMULT:
@@ -263,6 +268,26 @@ static void adjoint(int kind, uint32_t d, const float* other, const double* mix,
       }
     }
   }
+}
+
+/*
+ * TransE -- NOT in the reference (ScoreKind, train.hpp:13; SPEC.md lists
+ * translational models as a non-goal), so this restatement is its
+ * definition ("parity unpinned" against the reference; the CUDA path is
+ * checked against this).  Written in the reference's structure:
+ *   u = s + r (IR1),  q_t = u - t,  D_t = sqrt(sum_i q_t[i]^2) (sequential),
+ *   score f_t = -D_t, the same contrastive loss -(f_pos - LSE_j f_j),
+ *   w_j = softmax weight, coef_pos = -1/D_pos, coef_j = w_j/D_j (0 when D = 0),
+ *   node gradient contributions coef * (u - row) for dst and negatives,
+ *   src and relation gradient mix = -coef_pos q_pos - sum_j coef_j q_j.
+ */
+static double transe_dist(uint32_t d, const double* u, const float* t) {
+  double acc = 0.0;
+  for (uint32_t i = 0; i < d; ++i) {
+    const double q = u[i] - (double)t[i];
+    acc += q * q;
+  }
+  return sqrt(acc);
 }
 
 /* train.cpp:342-354 adagrad_update (FP64 math, FP32 storage; the update uses
@@ -294,7 +319,7 @@ static int check_model(int kind, uint32_t dim) {
   /* train.cpp:11-16 ScoreModel::validate */
   if (dim == 0) return LO_INVALID;
   if (kind == LO_KIND_COMPLEX && dim % 2 != 0) return LO_INVALID;
-  if (kind < 0 || kind > 2) return LO_INVALID;
+  if (kind < 0 || kind > 3) return LO_INVALID;
   return LO_OK;
 }
 
@@ -357,6 +382,9 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
   }
 
   /* batch_loss: train.cpp:236-275 */
+  const int transe = kind == LO_KIND_TRANSE;
+  double* dpos = (double*)malloc((P ? P : 1) * sizeof(double));
+  double* dneg = (double*)malloc((P ? P : 1) * k * sizeof(double));
   double loss = 0.0;
   for (uint64_t p = 0; p < P; ++p) {
     const uint32_t s = edges[3 * p], r = edges[3 * p + 1], t = edges[3 * p + 2];
@@ -364,15 +392,25 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
     combine(kind, d, E + (uint64_t)s * d, typed ? relE + (uint64_t)r * d : NULL, x);
     const float* dst = E + (uint64_t)t * d;
     double pos = 0.0;
-    for (uint32_t i = 0; i < d; ++i) {
-      const double term = x[i] * dst[i];
-      pos += term;
+    if (transe) {
+      dpos[p] = transe_dist(d, x, dst);
+      pos = -dpos[p];
+    } else {
+      for (uint32_t i = 0; i < d; ++i) {
+        const double term = x[i] * dst[i];
+        pos += term;
+      }
     }
     double row_max = -INFINITY;
     for (uint32_t j = 0; j < k; ++j) {
       const float* neg = E + (uint64_t)negs[p * k + j] * d;
       double fj = 0.0;
-      for (uint32_t i = 0; i < d; ++i) fj += x[i] * neg[i];
+      if (transe) {
+        dneg[p * k + j] = transe_dist(d, x, neg);
+        fj = -dneg[p * k + j];
+      } else {
+        for (uint32_t i = 0; i < d; ++i) fj += x[i] * neg[i];
+      }
       f[j] = fj;
       row_max = (row_max < fj) ? fj : row_max; /* std::max(row_max, f) */
     }
@@ -393,11 +431,25 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
     for (uint32_t j = 0; j < k; ++j) w[p * k + j] = w[p * k + j] * inv_sum;
     const float* dst = E + (uint64_t)edges[3 * p + 2] * d;
     double* mix = mixes + p * d;
-    for (uint32_t i = 0; i < d; ++i) mix[i] = -(double)dst[i];
-    for (uint32_t j = 0; j < k; ++j) {
-      const float* neg = E + (uint64_t)negs[p * k + j] * d;
-      const double wj = w[p * k + j];
-      for (uint32_t i = 0; i < d; ++i) mix[i] += wj * neg[i];
+    if (transe) {  /* coefficients replace w; mix = dL/du */
+      const double* x = ir1 + p * d;
+      const double cpos = dpos[p] > 0.0 ? -1.0 / dpos[p] : 0.0;
+      dpos[p] = cpos;
+      for (uint32_t i = 0; i < d; ++i) mix[i] = -(cpos * (x[i] - (double)dst[i]));
+      for (uint32_t j = 0; j < k; ++j) {
+        const double dj = dneg[p * k + j];
+        const double cj = dj > 0.0 ? w[p * k + j] / dj : 0.0;
+        w[p * k + j] = cj;
+        const float* neg = E + (uint64_t)negs[p * k + j] * d;
+        for (uint32_t i = 0; i < d; ++i) mix[i] -= cj * (x[i] - (double)neg[i]);
+      }
+    } else {
+      for (uint32_t i = 0; i < d; ++i) mix[i] = -(double)dst[i];
+      for (uint32_t j = 0; j < k; ++j) {
+        const float* neg = E + (uint64_t)negs[p * k + j] * d;
+        const double wj = w[p * k + j];
+        for (uint32_t i = 0; i < d; ++i) mix[i] += wj * neg[i];
+      }
     }
     con[p * slots].id = edges[3 * p + 2];
     con[p * slots].seq = p * slots;
@@ -433,7 +485,11 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
       const uint64_t p = con[c].seq / slots;
       const uint64_t slot = con[c].seq % slots;
       const double* x = ir1 + p * d;
-      if (slot == 0) {
+      if (transe && slot <= k) { /* coef * (u - own row), own row pre-update */
+        const double cf = slot == 0 ? dpos[p] : w[p * k + (slot - 1)];
+        const float* own = E + (uint64_t)id * d;
+        for (uint32_t i = 0; i < d; ++i) acc[i] += cf * (x[i] - (double)own[i]);
+      } else if (slot == 0) {
         for (uint32_t i = 0; i < d; ++i) acc[i] -= x[i]; /* train.cpp:310 */
       } else if (slot <= k) {
         const double wj = w[p * k + (slot - 1)];
@@ -492,7 +548,7 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
   if (loss_out) *loss_out = loss;
   free(ir1), free(w), free(f), free(con), free(mixes), free(rowsum), free(g), free(gall),
       free(gid);
-  free(rall), free(rid);
+  free(rall), free(rid), free(dpos), free(dneg);
   return LO_OK;
 }
 
@@ -661,14 +717,22 @@ int lo_evaluate(int kind, uint32_t d, const float* E, uint64_t num_nodes, const 
     }
     combine(kind, d, E + (uint64_t)s * d, typed ? relE + (uint64_t)r * d : NULL, ir1);
     double truth = 0.0;
-    for (uint32_t i = 0; i < d; ++i) truth += ir1[i] * E[(uint64_t)dd * d + i];
+    if (kind == LO_KIND_TRANSE) {
+      truth = -transe_dist(d, ir1, E + (uint64_t)dd * d);
+    } else {
+      for (uint32_t i = 0; i < d; ++i) truth += ir1[i] * E[(uint64_t)dd * d + i];
+    }
     lo_rng rng;
     lo_rng_init(&rng, lo_derive_seed(seed, 0x65766179ull, t, 0));
     uint64_t beaten = 0;
     for (uint32_t c = 0; c < num_candidates; ++c) {
       const uint64_t cand = lo_rng_below(&rng, num_nodes);
       double f = 0.0;
-      for (uint32_t i = 0; i < d; ++i) f += ir1[i] * E[cand * d + i];
+      if (kind == LO_KIND_TRANSE) {
+        f = -transe_dist(d, ir1, E + cand * d);
+      } else {
+        for (uint32_t i = 0; i < d; ++i) f += ir1[i] * E[cand * d + i];
+      }
       if (f >= truth) ++beaten;
     }
     const uint64_t rank = 1 + beaten;

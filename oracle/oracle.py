@@ -31,7 +31,7 @@ u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
-KINDS = {"dot": 0, "distmult": 1, "complex": 2}
+KINDS = {"dot": 0, "distmult": 1, "complex": 2, "transe": 3}
 
 
 def available(which: str) -> bool:

@@ -169,7 +169,7 @@ struct lgd_context {
     if (P <= batch_cap && kk <= k_cap) return;
     P = std::max(P, batch_cap);
     const uint64_t items = P * (kk + 2);
-    w.reserve(P * kk);
+    w.reserve(P * kk + P);  // + TransE's dst coefficients
     mix.reserve(P * dim);
     snap.reserve(P * dim);
     loss.reserve(P);
@@ -670,7 +670,7 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
   return guarded([&] {
     if (!out) throw std::invalid_argument("null output pointer");
     *out = nullptr;
-    if (model_kind < 0 || model_kind > 2) throw std::invalid_argument("unknown score model");
+    if (model_kind < 0 || model_kind > 3) throw std::invalid_argument("unknown score model");
     if (dim == 0) throw std::invalid_argument("embedding dimension must be positive");
     if (model_kind == LGD_MODEL_COMPLEX && dim % 2 != 0)
       throw std::invalid_argument("complex model requires an even dimension");

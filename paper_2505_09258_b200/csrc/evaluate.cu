@@ -56,6 +56,8 @@ __global__ void eval_score_kernel(int kind, uint32_t d, const float* __restrict_
       x[c] = sr[i];
     } else if (kind == 1) {
       x[c] = (double)sr[i] * (double)rel[(size_t)r * d + i];
+    } else if (kind == 3) {
+      x[c] = (double)sr[i] + (double)rel[(size_t)r * d + i];
     } else {
       const float* rl = rel + (size_t)r * d;
       const uint32_t j = i < h ? i : i - h;
@@ -69,9 +71,16 @@ __global__ void eval_score_kernel(int kind, uint32_t d, const float* __restrict_
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const uint32_t i = lane + 32 * c;
-      if (i < d) acc += x[c] * (double)row[i];
+      if (i < d) {
+        if (kind == 3) {
+          const double q = x[c] - (double)row[i];
+          acc += q * q;
+        } else {
+          acc += x[c] * (double)row[i];
+        }
+      }
     }
-    return warp_sum(acc);
+    return kind == 3 ? -sqrt(warp_sum(acc)) : warp_sum(acc);
   };
   const double truth = score(dd);
   uint32_t beaten = 0;

@@ -210,6 +210,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         ir1[j] = sr * rr - si * ri;
         ir1[j + h] = sr * ri + si * rr;
       }
+    } else if (KIND == 3) {  // TransE: u = s + r
+      for (uint32_t i = lane; i < d; i += 32) ir1[i] = (double)srow[i] + (double)rrow[i];
     } else {
       for (uint32_t i = lane; i < d; i += 32)
         ir1[i] = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
@@ -221,7 +223,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
     for (uint32_t q = lane; q <= k; q += 32) {
       const float* row = q < k ? R + (3 + q) * dpad : drow;
       double f = 0.0;
-      if ((d & 3) == 0) {
+      if (KIND == 3) {  // -||u - t||, squares summed sequentially
+        for (uint32_t i = 0; i < d; ++i) {
+          const double q = ir1[i] - (double)row[i];
+          f += q * q;
+        }
+        f = -sqrt(f);
+      } else if ((d & 3) == 0) {
         for (uint32_t i = 0; i < d; i += 4) {
           const float4 v = *reinterpret_cast<const float4*>(row + i);
           const double2 x0 = *reinterpret_cast<const double2*>(ir1 + i);
@@ -247,14 +255,34 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
     double sum = 0.0;
     for (uint32_t j = 0; j < k; ++j) sum += ebuf[j];  // sequential j (train.cpp:266-270)
     const double inv_sum = 1.0 / sum;
-    for (uint32_t j = lane; j < k; j += 32) a.w[p * k + j] = ebuf[j] * inv_sum;
     if (lane == 0) a.loss[p] = -(fbuf[k] - (row_max + log(sum)));  // train.cpp:274
-
-    // mix = sum_j w_j neg_j - dst, j ascending (train.cpp:306-323)
-    for (uint32_t i = lane; i < d; i += 32) {
-      double mx = -(double)drow[i];
-      for (uint32_t j = 0; j < k; ++j) mx += (ebuf[j] * inv_sum) * (double)R[(3 + j) * dpad + i];
-      a.mix[p * d + i] = mx;
+    if (KIND == 3) {
+      // TransE coefficients (oracle lo_batch_ex): c_j = w_j / D_j, c_pos =
+      // -1 / D_pos (0 at D = 0), stored where w lives (c_pos after P x k);
+      // mix = dL/du = -c_pos (u - t) - sum_j c_j (u - n_j), j ascending
+      for (uint32_t j = lane; j < k; j += 32) {
+        const double dj = -fbuf[j];
+        ebuf[j] = dj > 0.0 ? (ebuf[j] * inv_sum) / dj : 0.0;
+        a.w[p * k + j] = ebuf[j];
+      }
+      const double dpos = -fbuf[k];
+      const double cpos = dpos > 0.0 ? -1.0 / dpos : 0.0;
+      if (lane == 0) a.w[a.P * k + p] = cpos;
+      __syncwarp();
+      for (uint32_t i = lane; i < d; i += 32) {
+        const double u = ir1[i];
+        double mx = -(cpos * (u - (double)drow[i]));
+        for (uint32_t j = 0; j < k; ++j) mx -= ebuf[j] * (u - (double)R[(3 + j) * dpad + i]);
+        a.mix[p * d + i] = mx;
+      }
+    } else {
+      for (uint32_t j = lane; j < k; j += 32) a.w[p * k + j] = ebuf[j] * inv_sum;
+      // mix = sum_j w_j neg_j - dst, j ascending (train.cpp:306-323)
+      for (uint32_t i = lane; i < d; i += 32) {
+        double mx = -(double)drow[i];
+        for (uint32_t j = 0; j < k; ++j) mx += (ebuf[j] * inv_sum) * (double)R[(3 + j) * dpad + i];
+        a.mix[p * d + i] = mx;
+      }
     }
     // contribution keys in the reference's visit order: dst, negatives, src
     const uint64_t kb = p * (k + 2);
@@ -318,7 +346,8 @@ struct GMap {
 // issued first (predicated, no branches) so a lane keeps every element of the
 // item in flight at once; the FP64 arithmetic follows in the reference order.
 template <int KIND, int NC, bool REL>
-__device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g, double* acc) {
+__device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g, double* acc,
+                                         const float* own) {
   using M = GMap<KIND, NC>;
   constexpr int NE = M::NE;
   const uint32_t d = a.dim, h = d / 2, k = a.k;
@@ -343,7 +372,7 @@ __device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) acc[e] += (double)sv[e] * mv[e];
+      for (int e = 0; e < NE; ++e) acc[e] += KIND == 3 ? mv[e] : (double)sv[e] * mv[e];
     }
     return;
   }
@@ -353,7 +382,8 @@ __device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g
   const float* rel = KIND != 0 ? a.rel_theta + (size_t)__ldg(a.rel_keys + p) * d : nullptr;
   const float* s = a.snap + p * d;
   const double* mx = a.mix + p * d;
-  const double w = (slot >= 1 && !is_src) ? __ldg(a.w + p * k + (slot - 1)) : 0.0;
+  const double w = (slot >= 1 && !is_src) ? __ldg(a.w + p * k + (slot - 1))
+                   : (KIND == 3 && slot == 0) ? __ldg(a.w + a.P * k + p) : 0.0;
   float rv[NE], sv[NE];
   double mv[NE];
 #pragma unroll
@@ -365,7 +395,13 @@ __device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g
     mv[e] = (is_src && ok) ? __ldg(mx + i) : 0.0;
   }
   if (!is_src) {  // dst: g -= IR1 (train.cpp:310); negative j: g += w_j IR1 (:320)
-    if (KIND == 2) {
+    if (KIND == 3) {  // TransE: g += c (u - own row)
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const double x = (double)sv[e] + (double)rv[e];
+        acc[e] += w * (x - (double)own[e]);
+      }
+    } else if (KIND == 2) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const double sr = sv[c], si = sv[c + NC], rr = rv[c], ri = rv[c + NC];
@@ -390,7 +426,7 @@ __device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) acc[e] += KIND == 0 ? mv[e] : (double)rv[e] * mv[e];
+      for (int e = 0; e < NE; ++e) acc[e] += (KIND == 0 || KIND == 3) ? mv[e] : (double)rv[e] * mv[e];
     }
   }
 }
@@ -461,14 +497,17 @@ __global__ void __launch_bounds__(kSegThreads) segment_pass1(BatchArgs a, uint64
     const bool finish = live && !first_piece && !last_piece;
     const uint32_t row = live ? (REL ? skeys[base + pstart] : from_pool(a, skeys[base + pstart])) : 0;
     float tv[NE], sv[NE];
-    if (finish && !(REL ? a.grad_rels : a.grad_nodes)) {  // prefetch theta / state
+    constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
+    const bool upd = finish && !(REL ? a.grad_rels : a.grad_nodes);
+    if (upd || (kOwn && live)) {  // prefetch theta / state
       const float* th = row_theta<REL>(a, row);
       const float* st = row_state<REL>(a, row);
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
+        tv[e] = 0.f;
         if (M::ok(e, g, d, h)) {
           tv[e] = th[M::idx(e, g, h)];
-          sv[e] = st[M::idx(e, g, h)];
+          if (upd) sv[e] = st[M::idx(e, g, h)];
         }
       }
     }
@@ -481,7 +520,7 @@ __global__ void __launch_bounds__(kSegThreads) segment_pass1(BatchArgs a, uint64
 #pragma unroll
     for (int off = 8; off < 32; off <<= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
     for (int q = 0; q < maxlen; ++q) {
-      if (q < len) add_item<KIND, NC, REL>(a, __ldg(svals + base + pstart + q), g, acc);
+      if (q < len) add_item<KIND, NC, REL>(a, __ldg(svals + base + pstart + q), g, acc, tv);
     }
     if (first_piece || last_piece) {
       double* dst = (first_piece ? a.part_first : a.part_last) + c * d;
@@ -525,7 +564,6 @@ __global__ void __launch_bounds__(kSegThreads) segment_pass1(BatchArgs a, uint64
 // first contribution are loaded while the current piece computes.
 template <int KIND, int NV>
 struct Lanes {
-  static constexpr int NE = 4 * NV;
   bool ok[NV];
   uint32_t off[NV];  // element offset of the lane's (real) vector
   uint32_t h;
@@ -647,6 +685,7 @@ struct SegCtx {  // hoisted kernel arguments
   const float* rel_theta;
   const uint32_t* rel_keys;
   uint32_t d, k, sbits, smask;
+  uint64_t cpos_off;  // TransE: offset of the dst coefficients in w (P k)
 };
 
 template <int KIND, int NV, bool REL>
@@ -664,8 +703,10 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
   it.slot = slot;
-  // dst (slot 0) uses w = -1: g - IR1 == g + (-1 * IR1) in IEEE arithmetic
-  it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1)) : -1.0;
+  // dst (slot 0) uses w = -1: g - IR1 == g + (-1 * IR1) in IEEE arithmetic;
+  // TransE's dst coefficient sits after the P x k negative coefficients
+  it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1))
+         : (KIND == 3 && pred && slot == 0) ? __ldg(x.w + x.cpos_off + p) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
   if (KIND != 0) {
     const uint32_t r = pred ? __ldg(x.rel_keys + p) : 0;
@@ -676,7 +717,8 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
 }
 
 template <int KIND, int NV, bool REL>
-__device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t k, double* acc) {
+__device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
+                                           const float* own) {
   constexpr int NE = 4 * NV;
   if (REL || it.slot > k) {  // adj_other(mix): other = src snapshot (REL) or relation row
     const float* o = REL ? it.sv : it.rv;
@@ -692,7 +734,16 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
         }
     } else {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) acc[e] += KIND == 0 ? it.mv[e] : (double)o[e] * it.mv[e];
+      for (int e = 0; e < NE; ++e)
+        acc[e] += (KIND == 0 || KIND == 3) ? it.mv[e] : (double)o[e] * it.mv[e];
+    }
+    return;
+  }
+  if (KIND == 3) {  // TransE: g += c (u - own row), u = s + r
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double x = (double)it.sv[e] + (double)it.rv[e];
+      acc[e] += it.w * (x - (double)own[e]);
     }
     return;
   }
@@ -717,17 +768,6 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
   }
 }
 
-// adagrad_update (train.cpp:342-354) with the compiler's inline IEEE
-// division / square root (bit-identical; zero or denormal operands take the
-// library slow path, which only genuinely-zero gradients of active lanes
-// reach).
-__device__ __forceinline__ void adagrad_plain(double gi, float& th, float& st, double lr,
-                                              double eps) {
-  const double acc = (double)st + gi * gi;
-  st = (float)acc;
-  th = (float)((double)th - lr * gi / (sqrt(acc) + eps));
-}
-
 template <int KIND, int NV, bool REL>
 __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     BatchArgs a, uint64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
@@ -739,7 +779,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
   if (base >= n) return;
   const Lanes<KIND, NV> L(lane, a.dim);
   const SegCtx x{a.snap, a.mix, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
-                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u};
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u, a.P * a.k};
+  constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
   float* __restrict__ theta = REL ? a.rel_theta : a.theta;
   float* __restrict__ state = REL ? a.rel_state : a.state;
   double* gout = REL ? a.grad_rels : a.grad_nodes;
@@ -793,7 +834,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     {
       const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, cur)) * d;
       const bool fin = finishing(t) && !gout;
-      L.template ldf<false>(theta + row, fin, cth);
+      L.template ldf<false>(theta + row, fin || kOwn, cth);
       L.template ldf<false>(state + row, fin, cst);
       load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
     }
@@ -808,18 +849,18 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         const int ns = nxt & 31;
         const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, ns)) * d;
         const bool fin = has_next && finishing(t + 1) && !gout;
-        L.template ldf<false>(theta + row, fin, nth);
+        L.template ldf<false>(theta + row, fin || (kOwn && has_next), nth);
         L.template ldf<false>(state + row, fin, nst);
         load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, ns), has_next, nit);
       }
       double acc[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-      add_loaded<KIND, NV, REL>(cit, x.k, acc);
+      add_loaded<KIND, NV, REL>(cit, x.k, acc, cth);
       for (int q = cur + 1; q < pend; ++q) {
         ItemRegs<NE> it;
         load_item<KIND, NV, REL>(x, L, item_val(q), true, it);
-        add_loaded<KIND, NV, REL>(it, x.k, acc);
+        add_loaded<KIND, NV, REL>(it, x.k, acc, cth);
       }
       const uint32_t rowid = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {
@@ -932,9 +973,9 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
 // ----------------------------------------------------------- dispatchers
 // score_kernel<KIND> is shared by every (dim, k): its dynamic-smem attribute
 // only grows; occupancy is cached per smem size.  (Host-side, per process.)
-size_t g_score_attr[3] = {0, 0, 0};
-size_t g_score_occ_smem[3] = {0, 0, 0};
-int g_score_occ[3] = {0, 0, 0};
+size_t g_score_attr[4] = {0, 0, 0, 0};
+size_t g_score_occ_smem[4] = {0, 0, 0, 0};
+int g_score_occ[4] = {0, 0, 0, 0};
 
 void sort_items(const BatchArgs& a, uint64_t items, const uint32_t* keys, const uint32_t* vals,
                 int key_bits, cudaStream_t st) {
@@ -1123,8 +1164,10 @@ void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* 
       return run_kind<0>(a, st, ev);
     case 1:
       return run_kind<1>(a, st, ev);
-    default:
+    case 2:
       return run_kind<2>(a, st, ev);
+    default:
+      return run_kind<3>(a, st, ev);
   }
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblegend_b200.so")
 
-MODELS = {"dot": 0, "distmult": 1, "complex": 2}
+MODELS = {"dot": 0, "distmult": 1, "complex": 2, "transe": 3}
 NO_RELATION = 0xFFFFFFFF
 
 KSTAT_SCORE, KSTAT_SORT, KSTAT_UPDATE, KSTAT_REL, KSTAT_SAMPLE, KSTAT_SHUFFLE = range(6)

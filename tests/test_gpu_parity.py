@@ -20,6 +20,9 @@ import paper_2505_09258_b200 as lgd
 
 pytestmark = pytest.mark.gpu
 KINDS = ["dot", "distmult", "complex"]
+# TransE is not in the reference: it is checked against the restatement only
+# (oracle/legend_oracle.c defines it; "parity unpinned" in DESIGN.md)
+ALL_KINDS = KINDS + ["transe"]
 
 
 def frob(a, b):
@@ -147,7 +150,7 @@ def test_batch_matches_golden(kind, d):
         assert_tables_close(rS, g["rS1"], "relS")
 
 
-@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("kind", ALL_KINDS)
 @pytest.mark.parametrize("d,k,P,V", [(100, 16, 3000, 5000), (64, 5, 777, 5000),
                                      (128, 40, 500, 5000), (32, 1, 64, 5000),
                                      (100, 16, 3000, 64), (100, 16, 3000, 2000),
@@ -224,6 +227,78 @@ def test_evaluate_matches_golden(kind):
     assert hits == pytest.approx(float(g["hits"]), abs=1e-12)
 
 
+# ------------------------------------------------- TransE vs restatement
+@pytest.mark.parametrize("n", [1, 4])
+def test_transe_epoch_matches_restatement(oracle, n):
+    """Same graphs / plans as the DistMult epoch fixtures, TransE scores."""
+    g = golden(f"epoch_distmult_n{n}")
+    V, R, d, k, B = int(g["V"]), int(g["R"]), int(g["d"]), int(g["k"]), int(g["batch"])
+    t = make_trainer("transe", d, V, R, g["edges"], n, k=k, batch=B, seed=int(g["seed"]))
+    t.init_store(int(g["store_seed"]))
+    res = t.run_epoch(0)
+    E, S, rE, rS = oracle.store_init(n, V, d, R, int(g["store_seed"]))
+    plan = dict(states=g["states"], bucket_order=g["bucket_order"],
+                state_offsets=g["state_offsets"])
+    want = oracle.run_epoch(g["edges"], V, R, n, plan, "transe", E, S, rE, rS, dim=d,
+                            batch_size=B, k=k, seed=int(g["seed"]), dumps=True)
+    assert res.edges_trained == want["edges_trained"]
+    assert res.unique_nodes == int(want["batch_nodes"].sum())
+    assert res.loss_sum == pytest.approx(want["loss_sum"], rel=1e-12)
+    Eg, Sg = t.tables()
+    assert_tables_close(Eg, E, "E")
+    assert_tables_close(Sg, S, "S")
+    rEg, rSg = t.get_relations()
+    assert_tables_close(rEg, rE, "relE")
+    assert_tables_close(rSg, rS, "relS")
+
+
+def test_transe_zero_distance_edges(oracle):
+    """u == t exactly (self loops over a zero relation row, and negatives equal
+    to the positive): the 1/D coefficients are defined as 0 there."""
+    V, R, d, k = 50, 3, 16, 4
+    rng = np.random.default_rng(9)
+    E0 = rng.uniform(-0.05, 0.05, (V, d)).astype(np.float32)
+    rE0 = rng.uniform(-0.05, 0.05, (R, d)).astype(np.float32)
+    rE0[0] = 0.0
+    P = 400
+    src = rng.integers(0, V, P)
+    rel = rng.integers(0, R, P)
+    dst = np.where(rel == 0, src, rng.integers(0, V, P))
+    edges = np.stack([src, rel, dst], 1).astype(np.uint32)
+    negs = np.where(rng.random((P, k)) < 0.3, dst[:, None],
+                    rng.integers(0, V, (P, k))).astype(np.uint32).reshape(-1)
+    t = make_trainer("transe", d, V, R, edges, 1, k=k)
+    t.load_tables(E0, np.zeros_like(E0))
+    t.set_relations(rE0, np.zeros_like(rE0))
+    E, S, rE, rS = E0.copy(), np.zeros_like(E0), rE0.copy(), np.zeros_like(rE0)
+    gr = t.batch_gradients(edges, negs)
+    want_g = oracle.batch("transe", E.copy(), S.copy(), rE.copy(), rS.copy(), edges, negs, k,
+                          apply=False, grads=True)
+    assert np.isfinite(gr["node_grads"]).all()
+    assert np.array_equal(gr["node_ids"], want_g["node_ids"])
+    np.testing.assert_allclose(gr["node_grads"], want_g["node_grads"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(gr["rel_grads"], want_g["rel_grads"], rtol=1e-10, atol=1e-14)
+    want = oracle.batch("transe", E, S, rE, rS, edges, negs, k)
+    got = t.train_batch(edges, negs)
+    assert got["loss"] == pytest.approx(want["loss"], rel=1e-12)
+    Eg, Sg = t.tables()
+    assert_tables_close(Eg, E, "E")
+    assert_tables_close(Sg, S, "S")
+
+
+def test_transe_evaluate_matches_restatement(oracle):
+    g = golden("eval_distmult")
+    E, rE, test = g["E"], g["relE"], g["test"]
+    t = make_trainer("transe", E.shape[1], E.shape[0], rE.shape[0], test, 1)
+    t.load_tables(E, np.zeros_like(E))
+    t.set_relations(rE, np.zeros_like(rE))
+    mrr, hits = t.evaluate(test, lgd.EvalOptions(hits_k=10, num_candidates=999,
+                                                 seed=int(g["seed"])))
+    wmrr, whits = oracle.evaluate("transe", E, rE, test, 999, 10, int(g["seed"]))
+    assert mrr == pytest.approx(wmrr, rel=1e-12)
+    assert hits == pytest.approx(whits, abs=1e-12)
+
+
 # ------------------------------------------- configs[0]: FB15k-shaped KG
 def test_fb15k_shaped_distmult_epoch_matches_oracle(oracle):
     """BASELINE configs[0]: 15k nodes, 1,345 relations, 592k edges, DistMult
@@ -268,7 +343,7 @@ def test_errors_follow_reference_classes():
 
 
 # ------------------------------------------- multi-GPU round schedule (1 GPU)
-@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("kind", ALL_KINDS)
 @pytest.mark.parametrize("world", [1, 2, 3])
 def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world):
     """`world` trainer contexts on one GPU run the partition-round schedule

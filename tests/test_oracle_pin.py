@@ -155,6 +155,49 @@ def test_finite_differences(oracle):
         assert fd == pytest.approx(res["node_grads"][0, i], rel=1e-3, abs=1e-6)
 
 
+def test_transe_restatement_finite_differences(oracle):
+    """TransE is not in the reference (train.hpp:13): its restatement is its
+    definition, so it is pinned by calculus instead -- every node and
+    relation gradient against central differences of the loss."""
+    rng = np.random.default_rng(4)
+    V, R, d, P, k = 12, 3, 5, 6, 3
+    E = rng.uniform(-0.5, 0.5, (V, d)).astype(np.float32)
+    rE = rng.uniform(-0.5, 0.5, (R, d)).astype(np.float32)
+    edges = np.stack([rng.integers(0, V, P), rng.integers(0, R, P), rng.integers(0, V, P)],
+                     1).astype(np.uint32)
+    negs = rng.integers(0, V, P * k).astype(np.uint32)
+    zS, zR = np.zeros_like(E), np.zeros_like(rE)
+    res = oracle.batch("transe", E.copy(), zS.copy(), rE.copy(), zR.copy(), edges, negs, k,
+                       apply=False, grads=True)
+
+    def loss(E_, rE_):
+        return oracle.batch("transe", E_, zS.copy(), rE_, zR.copy(), edges, negs, k,
+                            apply=False)["loss"]
+
+    for table, ids, grads in ((0, res["node_ids"], res["node_grads"]),
+                              (1, res["rel_ids"], res["rel_grads"])):
+        for u, row in enumerate(ids):
+            for i in range(d):
+                Ep, Em, rp, rm = E.copy(), E.copy(), rE.copy(), rE.copy()
+                tp, tm = (Ep, Em) if table == 0 else (rp, rm)
+                tp[row, i] += 1e-3
+                tm[row, i] -= 1e-3
+                fd = (loss(Ep, rp) - loss(Em, rm)) / (float(tp[row, i]) - float(tm[row, i]))
+                assert fd == pytest.approx(grads[u, i], rel=2e-3, abs=1e-6)
+
+
+def test_transe_scores_and_zero_distance(oracle):
+    # f = -||s + r - t||; an exact hit (u == t) has coefficient 0, not NaN
+    E = np.array([[0.5, 0.0], [0.5, 0.0], [1.5, 0.0]], np.float32)
+    rE = np.zeros((1, 2), np.float32)
+    edges = np.array([[0, 0, 1]], np.uint32)
+    res = oracle.batch("transe", E.copy(), np.zeros_like(E), rE.copy(), np.zeros_like(rE), edges,
+                       np.array([2, 2], np.uint32), 2, apply=False, grads=True)
+    # scores: pos 0, negatives -1, -1 -> loss = -(0 - (-1 + log 2))
+    assert res["loss"] == pytest.approx(-(0.0 - (-1.0 + np.log(2.0))), rel=1e-15)
+    assert np.isfinite(res["node_grads"]).all() and np.isfinite(res["rel_grads"]).all()
+
+
 def test_random_rank_baseline(oracle):
     # test_train.cpp:312-329: random embeddings rank near H(1000)/1000 = 0.00748
     rng = np.random.default_rng(2718)
