@@ -51,7 +51,14 @@ typedef struct {
   uint32_t batch_size;
   uint32_t negatives;
   int32_t shuffle;
-  uint32_t reserved;
+  /* 0: the reference's independent negatives, `negatives` per positive
+   * (train.cpp:365-373).  C > 0: shared-negative chunks -- every C
+   * consecutive positives of a batch share `negatives` ids, drawn
+   * ceil(P / C) * negatives per batch from the same bucket stream; scores on
+   * the tensor cores (TF32 in, FP32 accumulate).  Dot / DistMult / ComplEx,
+   * dim % 4 == 0, dim <= 128.  Not a reference mode: its oracle is the
+   * reference batch math on the expanded negative list. */
+  uint32_t shared_chunk;
   uint64_t seed;
 } lgd_train_options;
 

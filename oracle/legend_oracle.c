@@ -568,6 +568,38 @@ static int lo_batch_ex(int kind, uint32_t d, float* E, float* S, uint64_t num_no
  * trained edge (num_edges entries, in bucket_order), and every negative id
  * (num_edges * k entries).
  */
+/* Shared-negative chunks (not a reference mode): with
+ * chunk > 0 every run of `chunk` consecutive positives of a batch shares k
+ * negatives.  A batch of cnt positives draws ceil(cnt / chunk) * k values
+ * from the bucket stream (chunk-major, then j), right where the reference
+ * draws its cnt * k, and the reference batch math runs on the expansion
+ * negs[p * k + j] = shared[(p / chunk) * k + j].  neg_dump receives the
+ * shared draws. */
+static void expand_shared(const uint32_t* shared, uint64_t cnt, uint32_t k, uint32_t chunk,
+                          uint32_t* out) {
+  for (uint64_t p = 0; p < cnt; ++p)
+    memcpy(out + p * k, shared + (p / chunk) * k, k * sizeof(uint32_t));
+}
+
+int lo_expand_shared(const uint32_t* shared, uint64_t cnt, uint32_t k, uint32_t chunk,
+                     uint32_t* out) {
+  if (chunk == 0 || k == 0) return LO_INVALID;
+  expand_shared(shared, cnt, k, chunk, out);
+  return LO_OK;
+}
+
+int lo_run_epoch_ex(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
+                    uint64_t num_rels, uint32_t n, uint64_t stride, const uint64_t* bucket_offsets,
+                    const uint64_t* edge_order, uint64_t num_states, const uint32_t* states,
+                    const uint32_t* bucket_order, const uint64_t* state_offsets, int kind,
+                    uint32_t d, double lr, double eps, uint32_t batch_size, uint32_t k,
+                    uint32_t chunk, int shuffle, uint64_t seed, uint32_t epoch, float* E,
+                    float* S, float* relE, float* relS, double* loss_sum_out,
+                    uint64_t* edges_trained_out, uint64_t* buckets_trained_out,
+                    uint64_t* num_batches_out, uint64_t max_batches, double* batch_loss,
+                    uint64_t* batch_nodes, uint64_t* batch_rels, uint32_t* perm_dump,
+                    uint32_t* neg_dump);
+
 int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
                  uint64_t num_rels, uint32_t n, uint64_t stride, const uint64_t* bucket_offsets,
                  const uint64_t* edge_order, uint64_t num_states, const uint32_t* states,
@@ -578,6 +610,24 @@ int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
                  uint64_t* num_batches_out, uint64_t max_batches, double* batch_loss,
                  uint64_t* batch_nodes, uint64_t* batch_rels, uint32_t* perm_dump,
                  uint32_t* neg_dump) {
+  return lo_run_epoch_ex(edges, num_edges, num_nodes, num_rels, n, stride, bucket_offsets,
+                         edge_order, num_states, states, bucket_order, state_offsets, kind, d, lr,
+                         eps, batch_size, k, 0, shuffle, seed, epoch, E, S, relE, relS,
+                         loss_sum_out, edges_trained_out, buckets_trained_out, num_batches_out,
+                         max_batches, batch_loss, batch_nodes, batch_rels, perm_dump, neg_dump);
+}
+
+int lo_run_epoch_ex(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
+                    uint64_t num_rels, uint32_t n, uint64_t stride, const uint64_t* bucket_offsets,
+                    const uint64_t* edge_order, uint64_t num_states, const uint32_t* states,
+                    const uint32_t* bucket_order, const uint64_t* state_offsets, int kind,
+                    uint32_t d, double lr, double eps, uint32_t batch_size, uint32_t k,
+                    uint32_t chunk, int shuffle, uint64_t seed, uint32_t epoch, float* E,
+                    float* S, float* relE, float* relS, double* loss_sum_out,
+                    uint64_t* edges_trained_out, uint64_t* buckets_trained_out,
+                    uint64_t* num_batches_out, uint64_t max_batches, double* batch_loss,
+                    uint64_t* batch_nodes, uint64_t* batch_rels, uint32_t* perm_dump,
+                    uint32_t* neg_dump) {
   int rc = check_model(kind, d);
   if (rc) return rc;
   if (kind != LO_KIND_DOT && num_rels == 0) return LO_INVALID; /* pipeline.cpp:228-230 */
@@ -589,6 +639,7 @@ int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
   uint32_t* bucket = NULL;
   uint32_t* pos = NULL;
   uint32_t* negs = NULL;
+  uint32_t* shared = NULL;
   uint32_t* batch_edges = NULL;
   uint64_t cap = 0;
   rc = LO_OK;
@@ -599,14 +650,15 @@ int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
     const uint64_t m = bucket_offsets[b + 1] - bucket_offsets[b];
     if (m == 0) continue; /* pipeline.cpp:291: before the RNG is created */
     if (m > cap) {
-      free(bucket), free(pos), free(negs), free(batch_edges);
+      free(bucket), free(pos), free(negs), free(shared), free(batch_edges);
       cap = m;
       bucket = (uint32_t*)malloc(cap * 3 * sizeof(uint32_t));
       pos = (uint32_t*)malloc(cap * sizeof(uint32_t));
       uint64_t bcap = cap < batch_size ? cap : batch_size;
       negs = (uint32_t*)malloc(bcap * k * sizeof(uint32_t));
+      shared = (uint32_t*)malloc(bcap * k * sizeof(uint32_t));
       batch_edges = (uint32_t*)malloc(bcap * 3 * sizeof(uint32_t));
-      if (!bucket || !pos || !negs || !batch_edges) {
+      if (!bucket || !pos || !negs || !shared || !batch_edges) {
         rc = LO_NOMEM;
         goto done;
       }
@@ -656,10 +708,19 @@ int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
     }
     for (uint64_t off = 0; off < m; off += batch_size) { /* pipeline.cpp:303-312 */
       const uint64_t cnt = (m - off) < batch_size ? (m - off) : batch_size;
-      rc = lo_sample_negatives_rng(first, count, np, k, cnt, &rng, negs);
-      if (rc) goto done;
-      if (neg_dump) memcpy(neg_dump + neg_pos, negs, cnt * k * sizeof(uint32_t));
-      neg_pos += cnt * k;
+      if (chunk) {
+        const uint64_t nch = (cnt + chunk - 1) / chunk;
+        rc = lo_sample_negatives_rng(first, count, np, k, nch, &rng, shared);
+        if (rc) goto done;
+        if (neg_dump) memcpy(neg_dump + neg_pos, shared, nch * k * sizeof(uint32_t));
+        neg_pos += nch * k;
+        expand_shared(shared, cnt, k, chunk, negs);
+      } else {
+        rc = lo_sample_negatives_rng(first, count, np, k, cnt, &rng, negs);
+        if (rc) goto done;
+        if (neg_dump) memcpy(neg_dump + neg_pos, negs, cnt * k * sizeof(uint32_t));
+        neg_pos += cnt * k;
+      }
       double l = 0.0;
       uint64_t un = 0, ur = 0;
       rc = lo_batch(kind, d, E, S, num_nodes, relE, relS, num_rels, bucket + 3 * off, cnt, negs,
@@ -677,7 +738,7 @@ int lo_run_epoch(const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
     ++buckets_trained;
   }
 done:
-  free(bucket), free(pos), free(negs), free(batch_edges);
+  free(bucket), free(pos), free(negs), free(shared), free(batch_edges);
   if (loss_sum_out) *loss_sum_out = loss_sum;
   if (edges_trained_out) *edges_trained_out = edges_trained;
   if (buckets_trained_out) *buckets_trained_out = buckets_trained;

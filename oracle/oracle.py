@@ -75,9 +75,10 @@ class Oracle:
             bind("run_rounds", i32, [vp, u64, u64, u64, u32, vp, u64, u32, i32, u32, f64, f64,
                                      u32, u32, i32, u64, u32, vp, vp, vp, vp, vp, vp])
             bind("store_init", None, [u32, u64, u32, u64, u64, vp, vp, vp, vp])
-            bind("run_epoch", i32, [vp, u64, u64, u64, u32, u64, vp, vp, u64, vp, vp, vp, i32,
-                                    u32, f64, f64, u32, u32, i32, u64, u32, vp, vp, vp, vp, vp,
-                                    vp, vp, vp, u64, vp, vp, vp, vp, vp])
+            bind("run_epoch_ex", i32, [vp, u64, u64, u64, u32, u64, vp, vp, u64, vp, vp, vp,
+                                       i32, u32, f64, f64, u32, u32, u32, i32, u64, u32, vp, vp,
+                                       vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp, vp])
+            bind("expand_shared", i32, [vp, u64, u32, u32, vp])
         else:
             bind("store_init", i32, [C.c_char_p, u32, u64, u32, u64, u64, vp, vp, vp, vp])
             bind("run_epoch_inmem", i32, [vp, u64, u64, u64, u32, u64, vp, vp, vp, i32, u32, f64,
@@ -188,8 +189,10 @@ class Oracle:
 
     def run_epoch(self, edges, num_nodes, num_rels, n, plan, kind, E, S, relE, relS, *, dim,
                   lr=0.1, eps=1e-10, batch_size=100000, k=16, shuffle=True, seed=42, epoch=0,
-                  dumps=False):
-        """All-resident real-train epoch under `plan` (see plan_arrays), in place."""
+                  dumps=False, chunk=0):
+        """All-resident real-train epoch under `plan` (see plan_arrays), in place.
+        chunk > 0: shared-negative chunks (restatement only; k negatives per
+        chunk of `chunk` positives, expanded onto the reference batch math)."""
         kind = KINDS.get(kind, kind)
         edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
         Ecount = len(edges)
@@ -212,13 +215,14 @@ class Oracle:
             relS = np.zeros((1, dim), np.float32)
         if self.which == "restatement":
             stride, offsets, eorder = self.partition_plan(edges, num_nodes, n)
-            rc = self._fn["run_epoch"](
+            rc = self._fn["run_epoch_ex"](
                 _ptr(edges), Ecount, num_nodes, num_rels, n, stride, _ptr(offsets), _ptr(eorder),
                 S_, _ptr(states), _ptr(order), _ptr(soff), kind, dim, lr, eps, batch_size, k,
-                int(shuffle), seed, epoch, _ptr(E), _ptr(S), _ptr(relE), _ptr(relS), _ptr(loss),
+                chunk, int(shuffle), seed, epoch, _ptr(E), _ptr(S), _ptr(relE), _ptr(relS), _ptr(loss),
                 _ptr(et), _ptr(bt), _ptr(nb), maxb, _ptr(bl), _ptr(bn), _ptr(br), _ptr(pd),
                 _ptr(nd))
         else:
+            assert chunk == 0, "shared-negative chunks are not a reference mode"
             rc = self._fn["run_epoch_inmem"](
                 _ptr(edges), Ecount, num_nodes, num_rels, n, S_, _ptr(states), _ptr(order),
                 _ptr(soff), kind, dim, lr, eps, batch_size, k, int(shuffle), seed, epoch, _ptr(E),
@@ -231,7 +235,14 @@ class Oracle:
             b = out["num_batches"]
             out.update(batch_loss=bl[:b].copy(), batch_nodes=bn[:b].copy(),
                        batch_rels=br[:b].copy(), perm=pd[:Ecount].copy(),
-                       negs=nd[:out["edges_trained"] * k].copy())
+                       negs=nd[:out["edges_trained"] * k].copy() if not chunk else nd)
+        return out
+
+    def expand_shared(self, shared, cnt, k, chunk):
+        """[ceil(cnt/chunk) * k] shared draws -> the [cnt * k] per-positive list."""
+        shared = np.ascontiguousarray(shared, np.uint32)
+        out = np.zeros(cnt * k, np.uint32)
+        self._check(self._fn["expand_shared"](_ptr(shared), cnt, k, chunk, _ptr(out)))
         return out
 
     def bucket_sample(self, kind, bucket_edges, first, count, stream_seed, E, S, relE, relS, *,

@@ -106,6 +106,9 @@ struct lgd_context {
   uint32_t k_cap = 0;
   DevBuf<double> w, mix, loss, part_first, part_last;
   DevBuf<float> snap;
+  // shared-negative chunks (shared.cu)
+  DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowmax, sn_rowinv, sn_G;
+  DevBuf<double> sn_pos;
   DevBuf<uint32_t> node_keys, node_vals, rel_keys, iota, skeys, svals;
   DevBuf<uint8_t> chunk_flags;
   DevBuf<uint32_t> span_list;
@@ -126,6 +129,7 @@ struct lgd_context {
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
+  double score_bytes_total = 0.0;  // algorithmic score-phase bytes since the call began
 
   ~lgd_context() {
     cudaSetDevice(device);
@@ -140,6 +144,19 @@ struct lgd_context {
 
   bool typed() const { return kind != LGD_MODEL_DOT; }
   uint32_t k() const { return opt.negatives; }
+  uint32_t chunk() const { return opt.shared_chunk; }
+  // negative ids a batch of P positives draws: P k, or ceil(P / C) k shared
+  uint64_t batch_negs(uint64_t P) const {
+    return chunk() ? (P + chunk() - 1) / chunk() * k() : P * k();
+  }
+  // a bucket's draws: its batches' in order (pipeline.cpp:303-308)
+  uint64_t bucket_negs(uint64_t m) const {
+    const uint64_t B = opt.batch_size, full = m / B, rest = m - full * B;
+    return full * batch_negs(B) + batch_negs(rest);
+  }
+  uint64_t batch_items(uint64_t P) const {  // node-gradient contributions
+    return chunk() ? 2 * P + batch_negs(P) : P * (k() + 2);
+  }
 
   uint64_t part_begin(uint32_t p) const { return stride * p; }
   uint64_t part_rows(uint32_t p) const {
@@ -153,7 +170,7 @@ struct lgd_context {
     H.reserve(cap);
     perm.reserve(cap);
     shuffled.reserve(cap * 3);
-    negs.reserve(cap * std::max<uint32_t>(k(), 1));
+    negs.reserve(std::max<uint64_t>(bucket_negs(cap), 1));
     sh_keys_in.reserve(cap);
     sh_vals_in.reserve(cap);
     sh_keys_out.reserve(cap);
@@ -168,8 +185,21 @@ struct lgd_context {
     const uint32_t kk = k();
     if (P <= batch_cap && kk <= k_cap) return;
     P = std::max(P, batch_cap);
-    const uint64_t items = P * (kk + 2);
-    w.reserve(P * kk + P);  // + TransE's dst coefficients
+    const uint64_t items = batch_items(P);
+    if (chunk()) {
+      const SharedShape sh = shared_shape(dim, kk, chunk(), P);
+      const uint64_t rows = sh.nch * sh.tpc * 128;
+      sn_A.reserve(rows * sh.dpad);
+      sn_AT.reserve(rows * sh.dpad);
+      sn_B.reserve(sh.nch * sh.kpad * sh.dpad);
+      sn_BT.reserve(sh.nch * sh.kpad * sh.dpad);
+      sn_rowmax.reserve(rows);
+      sn_rowinv.reserve(rows);
+      sn_G.reserve(sh.nch * sh.kpad * dim);
+      sn_pos.reserve(P);
+    } else {
+      w.reserve(P * kk + P);  // + TransE's dst coefficients
+    }
     mix.reserve(P * dim);
     snap.reserve(P * dim);
     loss.reserve(P);
@@ -245,10 +275,44 @@ struct lgd_context {
     }
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
+    if (chunk()) {
+      const SharedShape sh = shared_shape(dim, a.k, chunk(), P);
+      a.chunk = chunk();
+      a.dpad = sh.dpad;
+      a.kpad = sh.kpad;
+      a.tpc = sh.tpc;
+      a.nch = sh.nch;
+      a.sh_A = sn_A.get();
+      a.sh_B = sn_B.get();
+      a.sh_AT = sn_AT.get();
+      a.sh_BT = sn_BT.get();
+      a.sh_rowmax = sn_rowmax.get();
+      a.sh_rowinv = sn_rowinv.get();
+      a.sh_pos = sn_pos.get();
+      a.sh_G = sn_G.get();
+    }
     return a;
   }
 
+  // Shared-negative chunks: dot-product scores (the tensor-core contraction),
+  // vector-lane dims (d % 4 == 0, ComplEx h even) up to 128.
+  void check_shared() const {
+    if (!chunk()) return;
+    if (kind == LGD_MODEL_TRANSE)
+      throw std::invalid_argument("shared negatives need a dot-product score (not TransE)");
+    const bool vec = kind == LGD_MODEL_COMPLEX ? (dim / 2) % 2 == 0 : dim % 4 == 0;
+    if (!vec || dim > 128)
+      throw std::invalid_argument("shared negatives need dim % 4 == 0 (ComplEx: dim % 4) and dim <= 128");
+  }
+
   uint64_t batch_launches(int node_bits = -1) const {
+    if (chunk()) {  // prep, gather, SG1-3, loss, node sort, pass 1/2 (+ relation path)
+      const int nb = node_bits >= 0 ? node_bits : bits_for(V ? V - 1 : 0);
+      const int rb = bits_for(R ? R - 1 : 0);
+      uint64_t c = 6 + 2 + 2 + (nb + 7) / 8;
+      if (typed()) c += 2 + 2 + (rb + 7) / 8;
+      return c;
+    }
     // K3 + loss reduce + pass1 + pass2 (+ relation pass1/2) + radix sorts
     // (upsweep histogram + scan + one onesweep pass per 8 key bits)
     const int nb = node_bits >= 0 ? node_bits : bits_for(V ? V - 1 : 0);
@@ -299,6 +363,7 @@ struct lgd_context {
                  const Pool* pool = nullptr, double* rel_grad_out = nullptr,
                  uint8_t* rel_flag_out = nullptr) {
     BatchArgs a = batch_args(bedges, bnegs, P, loss_out, pool);
+    score_bytes_total += score_bytes(P);
     if (rel_grad_out) {  // lock-step rounds: relation gradient only, applied later
       a.grad_rels = rel_grad_out;
       a.grad_rel_flag = rel_flag_out;
@@ -312,12 +377,18 @@ struct lgd_context {
       // algorithmic bytes per phase: score reads the edge and
       // (2 + k + t) rows per positive; the update's row traffic is added
       // from the unique counts at the end of the call.
-      kstats[LGD_KSTAT_SCORE].algorithmic_bytes +=
-          double(P) * (12.0 + 4.0 * dim * (2 + k() + (typed() ? 1 : 0)));
+      kstats[LGD_KSTAT_SCORE].algorithmic_bytes += score_bytes(P);
     } else {
       launch_train_batch(a, stream, nullptr);
     }
     launches += batch_launches(a.node_key_bits);
+  }
+
+  // algorithmic bytes of the score phase: the edge record and
+  // (2 + t) rows per positive, plus k rows per positive or per shared chunk
+  double score_bytes(uint64_t P) const {
+    return double(P) * (12.0 + 4.0 * dim * (2 + (typed() ? 1 : 0))) +
+           4.0 * dim * double(batch_negs(P));
   }
 
   Pool pool_of_state(size_t s) const {
@@ -347,6 +418,7 @@ struct lgd_context {
     if (opt.batch_size == 0) throw std::invalid_argument("batch size must be positive");
     if (opt.negatives == 0)
       throw std::invalid_argument("at least one negative per positive required");
+    check_shared();
   }
 
   // One bucket of work: bucket (bi, bj), its RNG stream index g (the
@@ -422,7 +494,7 @@ struct lgd_context {
     StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, it.g)), pos.get(),
                     reject.get()};
     if (bev) LGD_CUDA(cudaEventRecord(bev[1], stream));
-    launch_sample_nodes(slot, m * k(), it.pool, negs.get(), stream);
+    launch_sample_nodes(slot, bucket_negs(m), it.pool, negs.get(), stream);
     launches += 2;
     if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
   }
@@ -473,9 +545,8 @@ struct lgd_context {
       out->unique_rels = cnt[1];
       out->h2d_bytes = h2d_bytes;
       out->d2h_bytes = nb * 8 + sizeof cnt;
-      out->algorithmic_bytes =
-          double(edges_trained) * (12.0 + 4.0 * dim * (2 + kk + (typed() ? 1 : 0))) +
-          16.0 * dim * double(cnt[0] + cnt[1]);
+      (void)kk;
+      out->algorithmic_bytes = score_bytes_total + 16.0 * dim * double(cnt[0] + cnt[1]);
     }
   }
 
@@ -506,6 +577,7 @@ struct lgd_context {
     };
     LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
     LGD_CUDA(cudaEventRecord(ev_begin, stream));
+    score_bytes_total = 0.0;
     if (host_bucketed) {
       staging[0].reserve(max_m * 3);
       staging[1].reserve(max_m * 3);
@@ -537,8 +609,8 @@ struct lgd_context {
       sample_bucket(it, epoch, m, bev);
       for (uint64_t o = 0; o < m; o += opt.batch_size) {
         const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
-        run_batch(shuffled.get() + 3 * o, negs.get() + o * kk, P, batch_losses.get() + nb,
-                  &it.pool);
+        run_batch(shuffled.get() + 3 * o, negs.get() + (o / opt.batch_size) * batch_negs(opt.batch_size),
+                  P, batch_losses.get() + nb, &it.pool);
         ++nb;
       }
       edges_trained += m;
@@ -582,6 +654,7 @@ struct lgd_context {
     round_epoch = epoch;
     round_prepared = ~size_t(0);
     round_nb = round_edges = round_buckets = 0;
+    score_bytes_total = 0.0;
     LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
     LGD_CUDA(cudaEventRecord(ev_begin, stream));
     return round_batches;
@@ -608,7 +681,8 @@ struct lgd_context {
       }
       const uint64_t o = (step - round_first_batch[i]) * opt.batch_size;
       const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
-      run_batch(shuffled.get() + 3 * o, negs.get() + o * k(), P, batch_losses.get() + round_nb,
+      run_batch(shuffled.get() + 3 * o, negs.get() + (o / opt.batch_size) * batch_negs(opt.batch_size),
+                P, batch_losses.get() + round_nb,
                 &it.pool, typed() ? rel_grad.get() : nullptr, typed() ? rel_flag.get() : nullptr);
       ++round_nb;
     }
@@ -634,7 +708,11 @@ struct lgd_context {
     if (!tables_ready) throw std::invalid_argument("embedding store not initialised");
     if (opt.negatives == 0)
       throw std::invalid_argument("at least one negative per positive required");
-    const uint32_t kk = k();
+    check_shared();
+    const uint64_t nn = batch_negs(P);
+    for (uint64_t q = 0; q < nn; ++q)
+      if (h_negs[q] >= V)
+        throw std::out_of_range("node " + std::to_string(h_negs[q]) + " is not resident");
     for (uint64_t p = 0; p < P; ++p) {
       const uint32_t s = h_edges[3 * p], r = h_edges[3 * p + 1], t = h_edges[3 * p + 2];
       if (s >= V || t >= V) throw std::out_of_range("node " + std::to_string(s >= V ? s : t) +
@@ -644,16 +722,12 @@ struct lgd_context {
           throw std::invalid_argument("typed model requires a relation id on every edge");
         if (r >= R) throw std::out_of_range("relation id out of range");
       }
-      for (uint32_t j = 0; j < kk; ++j)
-        if (h_negs[p * kk + j] >= V)
-          throw std::out_of_range("node " + std::to_string(h_negs[p * kk + j]) +
-                                  " is not resident");
     }
     op_edges.reserve(std::max<uint64_t>(P * 3, 3));
-    op_negs.reserve(std::max<uint64_t>(P * kk, 1));
+    op_negs.reserve(std::max<uint64_t>(nn, 1));
     if (P) {
       LGD_CUDA(cudaMemcpyAsync(op_edges.get(), h_edges, P * 12, cudaMemcpyHostToDevice, stream));
-      LGD_CUDA(cudaMemcpyAsync(op_negs.get(), h_negs, P * kk * 4, cudaMemcpyHostToDevice, stream));
+      LGD_CUDA(cudaMemcpyAsync(op_negs.get(), h_negs, nn * 4, cudaMemcpyHostToDevice, stream));
     }
     ensure_batch(std::max<uint64_t>(P, 1));
     batch_losses.reserve(1);

@@ -686,9 +686,10 @@ struct SegCtx {  // hoisted kernel arguments
   const uint32_t* rel_keys;
   uint32_t d, k, sbits, smask;
   uint64_t cpos_off;  // TransE: offset of the dst coefficients in w (P k)
+  const float* gneg;  // shared-negative mode: gradient rows of the shared negatives
 };
 
-template <int KIND, int NV, bool REL>
+template <int KIND, int NV, bool REL, bool SH>
 __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>& L, uint32_t val,
                                           bool pred, ItemRegs<4 * NV>& it) {
   if (REL) {
@@ -703,6 +704,11 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
   it.slot = slot;
+  if (SH && slot == 1) {  // shared negative: its precomputed gradient row (shared.cu SG3)
+    it.w = 0.0;
+    L.template ldf<true>(x.gneg + (uint64_t)p * x.d, pred, it.sv);
+    return;
+  }
   // dst (slot 0) uses w = -1: g - IR1 == g + (-1 * IR1) in IEEE arithmetic;
   // TransE's dst coefficient sits after the P x k negative coefficients
   it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1))
@@ -716,10 +722,15 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   L.ldd(x.mix + row, pred && is_src, it.mv);
 }
 
-template <int KIND, int NV, bool REL>
+template <int KIND, int NV, bool REL, bool SH>
 __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
                                            const float* own) {
   constexpr int NE = 4 * NV;
+  if (SH && !REL && it.slot == 1) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] += (double)it.sv[e];
+    return;
+  }
   if (REL || it.slot > k) {  // adj_other(mix): other = src snapshot (REL) or relation row
     const float* o = REL ? it.sv : it.rv;
     if (KIND == 2) {
@@ -768,7 +779,7 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
   }
 }
 
-template <int KIND, int NV, bool REL>
+template <int KIND, int NV, bool REL, bool SH>
 __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     BatchArgs a, uint64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
@@ -779,7 +790,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
   if (base >= n) return;
   const Lanes<KIND, NV> L(lane, a.dim);
   const SegCtx x{a.snap, a.mix, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
-                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u, a.P * a.k};
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u, a.P * a.k, a.sh_G};
   constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
   float* __restrict__ theta = REL ? a.rel_theta : a.theta;
   float* __restrict__ state = REL ? a.rel_state : a.state;
@@ -836,7 +847,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       const bool fin = finishing(t) && !gout;
       L.template ldf<false>(theta + row, fin || kOwn, cth);
       L.template ldf<false>(state + row, fin, cst);
-      load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
+      load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
     }
     for (; t < np; ++t) {
       const int nxt = rest ? __ffs(rest) - 1 : nlive;
@@ -851,16 +862,16 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         const bool fin = has_next && finishing(t + 1) && !gout;
         L.template ldf<false>(theta + row, fin || (kOwn && has_next), nth);
         L.template ldf<false>(state + row, fin, nst);
-        load_item<KIND, NV, REL>(x, L, __shfl_sync(0xffffffffu, val, ns), has_next, nit);
+        load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, ns), has_next, nit);
       }
       double acc[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-      add_loaded<KIND, NV, REL>(cit, x.k, acc, cth);
+      add_loaded<KIND, NV, REL, SH>(cit, x.k, acc, cth);
       for (int q = cur + 1; q < pend; ++q) {
         ItemRegs<NE> it;
-        load_item<KIND, NV, REL>(x, L, item_val(q), true, it);
-        add_loaded<KIND, NV, REL>(it, x.k, acc, cth);
+        load_item<KIND, NV, REL, SH>(x, L, item_val(q), true, it);
+        add_loaded<KIND, NV, REL, SH>(it, x.k, acc, cth);
       }
       const uint32_t rowid = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {
@@ -997,10 +1008,29 @@ int vec_width(uint32_t d) {
   return d <= 128 ? 1 : (d <= 256 ? 2 : 0);
 }
 
-template <int KIND, int NV, bool REL>
+template <int KIND, int NV, bool REL, bool SH = false>
 void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
-  segment_pass1_vec<KIND, NV, REL><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
-                                                                 a.span_list, a.span_count);
+  segment_pass1_vec<KIND, NV, REL, SH><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
+                                                                     a.span_list, a.span_count);
+}
+
+// shared-negative mode: node items are dst / shared negative / src (slots 0-2)
+template <int KIND>
+void run_segments_shared(const BatchArgs& a, uint64_t items, cudaStream_t st) {
+  LGD_CUDA(cudaMemsetAsync(a.span_count, 0, sizeof(unsigned int), st));
+  const unsigned grid = ceil_div(ceil_div(items, 32), kSegThreads / 32);
+  const int nv = vec_width<KIND>(a.dim);
+  if (nv == 1) {
+    launch_vec_pass1<KIND, 1, false, true>(a, items, grid, st);
+  } else if (nv == 2) {
+    launch_vec_pass1<KIND, 2, false, true>(a, items, grid, st);
+  } else {
+    throw std::invalid_argument("shared negatives need a vector-lane dimension");
+  }
+  LGD_LAUNCH_CHECK();
+  segment_pass2<false><<<(unsigned)a.sm_count * 4, kPass2Threads, 0, st>>>(
+      a, items, a.skeys, a.span_list, a.span_count);
+  LGD_LAUNCH_CHECK();
 }
 
 template <int KIND, int NC>
@@ -1093,10 +1123,47 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   rec(4);
 }
 
+// Shared-negative chunks: shared.cu computes loss, mix and the negatives'
+// gradient rows on the tensor cores; the node / relation updates are the
+// same segmented reduction + Adagrad as the exact path.
+template <int KIND, int NC>
+void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
+  auto rec = [&](int i) {
+    if (ev && ev->enabled) LGD_CUDA(cudaEventRecord(ev->ev[i], st));
+  };
+  const uint64_t P = a.P;
+  rec(0);
+  launch_shared_scores(a, st);
+  loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
+  LGD_LAUNCH_CHECK();
+  rec(1);
+  BatchArgs b = a;  // node items: (index << 2) | slot, slot 0 dst, 1 negative, 2 src
+  b.k = 1;
+  b.slot_bits = 2;
+  const uint64_t items = 2 * P + a.nch * a.k;
+  sort_items(b, items, b.node_keys, b.node_vals, b.node_key_bits, st);
+  rec(2);
+  run_segments_shared<KIND>(b, items, st);
+  rec(3);
+  if (KIND != 0) {
+    sort_items(a, P, a.rel_keys, a.iota, a.rel_key_bits, st);
+    run_segments<KIND, NC>(a, P, true, st);
+  }
+  rec(4);
+}
+
 template <int KIND>
 void run_kind(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   const uint32_t lanes_elems = KIND == 2 ? a.dim / 2 : a.dim;
   const uint32_t nc = (lanes_elems + kGroup - 1) / kGroup;
+  if constexpr (KIND == 3) {
+    if (a.chunk) throw std::invalid_argument("shared negatives: TransE is not a dot-product score");
+  } else if (a.chunk) {
+    if (nc <= 4) return run_batch_shared<KIND, 4>(a, st, ev);
+    if (nc <= 8) return run_batch_shared<KIND, 8>(a, st, ev);
+    if (nc <= 16) return run_batch_shared<KIND, 16>(a, st, ev);
+    return run_batch_shared<KIND, 32>(a, st, ev);
+  }
   if (nc <= 1) return run_batch<KIND, 1>(a, st, ev);
   if (nc <= 2) return run_batch<KIND, 2>(a, st, ev);
   if (nc <= 4) return run_batch<KIND, 4>(a, st, ev);

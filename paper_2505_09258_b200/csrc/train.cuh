@@ -54,7 +54,29 @@ struct BatchArgs {
   double* grad_rels;
   uint8_t* grad_rel_flag;
   int sm_count;
+  // shared-negative chunks (shared.cu): chunk = 0 is the reference's
+  // per-positive mode; otherwise negs holds nch x k shared ids
+  uint32_t chunk;
+  uint32_t kpad, dpad, tpc;   // k -> multiple of 128, dim -> multiple of 16, tiles per chunk
+  uint64_t nch;               // chunks in this batch
+  float* sh_A;                // IR1 tiles, core-matrix layout (nch x tpc x 128 rows x dpad)
+  float* sh_AT;               // IR1^T per 64-positive slice (dpad x 64), core-matrix layout
+  float* sh_B;                // negative rows, core-matrix layout (nch x kpad x dpad)
+  float* sh_BT;               // N^T per 64-negative block (dpad x 64)
+  float* sh_rowmax;           // per padded tile row: max score, 1 / sum exp
+  float* sh_rowinv;
+  double* sh_pos;             // P positive scores (FP64)
+  float* sh_G;                // nch x kpad x dim: gradient of every shared negative
 };
+
+struct SharedShape {
+  uint32_t dpad, kpad, tpc;
+  uint64_t nch;
+};
+SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P);
+size_t shared_smem_bytes(uint32_t dpad);
+// prep + negative gather + the three tcgen05 kernels (scores, mix, gradients)
+void launch_shared_scores(const BatchArgs& a, cudaStream_t st);
 
 struct BatchEvents {  // optional per-phase timing (profiling mode)
   cudaEvent_t ev[5];

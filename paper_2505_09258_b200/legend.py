@@ -47,7 +47,7 @@ _ERRORS = {1: InvalidArgument, 2: LogicError, 3: OutOfRange, 4: RuntimeFailure}
 class _Options(C.Structure):
     _fields_ = [("learning_rate", C.c_double), ("adagrad_epsilon", C.c_double),
                 ("batch_size", C.c_uint32), ("negatives", C.c_uint32), ("shuffle", C.c_int32),
-                ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+                ("shared_chunk", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class _EpochResult(C.Structure):
@@ -162,10 +162,20 @@ class TrainOptions:
     negatives: int = 16
     shuffle: bool = True
     seed: int = 0
+    # 0: independent negatives per positive (the reference).  C > 0: every C
+    # consecutive positives share `negatives` ids (tensor-core scoring; not a
+    # reference mode -- DESIGN.md section 4b)
+    shared_chunk: int = 0
 
     def _c(self):
         return _Options(self.learning_rate, self.adagrad_epsilon, self.batch_size,
-                        self.negatives, int(self.shuffle), 0, self.seed)
+                        self.negatives, int(self.shuffle), self.shared_chunk, self.seed)
+
+    def batch_negatives(self, positives: int) -> int:
+        """Negative ids one batch of `positives` consumes."""
+        if self.shared_chunk:
+            return -(-positives // self.shared_chunk) * self.negatives
+        return positives * self.negatives
 
 
 @dataclass
@@ -556,8 +566,9 @@ class Trainer:
         loss = np.zeros(1, np.float64)
         nn = np.zeros(1, np.uint64)
         nr = np.zeros(1, np.uint64)
-        ids = np.zeros(P * (k + 2) + 1, np.uint32)
-        g = np.zeros((P * (k + 2) + 1, d), np.float64)
+        cap = min(P * (k + 2), max(self.num_nodes, 1)) + 1
+        ids = np.zeros(cap, np.uint32)
+        g = np.zeros((cap, d), np.float64)
         rids = np.zeros(P + 1, np.uint32)
         rg = np.zeros((P + 1, d), np.float64)
         _check(library().lgd_batch_gradients(self._h, _p(edges), P, _p(negs), _p(loss), _p(nn),
