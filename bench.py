@@ -41,6 +41,14 @@ K_NEG, BATCH, LR, SEED, ALPHA, GRAPH_SEED = 16, 100_000, 0.1, 42, 2.3, 20250509
 REF_SAMPLE_POSITIVES = 25_000  # positives per reference step (bounded CPU sample)
 
 
+def peaks_tensor():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    except Exception:
+        return 1590.0, "fallback"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -174,10 +182,10 @@ def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
             "seconds": dt, "edges": done}
 
 
-def setup_trainer(cfg, device):
+def setup_trainer(cfg, device, k=K_NEG, chunk=0):
     import paper_2505_09258_b200 as lgd
-    opts = lgd.TrainOptions(learning_rate=LR, batch_size=BATCH, negatives=K_NEG, shuffle=True,
-                            seed=SEED)
+    opts = lgd.TrainOptions(learning_rate=LR, batch_size=BATCH, negatives=k, shuffle=True,
+                            seed=SEED, shared_chunk=chunk)
     t = lgd.Trainer(lgd.ScoreModel(cfg["model"], cfg["dim"]), opts, device=device)
     t.generate_graph(cfg["nodes"], cfg["rels"], cfg["edges"], ALPHA, GRAPH_SEED)
     t.make_partition_plan(cfg["n"])
@@ -334,6 +342,11 @@ def main():
                          "partition-round schedule (default for N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--negatives", type=int, default=K_NEG,
+                    help="negatives per positive (or per shared chunk)")
+    ap.add_argument("--shared-chunk", type=int, default=0,
+                    help="C > 0: shared-negative chunks of C positives scored on the tensor "
+                         "cores (not a reference mode: no CPU baseline)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank, world, local, pg = dist_setup(args.gpus)
@@ -349,7 +362,7 @@ def main():
         return
     import paper_2505_09258_b200 as lgd
     t_setup = time.perf_counter()
-    t = setup_trainer(cfg, local)
+    t = setup_trainer(cfg, local, args.negatives, args.shared_chunk)
     G = cfg["n"] ** 2
     # weak scaling: rank r trains its own K consecutive buckets of the plan
     # (tables replicated per GPU)
@@ -414,8 +427,20 @@ def main():
         e2e = {"value": edges_all / wall, "unit": "edges/s",
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
+    tensor = None
+    if args.shared_chunk:  # the chunk x negatives x dim contractions on tcgen05
+        sc = stats["score"]
+        bf16, _ = peaks_tensor()
+        flops = 6.0 * res.edges_trained * args.negatives * cfg["dim"]  # 6 P k d
+        tensor = {"bound": "tensor", "kernel": "score phase: prep + gather + SG1/SG2/SG3 "
+                  "(tcgen05.mma kind::tf32)", "achieved": flops / (sc["total_ms"] / 1e3) / 1e12,
+                  "peak": bf16 / 2, "unit": "TFLOP/s",
+                  "frac": flops / (sc["total_ms"] / 1e3) / 1e12 / (bf16 / 2),
+                  "peak_source": "measured bf16 dense / 2 (TF32 rate)",
+                  "flops_per_step": flops / args.steps, "score_ms": round(sc["total_ms"], 3)}
+
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and not args.shared_chunk:
         offsets = t.bucket_offsets
         b = 1 if cfg["n"] > 1 else 0
         a0, a1 = int(offsets[b]), int(offsets[b + 1])
@@ -433,7 +458,11 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "num_nodes": cfg["nodes"],
                        "num_edges": cfg["edges"], "num_relations": cfg["rels"],
-                       "dim": cfg["dim"], "partitions": cfg["n"], "negatives": K_NEG,
+                       "dim": cfg["dim"], "partitions": cfg["n"], "negatives": args.negatives,
+                       "negatives_mode": (f"shared chunks of {args.shared_chunk} positives, "
+                                          f"{args.negatives} negatives each; TF32 tensor-core "
+                                          "scores, FP32 accumulate, FP64 updates"
+                                          if args.shared_chunk else "independent per positive"),
                        "batch_size": BATCH, "storage": "f32 (E||S), FP64 arithmetic",
                        "graph": f"power-law alpha={ALPHA}, generator seed {GRAPH_SEED}",
                        "step": "one bucket of the reference iteration plan",
@@ -446,6 +475,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
         }
+        if tensor:
+            line["tensor_roofline"] = tensor
         print(json.dumps(line), flush=True)
     t.close()
     if pg is not None:

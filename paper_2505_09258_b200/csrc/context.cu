@@ -248,6 +248,13 @@ struct lgd_context {
     a.node_vals = node_vals.get();
     a.slot_bits = bits_for(a.k + 1);
     if ((P << a.slot_bits) >> 32) throw std::invalid_argument("batch too large for 32-bit payloads");
+    // the relation id rides in the payload when it fits: K4 then needs no
+    // dependent rel_keys[p] load per contribution
+    a.rel_bits = 0;
+    if (typed() && R && !chunk()) {
+      const int rb = bits_for(R - 1);
+      if (bits_for(P ? P - 1 : 0) + a.slot_bits + rb <= 32) a.rel_bits = rb;
+    }
     a.rel_keys = rel_keys.get();
     a.iota = iota.get();
     a.skeys = skeys.get();

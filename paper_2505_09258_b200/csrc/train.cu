@@ -37,6 +37,7 @@ namespace {
 
 constexpr int kScoreWarps = 4;
 constexpr int kSegThreads = 256;
+constexpr int kSegDepth = 4;  // pieces whose theta / state rows are in flight per warp
 constexpr int kPass2Threads = 256;
 constexpr uint8_t kNoHead = 1;
 constexpr uint8_t kContOut = 2;
@@ -288,7 +289,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
     const uint64_t kb = p * (k + 2);
     for (uint32_t r = lane; r < nrows; r += 32) {
       const uint32_t id = pid[r];
-      const uint32_t pv = (uint32_t)p << a.slot_bits;  // payload: positive, slot
+      // payload: positive, (relation,) slot
+      const uint32_t pv = ((uint32_t)p << (a.slot_bits + a.rel_bits)) |
+                          (a.rel_bits ? pid[1] << a.slot_bits : 0u);
       if (r == 0) {
         a.node_keys[kb + k + 1] = to_pool(a, id);
         a.node_vals[kb + k + 1] = pv | (k + 1);
@@ -376,7 +379,7 @@ __device__ __forceinline__ void add_item(const BatchArgs& a, uint32_t val, int g
     }
     return;
   }
-  const uint64_t p = val >> a.slot_bits;
+  const uint64_t p = val >> (a.slot_bits + a.rel_bits);
   const uint32_t slot = val & ((1u << a.slot_bits) - 1u);
   const bool is_src = slot > k;
   const float* rel = KIND != 0 ? a.rel_theta + (size_t)__ldg(a.rel_keys + p) * d : nullptr;
@@ -606,6 +609,54 @@ struct Lanes {
       }
     }
   }
+  // cp.async the lane's elements of a global row into the same positions of
+  // a shared-memory row (zero-filled when !pred); lds reads them back.  Each
+  // lane only ever touches its own elements, so no warp sync is needed.
+  __device__ __forceinline__ void cpa(float* s, const float* g, bool pred) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!ok[v]) continue;
+      const uint32_t n = pred ? (KIND == 2 ? 8u : 16u) : 0u;
+      if (KIND == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s + off[v])),
+                     "l"(g + off[v]), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s + off[v] + h)),
+                     "l"(g + off[v] + h), "r"(n)
+                     : "memory");
+      } else {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s + off[v])),
+                     "l"(g + off[v]), "r"(n)
+                     : "memory");
+      }
+    }
+  }
+  __device__ __forceinline__ void lds(const float* s, float* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (KIND == 2) {
+        float2 re = make_float2(0.f, 0.f), im = make_float2(0.f, 0.f);
+        if (ok[v]) {
+          re = *reinterpret_cast<const float2*>(s + off[v]);
+          im = *reinterpret_cast<const float2*>(s + off[v] + h);
+        }
+        x[4 * v] = re.x;
+        x[4 * v + 1] = re.y;
+        x[4 * v + 2] = im.x;
+        x[4 * v + 3] = im.y;
+      } else {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok[v]) t = *reinterpret_cast<const float4*>(s + off[v]);
+        x[4 * v] = t.x;
+        x[4 * v + 1] = t.y;
+        x[4 * v + 2] = t.z;
+        x[4 * v + 3] = t.w;
+      }
+    }
+  }
   __device__ __forceinline__ void ldd(const double* b, bool pred, double* x) const {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -668,6 +719,25 @@ __device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, do
   th = (float)((double)th - (zero ? num : q));
 }
 
+// adagrad_update (train.cpp:342-354) on the lane's elements: only vectors
+// the lane owns run it (an idle lane's zero gradient would otherwise send the
+// warp through the IEEE slow path of 0 / x and sqrt(0)); a genuinely zero
+// gradient is exact through that slow path.
+template <int KIND, int NV>
+__device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const double* acc,
+                                              float* th, float* st, double lr, double eps) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (!L.ok[v]) continue;
+#pragma unroll
+    for (int e = 4 * v; e < 4 * v + 4; ++e) {
+      const double a2 = (double)st[e] + acc[e] * acc[e];
+      st[e] = (float)a2;
+      th[e] = (float)((double)th[e] - lr * acc[e] / (sqrt(a2) + eps));
+    }
+  }
+}
+
 // One contribution's operands: the src snapshot (dst / negative items), the
 // relation row, mix (src items) and the softmax weight.
 template <int NE>
@@ -685,6 +755,7 @@ struct SegCtx {  // hoisted kernel arguments
   const float* rel_theta;
   const uint32_t* rel_keys;
   uint32_t d, k, sbits, smask;
+  uint32_t pshift, rmask;  // positive = val >> pshift; relation = (val >> sbits) & rmask (0: look up)
   uint64_t cpos_off;  // TransE: offset of the dst coefficients in w (P k)
   const float* gneg;  // shared-negative mode: gradient rows of the shared negatives
 };
@@ -700,7 +771,7 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
     it.w = 0.0;
     return;
   }
-  const uint32_t p = val >> x.sbits;
+  const uint32_t p = val >> x.pshift;
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
   it.slot = slot;
@@ -715,7 +786,7 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
          : (KIND == 3 && pred && slot == 0) ? __ldg(x.w + x.cpos_off + p) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
   if (KIND != 0) {
-    const uint32_t r = pred ? __ldg(x.rel_keys + p) : 0;
+    const uint32_t r = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
     L.template ldf<true>(x.rel_theta + (uint64_t)r * x.d, pred, it.rv);
   }
   L.template ldf<true>(x.snap + row, pred && !is_src, it.sv);
@@ -790,7 +861,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
   if (base >= n) return;
   const Lanes<KIND, NV> L(lane, a.dim);
   const SegCtx x{a.snap, a.mix, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
-                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u, a.P * a.k, a.sh_G};
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G};
   constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
   float* __restrict__ theta = REL ? a.rel_theta : a.theta;
   float* __restrict__ state = REL ? a.rel_state : a.state;
@@ -837,64 +910,71 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
   if (lead_done) rest &= rest - 1;
   int t = lead_done ? 1 : 0;
   if (t < np) {
-    int cur = __ffs(rest) - 1;
-    rest &= rest - 1;
-    float cth[NE], cst[NE];
-    ItemRegs<NE> cit;
     auto rowof = [&](uint32_t kk) { return REL ? kk : from_pool(a, kk); };
-    {
-      const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, cur)) * d;
-      const bool fin = finishing(t) && !gout;
-      L.template ldf<false>(theta + row, fin || kOwn, cth);
-      L.template ldf<false>(state + row, fin, cst);
-      load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
-    }
-    for (; t < np; ++t) {
-      const int nxt = rest ? __ffs(rest) - 1 : nlive;
-      rest &= rest - 1;
-      const bool has_next = t + 1 < np;
-      const int pend = (t == np - 1 && ext_short) ? nlive + ext : nxt;
-      float nth[NE], nst[NE];
-      ItemRegs<NE> nit;
-      {
-        const int ns = nxt & 31;
-        const uint64_t row = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, ns)) * d;
-        const bool fin = has_next && finishing(t + 1) && !gout;
-        L.template ldf<false>(theta + row, fin || (kOwn && has_next), nth);
-        L.template ldf<false>(state + row, fin, nst);
-        load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, ns), has_next, nit);
+    // theta / state rows of the next kSegDepth pieces are in flight at once:
+    // cp.async into this warp's shared-memory ring (no registers held), one
+    // commit group per piece.  The first contribution of the next piece is
+    // prefetched in registers.
+    extern __shared__ __align__(16) float seg_ring[];
+    const uint32_t rowf = (a.dim + 3) & ~3u;
+    const uint32_t slotf = 2 * rowf;  // slot: theta, state
+    float* ring = seg_ring + (size_t)(threadIdx.x >> 5) * kSegDepth * slotf;
+    const int t0 = t;
+    auto start_of = [&](int u) { return (int)__fns(smask, 0, u + 1); };  // u-th piece start
+    auto stage = [&](int u) {
+      if (u < np) {
+        const int s0 = start_of(u);
+        const uint64_t off = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, s0 & 31)) * d;
+        const bool fin = finishing(u) && !gout;
+        float* slot = ring + (u % kSegDepth) * slotf;
+        L.cpa(slot, theta + off, fin || kOwn);
+        L.cpa(slot + rowf, state + off, fin);
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int u = 0; u < kSegDepth; ++u) stage(t0 + u);
+    ItemRegs<NE> cit, nit;
+    int cur = start_of(t0);
+    load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
+#pragma unroll 1
+    for (; t < np; ++t) {
+      const bool has_next = t + 1 < np;
+      const int nxt = has_next ? start_of(t + 1) : nlive;
+      const int pend = (t == np - 1 && ext_short) ? nlive + ext : nxt;
+      load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, nxt & 31), has_next, nit);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
+      float th[NE], st[NE];
+      const float* slot = ring + (t % kSegDepth) * slotf;
+      L.lds(slot, th);
+      L.lds(slot + rowf, st);
       double acc[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-      add_loaded<KIND, NV, REL, SH>(cit, x.k, acc, cth);
+      add_loaded<KIND, NV, REL, SH>(cit, x.k, acc, th);
       for (int q = cur + 1; q < pend; ++q) {
         ItemRegs<NE> it;
         load_item<KIND, NV, REL, SH>(x, L, item_val(q), true, it);
-        add_loaded<KIND, NV, REL, SH>(it, x.k, acc, cth);
+        add_loaded<KIND, NV, REL, SH>(it, x.k, acc, th);
       }
-      const uint32_t rowid = rowof(__shfl_sync(0xffffffffu, key, cur));
+      const uint32_t row = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {
         L.std_(a.part_first + c * d, acc);
       } else if (!finishing(t)) {
         L.std_(a.part_last + c * d, acc);
       } else if (gout) {
-        L.std_(gout + (uint64_t)rowid * d, acc);
-        if (lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[rowid] = 1;
+        L.std_(gout + (uint64_t)row * d, acc);
+        if (lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[row] = 1;
       } else {
-#pragma unroll
-        for (int e = 0; e < NE; ++e) adagrad_fast(acc[e], cth[e], cst[e], lr, eps);
-        L.stf(theta + (uint64_t)rowid * d, cth);
-        L.stf(state + (uint64_t)rowid * d, cst);
+        adagrad_lanes(L, acc, th, st, lr, eps);
+        L.stf(theta + (uint64_t)row * d, th);
+        L.stf(state + (uint64_t)row * d, st);
       }
-#pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        cth[e] = nth[e];
-        cst[e] = nst[e];
-      }
+      stage(t + kSegDepth);  // the slot just read is free again
       cit = nit;
       cur = nxt;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   if (lane == 0) {
     const int heads = __popc(hmask);
@@ -1010,8 +1090,15 @@ int vec_width(uint32_t d) {
 
 template <int KIND, int NV, bool REL, bool SH = false>
 void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
-  segment_pass1_vec<KIND, NV, REL, SH><<<grid, kSegThreads, 0, st>>>(a, items, a.skeys, a.svals,
-                                                                     a.span_list, a.span_count);
+  const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
+  static size_t attr = 0;  // per instantiation: grows only
+  if (smem > attr) {
+    LGD_CUDA(cudaFuncSetAttribute(segment_pass1_vec<KIND, NV, REL, SH>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  segment_pass1_vec<KIND, NV, REL, SH><<<grid, kSegThreads, smem, st>>>(
+      a, items, a.skeys, a.svals, a.span_list, a.span_count);
 }
 
 // shared-negative mode: node items are dst / shared negative / src (slots 0-2)
@@ -1140,6 +1227,7 @@ void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev
   BatchArgs b = a;  // node items: (index << 2) | slot, slot 0 dst, 1 negative, 2 src
   b.k = 1;
   b.slot_bits = 2;
+  b.rel_bits = 0;
   const uint64_t items = 2 * P + a.nch * a.k;
   sort_items(b, items, b.node_keys, b.node_vals, b.node_key_bits, st);
   rec(2);

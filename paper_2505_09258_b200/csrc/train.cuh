@@ -41,6 +41,8 @@ struct BatchArgs {
   unsigned long long* counters;  // [0] unique nodes, [1] unique rels (accumulated)
   double* batch_loss_out;     // one double: this batch's loss
   int slot_bits;              // bits for a slot in [0, k+1]
+  int rel_bits;               // > 0: the relation id rides in the payload above the slot
+                              // (p << (slot_bits + rel_bits) | rel << slot_bits | slot)
   // resident sampling pool (<= 3 node ranges, ascending): contribution keys
   // are pool indices, so the radix sort needs bits_for(pool size) bits only
   uint64_t pool_first[3];
