@@ -742,10 +742,11 @@ __device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const do
 // relation row, mix (src items) and the softmax weight.
 template <int NE>
 struct ItemRegs {
-  float sv[NE], rv[NE];
+  float sv[NE];
   double mv[NE];
   double w;
   uint32_t slot;
+  uint32_t rel;  // relation row id: read at use (a small, L1-resident table)
 };
 
 struct SegCtx {  // hoisted kernel arguments
@@ -785,16 +786,15 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1))
          : (KIND == 3 && pred && slot == 0) ? __ldg(x.w + x.cpos_off + p) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
-  if (KIND != 0) {
-    const uint32_t r = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
-    L.template ldf<true>(x.rel_theta + (uint64_t)r * x.d, pred, it.rv);
-  }
+  if (KIND != 0)
+    it.rel = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
   L.template ldf<true>(x.snap + row, pred && !is_src, it.sv);
   L.ldd(x.mix + row, pred && is_src, it.mv);
 }
 
 template <int KIND, int NV, bool REL, bool SH>
-__device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
+__device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV>& L,
+                                           const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
                                            const float* own) {
   constexpr int NE = 4 * NV;
   if (SH && !REL && it.slot == 1) {
@@ -802,8 +802,10 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
     for (int e = 0; e < NE; ++e) acc[e] += (double)it.sv[e];
     return;
   }
+  float rv[NE];
+  if (KIND != 0 && !REL) L.template ldf<true>(x.rel_theta + (uint64_t)it.rel * x.d, true, rv);
   if (REL || it.slot > k) {  // adj_other(mix): other = src snapshot (REL) or relation row
-    const float* o = REL ? it.sv : it.rv;
+    const float* o = REL ? it.sv : rv;
     if (KIND == 2) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
@@ -824,8 +826,8 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
   if (KIND == 3) {  // TransE: g += c (u - own row), u = s + r
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const double x = (double)it.sv[e] + (double)it.rv[e];
-      acc[e] += it.w * (x - (double)own[e]);
+      const double u = (double)it.sv[e] + (double)rv[e];
+      acc[e] += it.w * (u - (double)own[e]);
     }
     return;
   }
@@ -836,7 +838,7 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int re = 4 * v + t, im = 4 * v + 2 + t;
-        const double sr = it.sv[re], si = it.sv[im], rr = it.rv[re], ri = it.rv[im];
+        const double sr = it.sv[re], si = it.sv[im], rr = rv[re], ri = rv[im];
         const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
         acc[re] += it.w * xr;
         acc[im] += it.w * xi;
@@ -844,8 +846,8 @@ __device__ __forceinline__ void add_loaded(const ItemRegs<4 * NV>& it, uint32_t 
   } else {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const double x = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * (double)it.rv[e];
-      acc[e] += it.w * x;
+      const double u = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * (double)rv[e];
+      acc[e] += it.w * u;
     }
   }
 }
@@ -920,10 +922,12 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     const uint32_t slotf = 2 * rowf;  // slot: theta, state
     float* ring = seg_ring + (size_t)(threadIdx.x >> 5) * kSegDepth * slotf;
     const int t0 = t;
-    auto start_of = [&](int u) { return (int)__fns(smask, 0, u + 1); };  // u-th piece start
+    // piece starts still to stage / to process, lowest bit first
+    uint32_t srest = rest;
     auto stage = [&](int u) {
       if (u < np) {
-        const int s0 = start_of(u);
+        const int s0 = __ffs(srest) - 1;
+        srest &= srest - 1;
         const uint64_t off = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, s0 & 31)) * d;
         const bool fin = finishing(u) && !gout;
         float* slot = ring + (u % kSegDepth) * slotf;
@@ -935,12 +939,14 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
 #pragma unroll
     for (int u = 0; u < kSegDepth; ++u) stage(t0 + u);
     ItemRegs<NE> cit, nit;
-    int cur = start_of(t0);
+    int cur = __ffs(rest) - 1;
+    rest &= rest - 1;
     load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
 #pragma unroll 1
     for (; t < np; ++t) {
       const bool has_next = t + 1 < np;
-      const int nxt = has_next ? start_of(t + 1) : nlive;
+      const int nxt = has_next ? __ffs(rest) - 1 : nlive;
+      rest &= rest - 1;
       const int pend = (t == np - 1 && ext_short) ? nlive + ext : nxt;
       load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, nxt & 31), has_next, nit);
       asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
@@ -951,11 +957,11 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       double acc[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-      add_loaded<KIND, NV, REL, SH>(cit, x.k, acc, th);
+      add_loaded<KIND, NV, REL, SH>(x, L, cit, x.k, acc, th);
       for (int q = cur + 1; q < pend; ++q) {
         ItemRegs<NE> it;
         load_item<KIND, NV, REL, SH>(x, L, item_val(q), true, it);
-        add_loaded<KIND, NV, REL, SH>(it, x.k, acc, th);
+        add_loaded<KIND, NV, REL, SH>(x, L, it, x.k, acc, th);
       }
       const uint32_t row = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {

@@ -106,9 +106,14 @@ def main():
         with open(os.path.join(outdir, "ncu_full_summary.json"), "w") as f:
             json.dump(full, f, indent=1)
         traffic = {}
+        def node_pass(name):  # segment_pass1_vec<KIND, NV, REL, SH>: REL == 0
+            if "<" not in name:
+                return True
+            args = [x.strip() for x in name.split("<", 1)[1].split(">")[0].split(",")]
+            return len(args) < 3 or args[2] in ("0", "(bool)0", "false")
+
         for cls, tag in (("score", "score_kernel"), ("update", "segment_pass1")):
-            hits = [e for e in full if tag in e["kernel"] and "(bool)1" not in e["kernel"]
-                    and ", 1>" not in e["kernel"]]
+            hits = [e for e in full if tag in e["kernel"] and node_pass(e["kernel"])]
             if hits:
                 b = [to_bytes(e["dram__bytes_read.sum"]) + to_bytes(e["dram__bytes_write.sum"])
                      for e in hits]
