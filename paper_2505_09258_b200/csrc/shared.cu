@@ -38,7 +38,6 @@ namespace lgd {
 
 namespace {
 
-constexpr int kThreads = 128;  // 4 warps: TMEM lanes 0..127 = tile rows
 constexpr int kNegBlk = 64;    // negatives per S block (SG1 / SG2)
 constexpr int kPosSlice = 64;  // positives per slice (SG3)
 
@@ -168,96 +167,118 @@ __device__ __forceinline__ uint32_t pool_index(const BatchArgs& a, uint32_t id) 
 }
 
 // ------------------------------------------------------------ prep kernels
-// One warp per padded tile row: IR1 (TF32) in the core-matrix layout, the
-// positive score in FP64, snap = src row, mix = -dst, the dst / src
-// contribution items and the relation key.  Padding rows are zero.
-template <int KIND>
-__global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
-  const uint64_t row = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t C = a.chunk, d = a.dim, dp = a.dpad, h = d / 2;
-  const uint64_t rows_per_chunk = (uint64_t)a.tpc * 128;
-  if (row >= a.nch * rows_per_chunk) return;
-  const uint64_t c = row / rows_per_chunk, r = row - c * rows_per_chunk;
-  const uint64_t p = c * C + r;
-  const bool valid = r < C && p < a.P;
-  unsigned char* tile = reinterpret_cast<unsigned char*>(a.sh_A) + (row >> 7) * 128ull * dp * 4;
-  unsigned char* tslice = reinterpret_cast<unsigned char*>(a.sh_AT) + (row >> 6) * 64ull * dp * 4;
-  const uint32_t rr = (uint32_t)(row & 127), rt = (uint32_t)(row & 63);
-  if (!valid) {
-    for (uint32_t i = lane; i < dp; i += 32) {
-      *reinterpret_cast<float*>(tile + cm_offset(rr, i, dp)) = 0.f;
-      *reinterpret_cast<float*>(tslice + cm_offset(i, rt, 64)) = 0.f;
+// Both run one block per 64 rows: every warp fills 8 rows of a shared-memory
+// tile, then the block writes the tile in both core-matrix layouts (the
+// K-major row block and its transpose) as consecutive 16-byte chunks.
+constexpr int kPrepRows = 64;
+
+__device__ __forceinline__ void write_core_layouts(const float* tile, uint32_t ts, uint32_t dp,
+                                                   unsigned char* rows_out,
+                                                   unsigned char* cols_out) {
+  // rows_out: 64 rows x dp (cols = dp); cols_out: dp rows x 64 (cols = 64)
+  const uint32_t chunks = 64 * dp / 4;  // 16-byte chunks per layout
+  for (uint32_t i = threadIdx.x; i < chunks; i += blockDim.x) {
+    {  // K-major over dp: chunk i = core matrix i / 8, row i % 8 of it
+      const uint32_t cmi = i >> 3, rg = cmi / (dp / 4), qc = cmi - rg * (dp / 4);
+      const uint32_t r = rg * 8 + (i & 7);
+      *reinterpret_cast<float4*>(rows_out + 16ull * i) =
+          *reinterpret_cast<const float4*>(tile + r * ts + 4 * qc);
     }
-    return;
-  }
-  const uint32_t s = a.edges[3 * p], rel = a.edges[3 * p + 1], t = a.edges[3 * p + 2];
-  const float* srow = a.theta + (size_t)s * d;
-  const float* rrow = KIND != 0 ? a.rel_theta + (size_t)rel * d : nullptr;
-  const float* drow = a.theta + (size_t)t * d;
-  double pos = 0.0;
-  for (uint32_t i = lane; i < dp; i += 32) {
-    double x = 0.0;
-    if (i < d) {
-      if (KIND == 2) {
-        const uint32_t j = i < h ? i : i - h;
-        const double sr = srow[j], si = srow[j + h], qr = rrow[j], qi = rrow[j + h];
-        x = i < h ? sr * qr - si * qi : sr * qi + si * qr;
-      } else {
-        x = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
-      }
-      const float dv = drow[i];
-      pos += x * (double)dv;
-      a.snap[p * d + i] = srow[i];
-      a.mix[p * d + i] = -(double)dv;
+    {  // transpose: rows = dims, K = the 64 rows
+      const uint32_t cmi = i >> 3, ig = cmi >> 4, qc = cmi & 15;
+      const uint32_t e = ig * 8 + (i & 7);
+      float4 v;
+      v.x = tile[(4 * qc + 0) * ts + e];
+      v.y = tile[(4 * qc + 1) * ts + e];
+      v.z = tile[(4 * qc + 2) * ts + e];
+      v.w = tile[(4 * qc + 3) * ts + e];
+      *reinterpret_cast<float4*>(cols_out + 16ull * i) = v;
     }
-    const float xt = to_tf32((float)x);
-    *reinterpret_cast<float*>(tile + cm_offset(rr, i, dp)) = xt;
-    *reinterpret_cast<float*>(tslice + cm_offset(i, rt, 64)) = xt;
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
-  if (lane == 0) {
-    a.sh_pos[p] = pos;
-    a.node_keys[2 * p] = pool_index(a, t);
-    a.node_vals[2 * p] = (uint32_t)(p << 2);  // slot 0: dst
-    a.node_keys[2 * p + 1] = pool_index(a, s);
-    a.node_vals[2 * p + 1] = (uint32_t)(p << 2) | 2u;  // slot 2: src
-    if (KIND != 0) a.rel_keys[p] = rel;
   }
 }
 
-// One warp per padded negative slot (chunk, j < kpad): the TF32 row in the
-// core-matrix layout and, for j < k, the negative's contribution item.
-__global__ void __launch_bounds__(256) shared_gather_kernel(BatchArgs a) {
-  const uint64_t slot = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t d = a.dim, dp = a.dpad, k = a.k, kp = a.kpad;
-  if (slot >= a.nch * kp) return;
-  const uint64_t c = slot / kp;
-  const uint32_t j = (uint32_t)(slot - c * kp);
-  unsigned char* blk = reinterpret_cast<unsigned char*>(a.sh_B) + (slot >> 6) * 64ull * dp * 4;
-  unsigned char* tblk = reinterpret_cast<unsigned char*>(a.sh_BT) + (slot >> 6) * 64ull * dp * 4;
-  const uint32_t rr = (uint32_t)(slot & 63);
-  if (j >= k) {
-    for (uint32_t i = lane; i < dp; i += 32) {
-      *reinterpret_cast<float*>(blk + cm_offset(rr, i, dp)) = 0.f;
-      *reinterpret_cast<float*>(tblk + cm_offset(i, rr, 64)) = 0.f;
+// IR1 (TF32) of 64 padded tile rows, the positive score in FP64, snap = the
+// src row, the dst / src contribution items and the relation key.
+template <int KIND>
+__global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
+  extern __shared__ __align__(16) float ptile[];
+  const uint32_t C = a.chunk, d = a.dim, dp = a.dpad, h = d / 2, ts = dp + 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t rows_per_chunk = (uint64_t)a.tpc * 128;
+  const uint64_t row0 = (uint64_t)blockIdx.x * kPrepRows;
+  for (int rr = warp; rr < kPrepRows; rr += 8) {
+    const uint64_t row = row0 + rr;
+    const uint64_t c = row / rows_per_chunk, r = row - c * rows_per_chunk;
+    const uint64_t p = c * C + r;
+    float* trow = ptile + rr * ts;
+    if (!(r < C && p < a.P)) {
+      for (uint32_t i = lane; i < dp; i += 32) trow[i] = 0.f;
+      continue;
     }
-    return;
+    const uint32_t s = a.edges[3 * p], rel = a.edges[3 * p + 1], t = a.edges[3 * p + 2];
+    const float* srow = a.theta + (size_t)s * d;
+    const float* rrow = KIND != 0 ? a.rel_theta + (size_t)rel * d : nullptr;
+    const float* drow = a.theta + (size_t)t * d;
+    double pos = 0.0;
+    for (uint32_t i = lane; i < dp; i += 32) {
+      double x = 0.0;
+      if (i < d) {
+        if (KIND == 2) {
+          const uint32_t j = i < h ? i : i - h;
+          const double sr = srow[j], si = srow[j + h], qr = rrow[j], qi = rrow[j + h];
+          x = i < h ? sr * qr - si * qi : sr * qi + si * qr;
+        } else {
+          x = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
+        }
+        pos += x * (double)drow[i];
+        a.snap[p * d + i] = srow[i];
+      }
+      trow[i] = to_tf32((float)x);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
+    if (lane == 0) {
+      a.sh_pos[p] = pos;
+      a.node_keys[2 * p] = pool_index(a, t);
+      a.node_vals[2 * p] = (uint32_t)(p << 2);  // slot 0: dst
+      a.node_keys[2 * p + 1] = pool_index(a, s);
+      a.node_vals[2 * p + 1] = (uint32_t)(p << 2) | 2u;  // slot 2: src
+      if (KIND != 0) a.rel_keys[p] = rel;
+    }
   }
-  const uint32_t id = a.negs[c * k + j];
-  const float* row = a.theta + (size_t)id * d;
-  for (uint32_t i = lane; i < dp; i += 32) {
-    const float v = i < d ? to_tf32(row[i]) : 0.f;
-    *reinterpret_cast<float*>(blk + cm_offset(rr, i, dp)) = v;
-    *reinterpret_cast<float*>(tblk + cm_offset(i, rr, 64)) = v;
+  __syncthreads();
+  write_core_layouts(ptile, ts, dp, reinterpret_cast<unsigned char*>(a.sh_A) + row0 * dp * 4,
+                     reinterpret_cast<unsigned char*>(a.sh_AT) + row0 * dp * 4);
+}
+
+// TF32 rows of 64 padded negative slots (chunk, j < kpad) and, for j < k,
+// the negatives' contribution items.
+__global__ void __launch_bounds__(256) shared_gather_kernel(BatchArgs a) {
+  extern __shared__ __align__(16) float ptile[];
+  const uint32_t d = a.dim, dp = a.dpad, k = a.k, kp = a.kpad, ts = dp + 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t slot0 = (uint64_t)blockIdx.x * kPrepRows;
+  for (int rr = warp; rr < kPrepRows; rr += 8) {
+    const uint64_t slot = slot0 + rr;
+    const uint64_t c = slot / kp;
+    const uint32_t j = (uint32_t)(slot - c * kp);
+    float* trow = ptile + rr * ts;
+    if (j >= k) {
+      for (uint32_t i = lane; i < dp; i += 32) trow[i] = 0.f;
+      continue;
+    }
+    const uint32_t id = a.negs[c * k + j];
+    const float* row = a.theta + (size_t)id * d;
+    for (uint32_t i = lane; i < dp; i += 32) trow[i] = i < d ? to_tf32(row[i]) : 0.f;
+    if (lane == 0) {
+      const uint64_t item = 2 * a.P + c * k + j;
+      a.node_keys[item] = pool_index(a, id);
+      a.node_vals[item] = (uint32_t)((c * kp + j) << 2) | 1u;  // slot 1: shared negative
+    }
   }
-  if (lane == 0) {
-    const uint64_t item = 2 * a.P + c * k + j;
-    a.node_keys[item] = pool_index(a, id);
-    a.node_vals[item] = (uint32_t)((c * kp + j) << 2) | 1u;  // slot 1: shared negative
-  }
+  __syncthreads();
+  write_core_layouts(ptile, ts, dp, reinterpret_cast<unsigned char*>(a.sh_B) + slot0 * dp * 4,
+                     reinterpret_cast<unsigned char*>(a.sh_BT) + slot0 * dp * 4);
 }
 
 // --------------------------------------------------------- tensor-core GEMMs
@@ -278,325 +299,501 @@ __device__ __forceinline__ TileGeom tile_geom(const BatchArgs& a, uint64_t t) {
   return g;
 }
 
+// Pipelining (all three kernels): warp specialised.  Warp 8 (lane 0) issues
+// every bulk copy and MMA; warps 0-7 are the epilogue: warp w reads TMEM lane
+// quarter w % 4 (its 32 tile rows) and column half w / 4 of each 64-column
+// block.  S lives in two TMEM buffers, so the MMA of block b + 1 runs while
+// the epilogue drains block b.  mbarriers:
+//   ld_*   bulk copy landed (complete_tx)       mma_s[2]  S MMA done (commit)
+//   epi[2] the 8 epilogue warps read S buffer    wrdy      W written (8 warps)
+//   mma_w  the W-operand MMA done (commit): W and that block's operand free
+// Phase parity of a barrier used once per block b with buffer b % 2 is
+// (b / 2) & 1; of one used once per block, b & 1.
+constexpr int kWarps = 8;                      // epilogue warps
+constexpr int kThreadsSG = (kWarps + 1) * 32;  // + the control warp
+
+// Developer timeline of one CTA (build with -DLGD_TRACE; not in the product .so)
+#ifdef LGD_TRACE
+__device__ unsigned long long g_trace[2][4096];
+#define SG_TRACE(slot)                                                                 \
+  do {                                                                                 \
+    if (blockIdx.x == 64 && (threadIdx.x == kWarps * 32 || threadIdx.x == 32) &&       \
+        (slot) < 4096)                                                                 \
+      g_trace[threadIdx.x == 32 ? 1 : 0][(slot)] = clock64();                          \
+  } while (0)
+#else
+#define SG_TRACE(slot) \
+  do {                 \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+// 32 consecutive 32-bit TMEM columns of this thread's lane, one wait
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 2^x, flush-to-zero approximation (one MUFU op; 2^-inf = +0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// round a finite non-negative float to TF32, nearest, ties away (cvt.rna)
+__device__ __forceinline__ float tf32_pos(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+constexpr float kLog2e = 1.4426950408889634f;
+// softmax weights of 32 scores, branch-free: w = 2^(s log2e - m log2e) / Z,
+// zero where !keep (bit c of keep)
+__device__ __forceinline__ void weights32(const float* v, float ml2, float zinv, uint32_t keep,
+                                          float* w) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const float e = ex2(__fmaf_rn(v[c], kLog2e, -ml2)) * zinv;
+    w[c] = (keep >> c) & 1u ? tf32_pos(e) : 0.f;
+  }
+}
+__device__ __forceinline__ uint32_t keep_mask(uint32_t j0, uint32_t limit) {
+  // bit c set iff j0 + c < limit
+  if (j0 >= limit) return 0u;
+  const uint32_t n = limit - j0;
+  return n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+}
+
+// S = A . B^T over K = dpad into TMEM columns dcol (N = n columns)
+__device__ __forceinline__ void mma_scores(uint32_t dcol, uint32_t a0, uint32_t b0, uint32_t dp,
+                                           uint32_t n) {
+  const uint32_t kcore = (dp / 4) * 128;
+  const uint32_t id = instr_desc(128, n, false, false);
+  for (uint32_t ks = 0; ks < dp / 8; ++ks)
+    mma_tf32(dcol, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore), id,
+             ks > 0);
+}
+// D (+)= W . B^T with W [128 x 64] and B^T [dpad x 64], both K-major over 64
+__device__ __forceinline__ void mma_weights(uint32_t dcol, uint32_t w0, uint32_t t0, uint32_t dp,
+                                            bool accumulate) {
+  const uint32_t id = instr_desc(128, dp, false, false);
+  for (uint32_t ks = 0; ks < 64 / 8; ++ks)
+    mma_tf32(dcol, smem_desc(w0 + ks * 256, 128, 16 * 128), smem_desc(t0 + ks * 256, 128, 16 * 128),
+             id, accumulate || ks > 0);
+}
+
+// barrier setup shared by the three kernels
+__device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint64_t* bars,
+                                         int nbars, const uint32_t* counts) {
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc(tbase_s, tcols);
+  if (threadIdx.x == kWarps * 32) {
+    for (int i = 0; i < nbars; ++i) bar_init(bars + i, counts[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
 // SG1: per tile, S = IR1 N^T in 64-negative blocks; online max / sum of exp
 // per row -> M_p, 1/Z_p and loss_p = -(pos_p - (M_p + log Z_p)) (train.cpp:274).
-__global__ void __launch_bounds__(kThreads, 1) sg1_stats_kernel(BatchArgs a) {
+__global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad;
   const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kNegBlk * dp * 4;
   unsigned char* sA = smem;
   unsigned char* sN = smem + tile_bytes;  // two blocks
-  __shared__ uint64_t bars[4];            // 0: A, 1-2: N buffers, 3: MMA
+  __shared__ uint64_t bars[7];            // 0 ld_a, 1-2 ld_n, 3-4 mma_s, 5-6 epi
   __shared__ uint32_t tbase_s;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  __shared__ float red_m[128], red_z[128];
+  uint64_t *ld_a = bars, *ld_n = bars + 1, *mma_s = bars + 3, *epi = bars + 5;
+  const uint32_t counts[7] = {1, 1, 1, 1, 1, kWarps, kWarps};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
-  if (warp == 0) tmem_alloc(&tbase_s, 64);
-  if (tid == 0) {
-    for (int i = 0; i < 4; ++i) bar_init(bars + i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  sg_setup(&tbase_s, 128, bars, 7, counts);
   const uint32_t tbase = tbase_s;
   const uint32_t nblk = kp / kNegBlk;
-  const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
-  const unsigned char* gN =
-      reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
-  if (tid == 0) {
-    bar_expect(bars, tile_bytes);
-    bulk_load(sA, gA, tile_bytes, bars);
-    for (uint32_t b = 0; b < 2 && b < nblk; ++b) {
-      bar_expect(bars + 1 + b, blk_bytes);
-      bulk_load(sN + b * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes, bars + 1 + b);
+  const int q = warp & 3, hf = warp >> 2;
+  const uint32_t row = q * 32 + lane;
+  float m = -INFINITY, z = 0.f;  // running max and sum of 2^((s - m) log2e)
+  if (warp == kWarps) {          // control
+    if (lane == 0) {
+      const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
+      const unsigned char* gN =
+          reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
+      auto load_n = [&](uint32_t b) {
+        bar_expect(ld_n + (b & 1), blk_bytes);
+        bulk_load(sN + (b & 1) * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes,
+                  ld_n + (b & 1));
+      };
+      auto issue_s = [&](uint32_t b) {
+        bar_wait(ld_n + (b & 1), (b >> 1) & 1);
+        if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
+        tc_fence_after();
+        mma_scores(tbase + (b & 1) * 64, saddr(sA), saddr(sN + (b & 1) * blk_bytes), dp, kNegBlk);
+        mma_commit(mma_s + (b & 1));
+      };
+      bar_expect(ld_a, tile_bytes);
+      bulk_load(sA, gA, tile_bytes, ld_a);
+      for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_n(b);
+      bar_wait(ld_a, 0);
+      issue_s(0);
+      for (uint32_t b = 0; b < nblk; ++b) {
+        if (b + 1 < nblk) issue_s(b + 1);
+        bar_wait(mma_s + (b & 1), (b >> 1) & 1);
+        if (b + 2 < nblk) load_n(b + 2);
+      }
     }
-  }
-  const uint32_t idesc = instr_desc(128, kNegBlk, false, false);
-  const uint32_t kcore = (dp / 4) * 128;  // SBO: next 8-row group
-  float m = -INFINITY, z = 0.f;
-  const uint32_t row = tid;
-  for (uint32_t nb = 0; nb < nblk; ++nb) {
-    const uint32_t buf = nb & 1;
-    if (tid == 0) {
-      if (nb == 0) bar_wait(bars, 0);
-      bar_wait(bars + 1 + buf, (nb >> 1) & 1);
+  } else {  // epilogue
+    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + hf * 32;
+    for (uint32_t nb = 0; nb < nblk; ++nb) {
+      bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
       tc_fence_after();
-      const uint32_t a0 = saddr(sA), b0 = saddr(sN + buf * blk_bytes);
-      for (uint32_t ks = 0; ks < dp / 8; ++ks)
-        mma_tf32(tbase, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore),
-                 idesc, ks > 0);
-      mma_commit(bars + 3);
+      float v[32];
+      tmem_ld32(lane_addr + (nb & 1) * 64, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(epi + (nb & 1));
+      const uint32_t keep = keep_mask(nb * kNegBlk + hf * 32, k);
+      float bm = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) bm = fmaxf(bm, (keep >> c) & 1u ? v[c] : -INFINITY);
+      const float mn = fmaxf(m, bm);
+      const float ml2 = mn * kLog2e;
+      float zs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        zs += (keep >> c) & 1u ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+      z = (m == -INFINITY ? 0.f : z * ex2((m - mn) * kLog2e)) + zs;
+      m = mn;
     }
-    bar_wait(bars + 3, nb & 1);
-    tc_fence_after();
-    if (tid == 0 && nb + 2 < nblk) {  // the MMA is done with this buffer
-      bar_expect(bars + 1 + buf, blk_bytes);
-      bulk_load(sN + buf * blk_bytes, gN + (uint64_t)(nb + 2) * blk_bytes, blk_bytes,
-                bars + 1 + buf);
+    if (hf == 1) {
+      red_m[row] = m;
+      red_z[row] = z;
     }
-    float v[kNegBlk];
-    const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-#pragma unroll
-    for (int q = 0; q < kNegBlk; q += 16) tmem_ld16(lane_addr + q, v + q);
-    float bm = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < kNegBlk; ++q)
-      if (nb * kNegBlk + q < k) bm = fmaxf(bm, v[q]);
-    const float mn = fmaxf(m, bm);
-    float zs = 0.f;
-#pragma unroll
-    for (int q = 0; q < kNegBlk; ++q)
-      if (nb * kNegBlk + q < k) zs += __expf(v[q] - mn);
-    z = (m == -INFINITY ? 0.f : z * __expf(m - mn)) + zs;
-    m = mn;
-    tc_fence_before();
-    __syncthreads();
   }
-  if (row < g.valid) {
+  __syncthreads();
+  if (warp < 4 && row < g.valid) {  // combine the two column halves of each row
+    const float m1 = red_m[row], z1 = red_z[row];
+    const float M = fmaxf(m, m1);
+    const float Z = (m == -INFINITY ? 0.f : z * ex2((m - M) * kLog2e)) +
+                    (m1 == -INFINITY ? 0.f : z1 * ex2((m1 - M) * kLog2e));
     const uint64_t tr = g.row0 + row;
-    a.sh_rowmax[tr] = m;
-    a.sh_rowinv[tr] = 1.f / z;
+    a.sh_rowmax[tr] = M;
+    a.sh_rowinv[tr] = 1.f / Z;
     const uint64_t p = g.c * a.chunk + (tr - g.c * (uint64_t)a.tpc * 128);
-    a.loss[p] = -(a.sh_pos[p] - ((double)m + log((double)z)));
+    a.loss[p] = -(a.sh_pos[p] - ((double)M + log((double)Z)));
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_free(tbase, 64);
+  if (warp == 0) tmem_free(tbase, 128);
 }
 
-// SG2: per tile, mix += W N with W = exp(S - M) / Z recomputed block by block.
-// TMEM: mix accumulator in columns [0, dpad), S in [scol, scol + 64).
-__global__ void __launch_bounds__(kThreads, 1) sg2_mix_kernel(BatchArgs a, uint32_t tcols,
-                                                              uint32_t scol) {
+// SG2: per tile, mix = W N - dst with W = exp(S - M) / Z recomputed block by
+// block.  TMEM: mix in columns [0, dpad), S buffers at scol and scol + 64.
+// smem: IR1 tile, N blocks x2 (S operand), N^T blocks x2 (mix operand), W.
+__global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uint32_t tcols,
+                                                                uint32_t scol) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad, d = a.dim;
   const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kNegBlk * dp * 4;
   unsigned char* sA = smem;
-  unsigned char* sN = smem + tile_bytes;            // two blocks: N (64 x dpad) then N^T
-  unsigned char* sW = sN + 4 * blk_bytes;           // 128 x 64 f32, core-matrix layout
-  __shared__ uint64_t bars[5];  // 0: A, 1-2: N buffers, 3: S MMA, 4: mix MMA
+  unsigned char* sN = sA + tile_bytes;       // 2 x N block
+  unsigned char* sT = sN + 2 * blk_bytes;    // 2 x N^T block
+  unsigned char* sW = sT + 2 * blk_bytes;    // 128 x 64
+  // 0 ld_a, 1-2 ld_n, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
+  __shared__ uint64_t bars[11];
   __shared__ uint32_t tbase_s;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  uint64_t *ld_a = bars, *ld_n = bars + 1, *ld_t = bars + 3, *mma_s = bars + 5, *epi = bars + 7,
+           *wrdy = bars + 9, *mma_w = bars + 10;
+  const uint32_t counts[11] = {1, 1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
-  if (warp == 0) tmem_alloc(&tbase_s, tcols);
-  if (tid == 0) {
-    for (int i = 0; i < 5; ++i) bar_init(bars + i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  sg_setup(&tbase_s, tcols, bars, 11, counts);
+  const uint32_t tbase = tbase_s;
+  const uint32_t nblk = kp / kNegBlk;
+  const int q = warp & 3, hf = warp >> 2;
+  const uint32_t row = q * 32 + lane;
+  const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
+  if (warp == kWarps) {  // control
+    if (lane == 0) {
+      const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
+      const unsigned char* gN =
+          reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
+      const unsigned char* gT =
+          reinterpret_cast<const unsigned char*>(a.sh_BT) + g.c * (uint64_t)kp * dp * 4;
+      auto load_n = [&](uint32_t b) {
+        bar_expect(ld_n + (b & 1), blk_bytes);
+        bulk_load(sN + (b & 1) * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes,
+                  ld_n + (b & 1));
+      };
+      auto load_t = [&](uint32_t b) {
+        bar_expect(ld_t + (b & 1), blk_bytes);
+        bulk_load(sT + (b & 1) * blk_bytes, gT + (uint64_t)b * blk_bytes, blk_bytes,
+                  ld_t + (b & 1));
+      };
+      auto issue_s = [&](uint32_t b) {
+        bar_wait(ld_n + (b & 1), (b >> 1) & 1);
+        if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
+        tc_fence_after();
+        mma_scores(tbase + scol + (b & 1) * 64, saddr(sA), saddr(sN + (b & 1) * blk_bytes), dp,
+                   kNegBlk);
+        mma_commit(mma_s + (b & 1));
+      };
+      bar_expect(ld_a, tile_bytes);
+      bulk_load(sA, gA, tile_bytes, ld_a);
+      for (uint32_t b = 0; b < 2 && b < nblk; ++b) {
+        load_n(b);
+        load_t(b);
+      }
+      bar_wait(ld_a, 0);
+      issue_s(0);
+      for (uint32_t b = 0; b < nblk; ++b) {
+        SG_TRACE(b * 8 + 0);
+        if (b + 1 < nblk) issue_s(b + 1);
+        SG_TRACE(b * 8 + 1);
+        bar_wait(mma_s + (b & 1), (b >> 1) & 1);
+        if (b + 2 < nblk) load_n(b + 2);
+        bar_wait(wrdy, b & 1);  // the epilogue wrote W(b)
+        SG_TRACE(b * 8 + 2);
+        bar_wait(ld_t + (b & 1), (b >> 1) & 1);
+        tc_fence_after();
+        mma_weights(tbase, saddr(sW), saddr(sT + (b & 1) * blk_bytes), dp, b > 0);
+        mma_commit(mma_w);
+        SG_TRACE(b * 8 + 3);
+        bar_wait(mma_w, b & 1);
+        SG_TRACE(b * 8 + 4);
+        if (b + 2 < nblk) load_t(b + 2);
+      }
+    }
+  } else {  // epilogue
+    const bool valid = row < g.valid;
+    const float rm2 = valid ? a.sh_rowmax[g.row0 + row] * kLog2e : 0.f;
+    const float ri = valid ? a.sh_rowinv[g.row0 + row] : 0.f;
+    for (uint32_t nb = 0; nb < nblk; ++nb) {
+      SG_TRACE(nb * 8 + 0);
+      bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
+      tc_fence_after();
+      SG_TRACE(nb * 8 + 1);
+      float v[32];
+      tmem_ld32(lane_addr + scol + (nb & 1) * 64 + hf * 32, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(epi + (nb & 1));
+      float w[32];
+      weights32(v, rm2, ri, valid ? keep_mask(nb * kNegBlk + hf * 32, k) : 0u, w);
+      SG_TRACE(nb * 8 + 2);
+      if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W free again
+      SG_TRACE(nb * 8 + 3);
+#pragma unroll
+      for (int c = 0; c < 32; c += 4)
+        *reinterpret_cast<float4*>(sW + cm_offset(row, hf * 32 + c, kNegBlk)) =
+            make_float4(w[c], w[c + 1], w[c + 2], w[c + 3]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) bar_arrive(wrdy);
+      SG_TRACE(nb * 8 + 4);
+    }
+  }
+  __syncthreads();
+  bar_wait(mma_w, (nblk - 1) & 1);
+  tc_fence_after();
+  float* out = reinterpret_cast<float*>(sA);  // the IR1 tile is free now
+  const uint32_t ts = dp + 4;
+  if (warp < kWarps) {  // TMEM -> shared tile
+    const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
+    for (uint32_t cc = c0; cc < c1; cc += 16) {
+      float v[16];
+      tmem_ld16(lane_addr + cc, v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) out[row * ts + cc + e] = v[e];
+    }
   }
   tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tbase_s;
-  const uint32_t nblk = kp / kNegBlk;
-  const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
-  const unsigned char* gN =
-      reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
-  const unsigned char* gNT =
-      reinterpret_cast<const unsigned char*>(a.sh_BT) + g.c * (uint64_t)kp * dp * 4;
-  // buffer b: N block at sN + 2b blk, N^T block right after it
-  auto load_blk = [&](uint32_t nb, uint32_t b) {
-    bar_expect(bars + 1 + b, 2 * blk_bytes);
-    bulk_load(sN + 2 * b * blk_bytes, gN + (uint64_t)nb * blk_bytes, blk_bytes, bars + 1 + b);
-    bulk_load(sN + (2 * b + 1) * blk_bytes, gNT + (uint64_t)nb * blk_bytes, blk_bytes,
-              bars + 1 + b);
-  };
-  if (tid == 0) {
-    bar_expect(bars, tile_bytes);
-    bulk_load(sA, gA, tile_bytes, bars);
-    for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_blk(b, b);
-  }
-  const uint32_t row = tid;
-  const bool valid = row < g.valid;
-  const float rm = valid ? a.sh_rowmax[g.row0 + row] : 0.f;
-  const float ri = valid ? a.sh_rowinv[g.row0 + row] : 0.f;
-  const uint32_t kcore = (dp / 4) * 128;
-  const uint32_t id_s = instr_desc(128, kNegBlk, false, false);
-  const uint32_t id_m = instr_desc(128, dp, false, false);
-  const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-  for (uint32_t nb = 0; nb < nblk; ++nb) {
-    const uint32_t buf = nb & 1;
-    if (tid == 0) {
-      if (nb == 0) bar_wait(bars, 0);
-      if (nb >= 1) {  // mix MMA of block nb-1 done: its N buffer is free
-        bar_wait(bars + 4, (nb - 1) & 1);
-        if (nb + 1 < nblk) load_blk(nb + 1, (nb + 1) & 1);
+  if (warp < kWarps) {
+    // mix = sum_j w_j n_j - dst (train.cpp:306-323), coalesced; warp w writes
+    // rows w, w + 8, ...: dst ids lane-parallel, four rows' dst in flight
+    const uint64_t pbase = g.c * a.chunk + (g.row0 - g.c * (uint64_t)a.tpc * 128);
+    uint32_t myid = 0;
+    if (lane < 128 / kWarps && warp + kWarps * lane < g.valid)
+      myid = a.edges[3 * (pbase + warp + kWarps * lane) + 2];
+    for (uint32_t rb = 0; rb < 128 / kWarps; rb += 4) {
+      float dv[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t r = warp + kWarps * (rb + i);
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, rb + i);
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const uint32_t e = lane + 32 * e4;
+          dv[i][e4] = (r < g.valid && e < d) ? __ldg(a.theta + (size_t)id * d + e) : 0.f;
+        }
       }
-      bar_wait(bars + 1 + buf, (nb >> 1) & 1);
-      tc_fence_after();
-      const uint32_t a0 = saddr(sA), b0 = saddr(sN + 2 * buf * blk_bytes);
-      for (uint32_t ks = 0; ks < dp / 8; ++ks)
-        mma_tf32(tbase + scol, smem_desc(a0 + ks * 256, 128, kcore),
-                 smem_desc(b0 + ks * 256, 128, kcore), id_s, ks > 0);
-      mma_commit(bars + 3);
-    }
-    bar_wait(bars + 3, nb & 1);
-    tc_fence_after();
-    float v[kNegBlk];
 #pragma unroll
-    for (int q = 0; q < kNegBlk; q += 16) tmem_ld16(lane_addr + scol + q, v + q);
-    if (nb >= 1) bar_wait(bars + 4, (nb - 1) & 1);  // W buffer free again
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t r = warp + kWarps * (rb + i);
+        if (r >= g.valid) continue;
+        double* mx = a.mix + (pbase + r) * d;
 #pragma unroll
-    for (int q = 0; q < kNegBlk; q += 4) {
-      float4 w;
-      const uint32_t j = nb * kNegBlk + q;
-      w.x = (valid && j + 0 < k) ? __expf(v[q + 0] - rm) * ri : 0.f;
-      w.y = (valid && j + 1 < k) ? __expf(v[q + 1] - rm) * ri : 0.f;
-      w.z = (valid && j + 2 < k) ? __expf(v[q + 2] - rm) * ri : 0.f;
-      w.w = (valid && j + 3 < k) ? __expf(v[q + 3] - rm) * ri : 0.f;
-      w.x = to_tf32(w.x), w.y = to_tf32(w.y), w.z = to_tf32(w.z), w.w = to_tf32(w.w);
-      *reinterpret_cast<float4*>(sW + cm_offset(row, q, kNegBlk)) = w;
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t w0 = saddr(sW), t0 = saddr(sN + (2 * buf + 1) * blk_bytes);
-      // A = W (128 x 64 negatives), B = N^T (dpad x 64 negatives), both K-major
-      for (uint32_t ks = 0; ks < kNegBlk / 8; ++ks)
-        mma_tf32(tbase, smem_desc(w0 + ks * 256, 128, (kNegBlk / 4) * 128),
-                 smem_desc(t0 + ks * 256, 128, (kNegBlk / 4) * 128), id_m, (nb | ks) != 0);
-      mma_commit(bars + 4);
-    }
-  }
-  bar_wait(bars + 4, (nblk - 1) & 1);
-  tc_fence_after();
-  {
-    const uint64_t tr = g.row0 + row;
-    const uint64_t p = g.c * a.chunk + (tr - g.c * (uint64_t)a.tpc * 128);
-    double* mx = a.mix + p * d;
-    for (uint32_t q = 0; q < dp; q += 16) {  // collective loads: every lane, every step
-      float v[16];
-      tmem_ld16(lane_addr + q, v);
-      if (valid) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (q + e < d) mx[q + e] += (double)v[e];
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const uint32_t e = lane + 32 * e4;
+          if (e < d) mx[e] = (double)out[r * ts + e] - (double)dv[i][e4];
+        }
       }
     }
   }
-  tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_free(tbase, tcols);
 }
 
 // SG3: per (chunk, 128 negatives): G = W^T IR1 over the chunk's positives in
 // 64-positive slices; S^T = N IR1^T is recomputed per slice (M = the 128
-// negatives, N = 64 positives).  TMEM: G in [0, dpad), S^T in [scol, +64).
-__global__ void __launch_bounds__(kThreads, 1) sg3_grad_kernel(BatchArgs a, uint32_t tcols,
-                                                               uint32_t scol) {
+// negatives, N = 64 positives).  TMEM: G in [0, dpad), S^T at scol, scol + 64.
+// smem: N block (128 x dpad), IR1 slices x2 (S operand), IR1^T slices x2
+// (G operand), W^T.
+__global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, uint32_t tcols,
+                                                                 uint32_t scol) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad, d = a.dim;
   const uint32_t nblk_bytes = 128 * dp * 4, sl_bytes = kPosSlice * dp * 4;
-  unsigned char* sN = smem;                 // 128 negatives x dpad
-  unsigned char* sA = smem + nblk_bytes;    // two buffers: IR1 slice (64 x dpad), then IR1^T
-  unsigned char* sW = sA + 4 * sl_bytes;    // W^T: 128 negatives x 64 positives
-  __shared__ uint64_t bars[5];  // 0: N, 1-2: slices, 3: S MMA, 4: G MMA
+  unsigned char* sN = smem;
+  unsigned char* sA = sN + nblk_bytes;     // 2 x IR1 slice
+  unsigned char* sT = sA + 2 * sl_bytes;   // 2 x IR1^T slice
+  unsigned char* sW = sT + 2 * sl_bytes;   // 128 x 64
+  // 0 ld_n, 1-2 ld_a, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
+  __shared__ uint64_t bars[11];
   __shared__ uint32_t tbase_s;
-  __shared__ float s_m[kPosSlice], s_i[kPosSlice];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t nbpc = kp / 128;  // negative blocks per chunk
+  uint64_t *ld_n = bars, *ld_a = bars + 1, *ld_t = bars + 3, *mma_s = bars + 5, *epi = bars + 7,
+           *wrdy = bars + 9, *mma_w = bars + 10;
+  const uint32_t counts[11] = {1, 1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, hf = warp >> 2;
+  const uint32_t row = q * 32 + lane;  // negative n0 + row
+  const uint32_t nbpc = kp / 128;
   const uint64_t c = blockIdx.x / nbpc;
   const uint32_t n0 = (blockIdx.x - c * nbpc) * 128;
   const uint64_t left = a.P - c * a.chunk;
   const uint64_t chunk_rows = left < a.chunk ? left : a.chunk;
   const uint32_t nsl = (uint32_t)((chunk_rows + kPosSlice - 1) / kPosSlice);
-  if (warp == 0) tmem_alloc(&tbase_s, tcols);
-  if (tid == 0) {
-    for (int i = 0; i < 5; ++i) bar_init(bars + i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint64_t crow0 = c * (uint64_t)a.tpc * 128;
+  sg_setup(&tbase_s, tcols, bars, 11, counts);
+  const uint32_t tbase = tbase_s;
+  const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
+  if (warp == kWarps) {  // control
+    if (lane == 0) {
+      const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + crow0 * dp * 4;
+      const unsigned char* gT = reinterpret_cast<const unsigned char*>(a.sh_AT) + crow0 * dp * 4;
+      const unsigned char* gN =
+          reinterpret_cast<const unsigned char*>(a.sh_B) + (c * (uint64_t)kp + n0) * dp * 4;
+      auto load_a = [&](uint32_t s) {
+        bar_expect(ld_a + (s & 1), sl_bytes);
+        bulk_load(sA + (s & 1) * sl_bytes, gA + (uint64_t)s * sl_bytes, sl_bytes, ld_a + (s & 1));
+      };
+      auto load_t = [&](uint32_t s) {
+        bar_expect(ld_t + (s & 1), sl_bytes);
+        bulk_load(sT + (s & 1) * sl_bytes, gT + (uint64_t)s * sl_bytes, sl_bytes, ld_t + (s & 1));
+      };
+      auto issue_s = [&](uint32_t s) {
+        bar_wait(ld_a + (s & 1), (s >> 1) & 1);
+        if (s >= 2) bar_wait(epi + (s & 1), ((s - 2) >> 1) & 1);
+        tc_fence_after();
+        mma_scores(tbase + scol + (s & 1) * 64, saddr(sN), saddr(sA + (s & 1) * sl_bytes), dp,
+                   kPosSlice);
+        mma_commit(mma_s + (s & 1));
+      };
+      bar_expect(ld_n, nblk_bytes);
+      bulk_load(sN, gN, nblk_bytes, ld_n);
+      for (uint32_t s = 0; s < 2 && s < nsl; ++s) {
+        load_a(s);
+        load_t(s);
+      }
+      bar_wait(ld_n, 0);
+      issue_s(0);
+      for (uint32_t s = 0; s < nsl; ++s) {
+        if (s + 1 < nsl) issue_s(s + 1);
+        bar_wait(mma_s + (s & 1), (s >> 1) & 1);
+        if (s + 2 < nsl) load_a(s + 2);
+        bar_wait(wrdy, s & 1);
+        bar_wait(ld_t + (s & 1), (s >> 1) & 1);
+        tc_fence_after();
+        mma_weights(tbase, saddr(sW), saddr(sT + (s & 1) * sl_bytes), dp, s > 0);
+        mma_commit(mma_w);
+        bar_wait(mma_w, s & 1);
+        if (s + 2 < nsl) load_t(s + 2);
+      }
+    }
+  } else {  // epilogue: row = negative, columns = the slice's positives
+    const bool nvalid = n0 + row < k;
+    for (uint32_t s = 0; s < nsl; ++s) {
+      // statistics of this half's 32 positives: lane i holds positive i
+      const uint64_t pq = (uint64_t)s * kPosSlice + hf * 32 + lane;
+      const bool pv = pq < chunk_rows;
+      const float my_m2 = pv ? a.sh_rowmax[crow0 + pq] * kLog2e : 0.f;
+      const float my_i = pv ? a.sh_rowinv[crow0 + pq] : 0.f;
+      const uint32_t pmask = __ballot_sync(0xffffffffu, pv);  // every lane: no divergent vote
+      const uint32_t keep = nvalid ? pmask : 0u;
+      bar_wait(mma_s + (s & 1), (s >> 1) & 1);
+      tc_fence_after();
+      float v[32];
+      tmem_ld32(lane_addr + scol + (s & 1) * 64 + hf * 32, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(epi + (s & 1));
+      float w[32];
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const float m2 = __shfl_sync(0xffffffffu, my_m2, cc);
+        const float zi = __shfl_sync(0xffffffffu, my_i, cc);
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -m2)) * zi;
+        w[cc] = (keep >> cc) & 1u ? tf32_pos(e) : 0.f;
+      }
+      if (s >= 1) bar_wait(mma_w, (s - 1) & 1);
+#pragma unroll
+      for (int cc = 0; cc < 32; cc += 4)
+        *reinterpret_cast<float4*>(sW + cm_offset(row, hf * 32 + cc, kPosSlice)) =
+            make_float4(w[cc], w[cc + 1], w[cc + 2], w[cc + 3]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) bar_arrive(wrdy);
+    }
+  }
+  __syncthreads();
+  bar_wait(mma_w, (nsl - 1) & 1);
+  tc_fence_after();
+  float* out = reinterpret_cast<float*>(sN);  // the negative block is free now
+  const uint32_t ts = dp + 4;
+  if (warp < kWarps) {
+    const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
+    for (uint32_t cc = c0; cc < c1; cc += 16) {
+      float v[16];
+      tmem_ld16(lane_addr + cc, v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) out[row * ts + cc + e] = v[e];
+    }
   }
   tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tbase_s;
-  const uint64_t crow0 = c * (uint64_t)a.tpc * 128;  // the chunk's first padded row
-  const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + crow0 * dp * 4;
-  const unsigned char* gAT = reinterpret_cast<const unsigned char*>(a.sh_AT) + crow0 * dp * 4;
-  const unsigned char* gN =
-      reinterpret_cast<const unsigned char*>(a.sh_B) + (c * (uint64_t)kp + n0) * dp * 4;
-  auto load_slice = [&](uint32_t s, uint32_t b) {
-    bar_expect(bars + 1 + b, 2 * sl_bytes);
-    bulk_load(sA + 2 * b * sl_bytes, gA + (uint64_t)s * sl_bytes, sl_bytes, bars + 1 + b);
-    bulk_load(sA + (2 * b + 1) * sl_bytes, gAT + (uint64_t)s * sl_bytes, sl_bytes, bars + 1 + b);
-  };
-  if (tid == 0) {
-    bar_expect(bars, nblk_bytes);
-    bulk_load(sN, gN, nblk_bytes, bars);
-    for (uint32_t s = 0; s < 2 && s < nsl; ++s) load_slice(s, s);
-  }
-  const uint32_t row = tid;  // negative n0 + row
-  const bool nvalid = n0 + row < k;
-  const uint32_t kcore = (dp / 4) * 128;
-  const uint32_t id_s = instr_desc(128, kPosSlice, false, false);
-  const uint32_t id_g = instr_desc(128, dp, false, false);
-  const uint32_t lane_addr = tbase + ((uint32_t)(warp * 32) << 16);
-  for (uint32_t s = 0; s < nsl; ++s) {
-    const uint32_t buf = s & 1;
-    if (tid < kPosSlice) {  // row statistics of this slice's positives
-      const uint64_t q = (uint64_t)s * kPosSlice + tid;
-      s_m[tid] = q < chunk_rows ? a.sh_rowmax[crow0 + q] : 0.f;
-      s_i[tid] = q < chunk_rows ? a.sh_rowinv[crow0 + q] : 0.f;
-    }
-    if (tid == 0) {
-      if (s == 0) bar_wait(bars, 0);
-      if (s >= 1) {
-        bar_wait(bars + 4, (s - 1) & 1);
-        if (s + 1 < nsl) load_slice(s + 1, (s + 1) & 1);
-      }
-      bar_wait(bars + 1 + buf, (s >> 1) & 1);
-      tc_fence_after();
-      const uint32_t a0 = saddr(sN), b0 = saddr(sA + 2 * buf * sl_bytes);
-      for (uint32_t ks = 0; ks < dp / 8; ++ks)
-        mma_tf32(tbase + scol, smem_desc(a0 + ks * 256, 128, kcore),
-                 smem_desc(b0 + ks * 256, 128, kcore), id_s, ks > 0);
-      mma_commit(bars + 3);
-    }
-    bar_wait(bars + 3, s & 1);
-    tc_fence_after();
-    __syncthreads();  // s_m / s_i visible
-    float v[kPosSlice];
-#pragma unroll
-    for (int q = 0; q < kPosSlice; q += 16) tmem_ld16(lane_addr + scol + q, v + q);
-    if (s >= 1) bar_wait(bars + 4, (s - 1) & 1);
-#pragma unroll
-    for (int q = 0; q < kPosSlice; q += 4) {
-      float w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint64_t pq = (uint64_t)s * kPosSlice + q + e;
-        w[e] = (nvalid && pq < chunk_rows) ? to_tf32(__expf(v[q + e] - s_m[q + e]) * s_i[q + e])
-                                           : 0.f;
-      }
-      *reinterpret_cast<float4*>(sW + cm_offset(row, q, kPosSlice)) =
-          make_float4(w[0], w[1], w[2], w[3]);
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t w0 = saddr(sW), t0 = saddr(sA + (2 * buf + 1) * sl_bytes);
-      // A = W^T (128 negatives x 64 positives), B = IR1^T (dpad x 64 positives)
-      for (uint32_t ks = 0; ks < kPosSlice / 8; ++ks)
-        mma_tf32(tbase, smem_desc(w0 + ks * 256, 128, (kPosSlice / 4) * 128),
-                 smem_desc(t0 + ks * 256, 128, (kPosSlice / 4) * 128), id_g, (s | ks) != 0);
-      mma_commit(bars + 4);
+  if (warp < kWarps) {  // G rows, coalesced
+    const uint32_t nrows = k > n0 ? (k - n0 < 128 ? k - n0 : 128) : 0;
+    for (uint32_t r = warp; r < nrows; r += kWarps) {
+      float* gout = a.sh_G + (c * (uint64_t)kp + n0 + r) * d;
+      for (uint32_t e = lane; e < d; e += 32) gout[e] = out[r * ts + e];
     }
   }
-  bar_wait(bars + 4, (nsl - 1) & 1);
-  tc_fence_after();
-  float* gout = a.sh_G + (c * (uint64_t)kp + n0 + row) * d;
-  for (uint32_t q = 0; q < dp; q += 16) {
-    float v[16];
-    tmem_ld16(lane_addr + q, v);
-    if (nvalid) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (q + e < d) gout[q + e] = v[e];
-    }
-  }
-  tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_free(tbase, tcols);
 }
@@ -613,6 +810,12 @@ void set_smem(K kernel, size_t bytes) {
 }
 
 }  // namespace
+
+#ifdef LGD_TRACE
+extern "C" int lgd_debug_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P) {
   SharedShape s{};
@@ -632,21 +835,22 @@ size_t shared_smem_bytes(uint32_t dpad) {
 
 void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   const uint64_t rows = a.nch * (uint64_t)a.tpc * 128;
+  const uint32_t dp = a.dpad;
+  const size_t psm = (size_t)kPrepRows * (dp + 4) * 4;
   switch (a.kind) {
     case 0:
-      shared_prep_kernel<0><<<ceil_div(rows * 32, 256), 256, 0, st>>>(a);
+      shared_prep_kernel<0><<<(unsigned)(rows / kPrepRows), 256, psm, st>>>(a);
       break;
     case 1:
-      shared_prep_kernel<1><<<ceil_div(rows * 32, 256), 256, 0, st>>>(a);
+      shared_prep_kernel<1><<<(unsigned)(rows / kPrepRows), 256, psm, st>>>(a);
       break;
     default:
-      shared_prep_kernel<2><<<ceil_div(rows * 32, 256), 256, 0, st>>>(a);
+      shared_prep_kernel<2><<<(unsigned)(rows / kPrepRows), 256, psm, st>>>(a);
       break;
   }
   LGD_LAUNCH_CHECK();
-  shared_gather_kernel<<<ceil_div(a.nch * (uint64_t)a.kpad * 32, 256), 256, 0, st>>>(a);
+  shared_gather_kernel<<<(unsigned)(a.nch * (uint64_t)a.kpad / kPrepRows), 256, psm, st>>>(a);
   LGD_LAUNCH_CHECK();
-  const uint32_t dp = a.dpad;
   const size_t t = 128ull * dp * 4, b = (size_t)kNegBlk * dp * 4;
   const size_t sm1 = t + 2 * b;
   const size_t sm2 = t + 4 * b + 128 * kNegBlk * 4;
@@ -657,12 +861,12 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   if (sm3 > set3) set_smem(sg3_grad_kernel, set3 = sm3);
   const unsigned tiles = (unsigned)(a.nch * a.tpc);
   const uint32_t scol = (dp + 31) & ~31u;
-  const uint32_t tcols = pow2_cols(scol + 64);
-  sg1_stats_kernel<<<tiles, kThreads, sm1, st>>>(a);
+  const uint32_t tcols = pow2_cols(scol + 128);  // G / mix, then two S buffers
+  sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);
   LGD_LAUNCH_CHECK();
-  sg2_mix_kernel<<<tiles, kThreads, sm2, st>>>(a, tcols, scol);
+  sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, scol);
   LGD_LAUNCH_CHECK();
-  sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreads, sm3, st>>>(a, tcols, scol);
+  sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, scol);
   LGD_LAUNCH_CHECK();
 }
 

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblegend_b200.so")
+LIB_PATH = os.environ.get("LGD_LIBRARY") or os.path.join(_HERE, "liblegend_b200.so")
 
 MODELS = {"dot": 0, "distmult": 1, "complex": 2, "transe": 3}
 NO_RELATION = 0xFFFFFFFF
