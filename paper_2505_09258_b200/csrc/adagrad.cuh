@@ -1,0 +1,97 @@
+// adagrad.cuh -- the reference's FP64 Adagrad element update (train.cpp:342-354)
+//
+//   a = double(S) + g * g;   S' = float(a);
+//   theta' = float(double(theta) - lr * g / (sqrt(a) + eps))
+//
+// bit-identical, with a fast path.  The exact form needs IEEE double sqrt and
+// division (~50 instructions per element with CUDA's inline sequences and
+// their slow-path branches).  The fast path computes q = lr g / (sqrt(a) +
+// eps) to ~2^-50 relative from FP64 MUFU seeds and two Newton steps each,
+// then t = theta - q and f = float(t).  float(t_exact) == f is guaranteed when
+// t lies farther than the error bound from the f32 rounding midpoints around
+// f; otherwise (and for zero / non-normal operands) the caller redoes the
+// element with the exact form.  Both forms take the products, sums and
+// conversions in the reference's order, so the result is the reference's to
+// the bit either way.
+#pragma once
+
+#include <cstdint>
+
+namespace lgd {
+
+// FP64 MUFU seeds (~2^-22 relative): no f32 <-> f64 conversions, which share
+// the MIO path with shared-memory traffic
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// The exact reference update (CUDA's correctly rounded sqrt and division).
+__device__ __forceinline__ void adagrad_exact(double g, float& th, float& st, double lr,
+                                              double eps) {
+  const double a2 = (double)st + g * g;
+  st = (float)a2;
+  th = (float)((double)th - lr * g / (sqrt(a2) + eps));
+}
+
+// Fast path: returns false when the element must be redone exactly (th and st
+// are left untouched then).
+__device__ __forceinline__ bool adagrad_try_fast(double g, float& th, float& st, double lr,
+                                                 double eps) {
+  const double a2 = (double)st + g * g;
+  const float af = (float)a2;
+  const double num = lr * g;
+  const double t0 = (double)th;
+  if (num == 0.0) {  // q = +-0 exactly: theta - q needs no division
+    st = af;
+    th = (float)(t0 - num);
+    return true;
+  }
+  // a2 within the normal float range (the MUFU seeds flush denormals)
+  const uint32_t ab = __float_as_uint(af);
+  bool ok = ((ab >> 23) & 0xffu) - 1u < 0xfeu;
+  // sqrt(a2): s = a2 * rsqrt(a2) from a ~2^-20 seed, two Newton (Heron)
+  // steps: the error squares each time, so only the roundings of the last
+  // steps remain (< 2^-50 relative)
+  const double y = rsqrt_approx(a2);
+  const double h = 0.5 * y;
+  const double s = a2 * y;
+  const double s1 = __fma_rn(h, __fma_rn(-s, s, a2), s);
+  const double s2 = __fma_rn(h, __fma_rn(-s1, s1, a2), s1);
+  const double den = s2 + eps;
+  // 1 / den: ~2^-20 seed, two Newton steps (< 2^-50 relative)
+  const double r = rcp_approx(den);
+  const double r1 = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
+  const double r2 = __fma_rn(r1, __fma_rn(-den, r1, 1.0), r1);
+  const double q = num * r2;
+  const double t = t0 - q;
+  const float f = (float)t;
+  // distance of t from the f32 rounding midpoints around f
+  const uint32_t fb = __float_as_uint(f);
+  const uint32_t fe = (fb >> 23) & 0xffu;
+  ok = ok && fe - 1u < 0xfdu;  // f normal, not at the top binade
+  // ulp(f) as a double: 2^(fe - 127 - 23)
+  const double ulp = __longlong_as_double((long long)(fe - 150 + 1023) << 52);
+  const double dlt = t - (double)f;  // exact (t and f are within one f32 ulp)
+  const bool toward_zero = (dlt < 0.0) != ((fb >> 31) != 0u);
+  // below a power of two the spacing toward zero halves
+  const double half = (toward_zero && (fb & 0x7fffffu) == 0u) ? 0.25 * ulp : 0.5 * ulp;
+  // |t_ref - t| <= 2^-46 |q| + 2^-51 |t| (the Newton results are within a
+  // few roundings, ~2^-50 |q|, of the exact quotient; t and t_ref each carry
+  // one more rounding of 2^-53 |t|)
+  const double bound = __fma_rn(0x1p-46, fabs(q), 0x1p-51 * fabs(t));
+  ok = ok && fabs(dlt) + bound < half;
+  if (ok) {
+    st = af;
+    th = f;
+  }
+  return ok;
+}
+
+}  // namespace lgd

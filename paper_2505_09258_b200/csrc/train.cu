@@ -28,6 +28,7 @@
 // exactly like the reference's unfused x86-64 double arithmetic.
 #include <cub/device/device_radix_sort.cuh>
 
+#include "adagrad.cuh"
 #include "common.cuh"
 #include "train.cuh"
 
@@ -450,7 +451,10 @@ __device__ __forceinline__ float* row_state(const BatchArgs& a, uint32_t r) {
 // vectors) would otherwise send every warp through it.  Bit-identical to the
 // reference for all inputs.
 __device__ __forceinline__ double opaque_sel(bool p, double a, double b);
-__device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr, double eps);
+__device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr,
+                                             double eps) {
+  if (!adagrad_try_fast(gi, th, st, lr, eps)) adagrad_exact(gi, th, st, lr, eps);
+}
 __device__ __forceinline__ void adagrad_elem(double gi, float& th, float& st, double lr,
                                              double eps) {
   adagrad_fast(gi, th, st, lr, eps);
@@ -709,15 +713,6 @@ __device__ __forceinline__ double opaque_sel(bool p, double a, double b) {
 // adagrad_update (train.cpp:342-354) with the inline (fast-path) IEEE
 // division and square root; a zero quotient (lr*g == +-0) is selected, never
 // divided, since zero operands take CUDA's slow path.  Bit-identical.
-__device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr,
-                                             double eps) {
-  const double acc = (double)st + gi * gi;
-  st = (float)acc;
-  const double num = lr * gi;
-  const bool zero = num == 0.0;
-  const double q = opaque_sel(zero, 1.0, num) / (sqrt(opaque_sel(zero, 1.0, acc)) + eps);
-  th = (float)((double)th - (zero ? num : q));
-}
 
 // adagrad_update (train.cpp:342-354) on the lane's elements: only vectors
 // the lane owns run it (an idle lane's zero gradient would otherwise send the
@@ -726,15 +721,18 @@ __device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, do
 template <int KIND, int NV>
 __device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const double* acc,
                                               float* th, float* st, double lr, double eps) {
+  uint32_t slow = 0;  // elements the fast path could not certify (~0.05%)
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (!L.ok[v]) continue;
 #pragma unroll
-    for (int e = 4 * v; e < 4 * v + 4; ++e) {
-      const double a2 = (double)st[e] + acc[e] * acc[e];
-      st[e] = (float)a2;
-      th[e] = (float)((double)th[e] - lr * acc[e] / (sqrt(a2) + eps));
-    }
+    for (int e = 4 * v; e < 4 * v + 4; ++e)
+      if (!adagrad_try_fast(acc[e], th[e], st[e], lr, eps)) slow |= 1u << e;
+  }
+  if (slow) {
+#pragma unroll
+    for (int e = 0; e < 4 * NV; ++e)
+      if ((slow >> e) & 1u) adagrad_exact(acc[e], th[e], st[e], lr, eps);
   }
 }
 
