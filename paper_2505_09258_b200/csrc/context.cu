@@ -506,11 +506,18 @@ struct lgd_context {
     if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
   }
 
+  // the largest bucket of the partition plan: scratch is sized for it once,
+  // so no buffer grows (cudaFree + cudaMalloc, a device sync) mid-epoch
+  uint64_t max_bucket() const {
+    uint64_t mx = 0;
+    for (size_t b = 0; b + 1 < offsets.size(); ++b) mx = std::max(mx, offsets[b + 1] - offsets[b]);
+    return mx;
+  }
+
   void reserve_for(const std::vector<WorkItem>& items, uint64_t* total_batches) {
-    uint64_t max_m = 0, tb = 0;
+    uint64_t max_m = max_bucket(), tb = 0;
     for (const auto& it : items) {
       const uint64_t m = bucket_size(it);
-      max_m = std::max(max_m, m);
       tb += (m + opt.batch_size - 1) / opt.batch_size;
     }
     ensure_bucket(max_m);
@@ -565,8 +572,7 @@ struct lgd_context {
     check_ready();
     const auto t0 = std::chrono::steady_clock::now();
     reserve_for(items, nullptr);
-    uint64_t max_m = 0;
-    for (const auto& it : items) max_m = std::max(max_m, bucket_size(it));
+    const uint64_t max_m = max_bucket();
     auto next_nonempty = [&](size_t i) {
       while (i < items.size() && bucket_size(items[i]) == 0) ++i;
       return i;
