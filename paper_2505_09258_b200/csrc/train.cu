@@ -39,6 +39,27 @@ namespace {
 constexpr int kScoreWarps = 4;
 constexpr int kSegThreads = 256;
 constexpr int kSegDepth = 4;  // pieces whose theta / state rows are in flight per warp
+
+// Developer timeline of K4 warps (build with -DLGD_TRACE; not in the product .so)
+#ifdef LGD_TRACE
+__device__ unsigned long long g_trace_k4[8][1024];
+__device__ unsigned int g_trace_k4_n[8];
+#define K4_TRACE(tag)                                                                  \
+  do {                                                                                 \
+    const unsigned wg = (blockIdx.x * kSegThreads + threadIdx.x) >> 5;                 \
+    if ((threadIdx.x & 31) == 0 && wg % 7001 == 0 && wg / 7001 < 8) {                  \
+      const unsigned i = g_trace_k4_n[wg / 7001]++;                                    \
+      if (i < 512) {                                                                   \
+        g_trace_k4[wg / 7001][2 * i] = clock64();                                      \
+        g_trace_k4[wg / 7001][2 * i + 1] = (tag);                                      \
+      }                                                                                \
+    }                                                                                  \
+  } while (0)
+#else
+#define K4_TRACE(tag) \
+  do {                \
+  } while (0)
+#endif
 constexpr int kPass2Threads = 256;
 constexpr uint8_t kNoHead = 1;
 constexpr uint8_t kContOut = 2;
@@ -942,6 +963,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
 #pragma unroll 1
     for (; t < np; ++t) {
+      K4_TRACE(1);
       const bool has_next = t + 1 < np;
       const int nxt = has_next ? __ffs(rest) - 1 : nlive;
       rest &= rest - 1;
@@ -952,15 +974,18 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       const float* slot = ring + (t % kSegDepth) * slotf;
       L.lds(slot, th);
       L.lds(slot + rowf, st);
+      K4_TRACE(2 + 16 * (pend - cur));
       double acc[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) acc[e] = 0.0;
       add_loaded<KIND, NV, REL, SH>(x, L, cit, x.k, acc, th);
+      K4_TRACE(3);
       for (int q = cur + 1; q < pend; ++q) {
         ItemRegs<NE> it;
         load_item<KIND, NV, REL, SH>(x, L, item_val(q), true, it);
         add_loaded<KIND, NV, REL, SH>(x, L, it, x.k, acc, th);
       }
+      K4_TRACE(4);
       const uint32_t row = rowof(__shfl_sync(0xffffffffu, key, cur));
       if (t == 0 && cont_in) {
         L.std_(a.part_first + c * d, acc);
@@ -971,6 +996,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         if (lane == 0) (REL ? a.grad_rel_flag : a.grad_node_flag)[row] = 1;
       } else {
         adagrad_lanes(L, acc, th, st, lr, eps);
+        K4_TRACE(5);
         L.stf(theta + (uint64_t)row * d, th);
         L.stf(state + (uint64_t)row * d, st);
       }
@@ -1315,6 +1341,14 @@ size_t batch_sort_temp_bytes(uint64_t max_items) {
 }
 
 size_t score_smem_bytes(uint32_t dim, uint32_t k) { return ScoreSmem(dim, k).block_bytes(); }
+
+#ifdef LGD_TRACE
+extern "C" int lgd_debug_trace_k4(unsigned long long* out) {
+  unsigned int z[8] = {0};
+  cudaMemcpyFromSymbol(out, g_trace_k4, sizeof(g_trace_k4));
+  return cudaMemcpyToSymbol(g_trace_k4_n, z, sizeof z) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   if (a.P == 0) return;
