@@ -299,11 +299,15 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         a.mix[p * d + i] = mx;
       }
     } else {
-      for (uint32_t j = lane; j < k; j += 32) a.w[p * k + j] = ebuf[j] * inv_sum;
+      for (uint32_t j = lane; j < k; j += 32) {  // w_j = IR3_j / S as IR3_j * (1 / S)
+        ebuf[j] = ebuf[j] * inv_sum;
+        a.w[p * k + j] = ebuf[j];
+      }
+      __syncwarp();
       // mix = sum_j w_j neg_j - dst, j ascending (train.cpp:306-323)
       for (uint32_t i = lane; i < d; i += 32) {
         double mx = -(double)drow[i];
-        for (uint32_t j = 0; j < k; ++j) mx += (ebuf[j] * inv_sum) * (double)R[(3 + j) * dpad + i];
+        for (uint32_t j = 0; j < k; ++j) mx += ebuf[j] * (double)R[(3 + j) * dpad + i];
         a.mix[p * d + i] = mx;
       }
     }
