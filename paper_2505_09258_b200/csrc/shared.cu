@@ -348,6 +348,46 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 32 consecutive 32-bit TMEM columns of this thread's lane <- v
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T ("TS": A is read from TMEM, lane = row)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// a [128 x dpad] K-major core-matrix tile in shared memory -> TMEM columns
+// [tcol, tcol + dpad), lane = row (one 128 x 8 slice per tcgen05.cp; ordered
+// before the MMAs this thread issues next)
+__device__ __forceinline__ void tile_to_tmem(uint32_t tcol, uint32_t a0, uint32_t dp) {
+  const uint32_t kcore = (dp / 4) * 128;
+  for (uint32_t ks = 0; ks < dp / 8; ++ks)
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tcol + ks * 8),
+                 "l"(smem_desc(a0 + ks * 256, 128, kcore))
+                 : "memory");
+}
+
 // 2^x, flush-to-zero approximation (one MUFU op; 2^-inf = +0)
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -376,22 +416,23 @@ __device__ __forceinline__ uint32_t keep_mask(uint32_t j0, uint32_t limit) {
   return n >= 32 ? 0xffffffffu : (1u << n) - 1u;
 }
 
-// S = A . B^T over K = dpad into TMEM columns dcol (N = n columns)
-__device__ __forceinline__ void mma_scores(uint32_t dcol, uint32_t a0, uint32_t b0, uint32_t dp,
+// S = A . B^T over K = dpad into TMEM columns dcol (N = n columns); A in
+// TMEM at acol, B K-major in shared memory
+__device__ __forceinline__ void mma_scores(uint32_t dcol, uint32_t acol, uint32_t b0, uint32_t dp,
                                            uint32_t n) {
   const uint32_t kcore = (dp / 4) * 128;
   const uint32_t id = instr_desc(128, n, false, false);
   for (uint32_t ks = 0; ks < dp / 8; ++ks)
-    mma_tf32(dcol, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore), id,
-             ks > 0);
+    mma_tf32_ts(dcol, acol + ks * 8, smem_desc(b0 + ks * 256, 128, kcore), id, ks > 0);
 }
-// D (+)= W . B^T with W [128 x 64] and B^T [dpad x 64], both K-major over 64
-__device__ __forceinline__ void mma_weights(uint32_t dcol, uint32_t w0, uint32_t t0, uint32_t dp,
+// D (+)= W . B^T with W [128 x 64] in TMEM at wcol and B^T [dpad x 64]
+// K-major in shared memory
+__device__ __forceinline__ void mma_weights(uint32_t dcol, uint32_t wcol, uint32_t t0, uint32_t dp,
                                             bool accumulate) {
   const uint32_t id = instr_desc(128, dp, false, false);
   for (uint32_t ks = 0; ks < 64 / 8; ++ks)
-    mma_tf32(dcol, smem_desc(w0 + ks * 256, 128, 16 * 128), smem_desc(t0 + ks * 256, 128, 16 * 128),
-             id, accumulate || ks > 0);
+    mma_tf32_ts(dcol, wcol + ks * 8, smem_desc(t0 + ks * 256, 128, 16 * 128), id,
+                accumulate || ks > 0);
 }
 
 // barrier setup shared by the three kernels
@@ -423,7 +464,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   const uint32_t counts[7] = {1, 1, 1, 1, 1, kWarps, kWarps};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
-  sg_setup(&tbase_s, 128, bars, 7, counts);
+  sg_setup(&tbase_s, 256, bars, 7, counts);  // S buffers [0, 128), IR1 tile [128, 128 + dpad)
   const uint32_t tbase = tbase_s;
   const uint32_t nblk = kp / kNegBlk;
   const int q = warp & 3, hf = warp >> 2;
@@ -443,13 +484,16 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
         bar_wait(ld_n + (b & 1), (b >> 1) & 1);
         if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + (b & 1) * 64, saddr(sA), saddr(sN + (b & 1) * blk_bytes), dp, kNegBlk);
+        mma_scores(tbase + (b & 1) * 64, tbase + 128, saddr(sN + (b & 1) * blk_bytes), dp,
+                   kNegBlk);
         mma_commit(mma_s + (b & 1));
       };
       bar_expect(ld_a, tile_bytes);
       bulk_load(sA, gA, tile_bytes, ld_a);
       for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_n(b);
       bar_wait(ld_a, 0);
+      tc_fence_after();
+      tile_to_tmem(tbase + 128, saddr(sA), dp);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
         if (b + 1 < nblk) issue_s(b + 1);
@@ -499,12 +543,14 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_free(tbase, 128);
+  if (warp == 0) tmem_free(tbase, 256);
 }
 
 // SG2: per tile, mix = W N - dst with W = exp(S - M) / Z recomputed block by
-// block.  TMEM: mix in columns [0, dpad), S buffers at scol and scol + 64.
-// smem: IR1 tile, N blocks x2 (S operand), N^T blocks x2 (mix operand), W.
+// block.  TMEM (512 columns): mix [0, 128), S buffers [128, 256), the IR1
+// tile [256, 256 + dpad) (A of the S MMA), W [384, 448) (A of the mix MMA).
+// smem: IR1 tile (staging for tcgen05.cp), N blocks x2, N^T blocks x2: the
+// MMAs read only their B operands from shared memory.
 __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uint32_t tcols,
                                                                 uint32_t scol) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -513,7 +559,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
   unsigned char* sA = smem;
   unsigned char* sN = sA + tile_bytes;       // 2 x N block
   unsigned char* sT = sN + 2 * blk_bytes;    // 2 x N^T block
-  unsigned char* sW = sT + 2 * blk_bytes;    // 128 x 64
+  (void)scol;
   // 0 ld_a, 1-2 ld_n, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
   __shared__ uint64_t bars[11];
   __shared__ uint32_t tbase_s;
@@ -549,7 +595,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
         bar_wait(ld_n + (b & 1), (b >> 1) & 1);
         if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + scol + (b & 1) * 64, saddr(sA), saddr(sN + (b & 1) * blk_bytes), dp,
+        mma_scores(tbase + 128 + (b & 1) * 64, tbase + 256, saddr(sN + (b & 1) * blk_bytes), dp,
                    kNegBlk);
         mma_commit(mma_s + (b & 1));
       };
@@ -560,6 +606,8 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
         load_t(b);
       }
       bar_wait(ld_a, 0);
+      tc_fence_after();
+      tile_to_tmem(tbase + 256, saddr(sA), dp);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
         SG_TRACE(b * 8 + 0);
@@ -571,7 +619,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
         SG_TRACE(b * 8 + 2);
         bar_wait(ld_t + (b & 1), (b >> 1) & 1);
         tc_fence_after();
-        mma_weights(tbase, saddr(sW), saddr(sT + (b & 1) * blk_bytes), dp, b > 0);
+        mma_weights(tbase, tbase + 384, saddr(sT + (b & 1) * blk_bytes), dp, b > 0);
         mma_commit(mma_w);
         SG_TRACE(b * 8 + 3);
         bar_wait(mma_w, b & 1);
@@ -589,7 +637,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       tc_fence_after();
       SG_TRACE(nb * 8 + 1);
       float v[32];
-      tmem_ld32(lane_addr + scol + (nb & 1) * 64 + hf * 32, v);
+      tmem_ld32(lane_addr + 128 + (nb & 1) * 64 + hf * 32, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (nb & 1));
@@ -597,12 +645,11 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       weights32(v, rm2, ri, valid ? keep_mask(nb * kNegBlk + hf * 32, k) : 0u, w);
       SG_TRACE(nb * 8 + 2);
       if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W free again
+      tc_fence_after();
       SG_TRACE(nb * 8 + 3);
-#pragma unroll
-      for (int c = 0; c < 32; c += 4)
-        *reinterpret_cast<float4*>(sW + cm_offset(row, hf * 32 + c, kNegBlk)) =
-            make_float4(w[c], w[c + 1], w[c + 2], w[c + 3]);
-      fence_async_smem();
+      tmem_st32(lane_addr + 384 + hf * 32, w);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(wrdy);
       SG_TRACE(nb * 8 + 4);
@@ -662,9 +709,10 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
 
 // SG3: per (chunk, 128 negatives): G = W^T IR1 over the chunk's positives in
 // 64-positive slices; S^T = N IR1^T is recomputed per slice (M = the 128
-// negatives, N = 64 positives).  TMEM: G in [0, dpad), S^T at scol, scol + 64.
-// smem: N block (128 x dpad), IR1 slices x2 (S operand), IR1^T slices x2
-// (G operand), W^T.
+// negatives, N = 64 positives).  TMEM (512 columns): G [0, 128), S^T buffers
+// [128, 256), the negative block [256, 256 + dpad), W^T [384, 448).
+// smem: the negative block (staging for tcgen05.cp), IR1 slices x2 (B of the
+// S^T MMA), IR1^T slices x2 (B of the G MMA).
 __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, uint32_t tcols,
                                                                  uint32_t scol) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -673,7 +721,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   unsigned char* sN = smem;
   unsigned char* sA = sN + nblk_bytes;     // 2 x IR1 slice
   unsigned char* sT = sA + 2 * sl_bytes;   // 2 x IR1^T slice
-  unsigned char* sW = sT + 2 * sl_bytes;   // 128 x 64
+  (void)scol;
   // 0 ld_n, 1-2 ld_a, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
   __shared__ uint64_t bars[11];
   __shared__ uint32_t tbase_s;
@@ -711,7 +759,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
         bar_wait(ld_a + (s & 1), (s >> 1) & 1);
         if (s >= 2) bar_wait(epi + (s & 1), ((s - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + scol + (s & 1) * 64, saddr(sN), saddr(sA + (s & 1) * sl_bytes), dp,
+        mma_scores(tbase + 128 + (s & 1) * 64, tbase + 256, saddr(sA + (s & 1) * sl_bytes), dp,
                    kPosSlice);
         mma_commit(mma_s + (s & 1));
       };
@@ -722,6 +770,8 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
         load_t(s);
       }
       bar_wait(ld_n, 0);
+      tc_fence_after();
+      tile_to_tmem(tbase + 256, saddr(sN), dp);
       issue_s(0);
       for (uint32_t s = 0; s < nsl; ++s) {
         if (s + 1 < nsl) issue_s(s + 1);
@@ -730,7 +780,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
         bar_wait(wrdy, s & 1);
         bar_wait(ld_t + (s & 1), (s >> 1) & 1);
         tc_fence_after();
-        mma_weights(tbase, saddr(sW), saddr(sT + (s & 1) * sl_bytes), dp, s > 0);
+        mma_weights(tbase, tbase + 384, saddr(sT + (s & 1) * sl_bytes), dp, s > 0);
         mma_commit(mma_w);
         bar_wait(mma_w, s & 1);
         if (s + 2 < nsl) load_t(s + 2);
@@ -749,7 +799,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       bar_wait(mma_s + (s & 1), (s >> 1) & 1);
       tc_fence_after();
       float v[32];
-      tmem_ld32(lane_addr + scol + (s & 1) * 64 + hf * 32, v);
+      tmem_ld32(lane_addr + 128 + (s & 1) * 64 + hf * 32, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (s & 1));
@@ -761,12 +811,11 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
         const float e = ex2(__fmaf_rn(v[cc], kLog2e, -m2)) * zi;
         w[cc] = (keep >> cc) & 1u ? tf32_pos(e) : 0.f;
       }
-      if (s >= 1) bar_wait(mma_w, (s - 1) & 1);
-#pragma unroll
-      for (int cc = 0; cc < 32; cc += 4)
-        *reinterpret_cast<float4*>(sW + cm_offset(row, hf * 32 + cc, kPosSlice)) =
-            make_float4(w[cc], w[cc + 1], w[cc + 2], w[cc + 3]);
-      fence_async_smem();
+      if (s >= 1) bar_wait(mma_w, (s - 1) & 1);  // W^T free again
+      tc_fence_after();
+      tmem_st32(lane_addr + 384 + hf * 32, w);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(wrdy);
     }
@@ -828,8 +877,8 @@ SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P) {
 
 size_t shared_smem_bytes(uint32_t dpad) {
   const size_t t = 128ull * dpad * 4, b = (size_t)kNegBlk * dpad * 4;
-  const size_t sg2 = t + 4 * b + 128 * kNegBlk * 4;
-  const size_t sg3 = t + 4 * (size_t)kPosSlice * dpad * 4 + 128 * kPosSlice * 4;
+  const size_t sg2 = t + 4 * b;
+  const size_t sg3 = t + 4 * (size_t)kPosSlice * dpad * 4;
   return sg2 > sg3 ? sg2 : sg3;
 }
 
@@ -853,15 +902,15 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   LGD_LAUNCH_CHECK();
   const size_t t = 128ull * dp * 4, b = (size_t)kNegBlk * dp * 4;
   const size_t sm1 = t + 2 * b;
-  const size_t sm2 = t + 4 * b + 128 * kNegBlk * 4;
-  const size_t sm3 = t + 4 * (size_t)kPosSlice * dp * 4 + 128 * kPosSlice * 4;
+  const size_t sm2 = t + 4 * b;
+  const size_t sm3 = t + 4 * (size_t)kPosSlice * dp * 4;
   static size_t set1 = 0, set2 = 0, set3 = 0;  // attributes only grow
   if (sm1 > set1) set_smem(sg1_stats_kernel, set1 = sm1);
   if (sm2 > set2) set_smem(sg2_mix_kernel, set2 = sm2);
   if (sm3 > set3) set_smem(sg3_grad_kernel, set3 = sm3);
   const unsigned tiles = (unsigned)(a.nch * a.tpc);
-  const uint32_t scol = (dp + 31) & ~31u;
-  const uint32_t tcols = pow2_cols(scol + 128);  // G / mix, then two S buffers
+  const uint32_t scol = 128;    // S buffers at [128, 256)
+  const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
   sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);
   LGD_LAUNCH_CHECK();
   sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, scol);
