@@ -38,7 +38,8 @@ namespace lgd {
 
 namespace {
 
-constexpr int kNegBlk = 64;    // negatives per S block (SG1 / SG2)
+constexpr int kNegBlk = 64;    // negatives per S block (SG2)
+constexpr int kStatBlk = 128;  // negatives per S block (SG1: one N = 128 MMA chain per block)
 constexpr int kPosSlice = 64;  // positives per slice (SG3)
 
 // ------------------------------------------------------------ PTX helpers
@@ -454,7 +455,7 @@ __device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint
 __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad;
-  const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kNegBlk * dp * 4;
+  const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kStatBlk * dp * 4;
   unsigned char* sA = smem;
   unsigned char* sN = smem + tile_bytes;  // two blocks
   __shared__ uint64_t bars[7];            // 0 ld_a, 1-2 ld_n, 3-4 mma_s, 5-6 epi
@@ -464,9 +465,9 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   const uint32_t counts[7] = {1, 1, 1, 1, 1, kWarps, kWarps};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
-  sg_setup(&tbase_s, 256, bars, 7, counts);  // S buffers [0, 128), IR1 tile [128, 128 + dpad)
+  sg_setup(&tbase_s, 512, bars, 7, counts);  // S buffers [0, 256), IR1 tile [256, 256 + dpad)
   const uint32_t tbase = tbase_s;
-  const uint32_t nblk = kp / kNegBlk;
+  const uint32_t nblk = kp / kStatBlk;
   const int q = warp & 3, hf = warp >> 2;
   const uint32_t row = q * 32 + lane;
   float m = -INFINITY, z = 0.f;  // running max and sum of 2^((s - m) log2e)
@@ -484,8 +485,8 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
         bar_wait(ld_n + (b & 1), (b >> 1) & 1);
         if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + (b & 1) * 64, tbase + 128, saddr(sN + (b & 1) * blk_bytes), dp,
-                   kNegBlk);
+        mma_scores(tbase + (b & 1) * kStatBlk, tbase + 256, saddr(sN + (b & 1) * blk_bytes), dp,
+                   kStatBlk);
         mma_commit(mma_s + (b & 1));
       };
       bar_expect(ld_a, tile_bytes);
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
       for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_n(b);
       bar_wait(ld_a, 0);
       tc_fence_after();
-      tile_to_tmem(tbase + 128, saddr(sA), dp);
+      tile_to_tmem(tbase + 256, saddr(sA), dp);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
         if (b + 1 < nblk) issue_s(b + 1);
@@ -502,25 +503,33 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
       }
     }
   } else {  // epilogue
-    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + hf * 32;
+    // each warp half covers 64 of a block's 128 columns
+    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + hf * (kStatBlk / 2);
     for (uint32_t nb = 0; nb < nblk; ++nb) {
       bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
       tc_fence_after();
-      float v[32];
-      tmem_ld32(lane_addr + (nb & 1) * 64, v);
+      float v[64];
+      tmem_ld32(lane_addr + (nb & 1) * kStatBlk, v);
+      tmem_ld32(lane_addr + (nb & 1) * kStatBlk + 32, v + 32);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (nb & 1));
-      const uint32_t keep = keep_mask(nb * kNegBlk + hf * 32, k);
+      const uint32_t j0 = nb * kStatBlk + hf * (kStatBlk / 2);
+      const uint32_t keep0 = keep_mask(j0, k), keep1 = keep_mask(j0 + 32, k);
       float bm = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) bm = fmaxf(bm, (keep >> c) & 1u ? v[c] : -INFINITY);
+      for (int c = 0; c < 64; ++c) {
+        const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
+        bm = fmaxf(bm, kc ? v[c] : -INFINITY);
+      }
       const float mn = fmaxf(m, bm);
       const float ml2 = mn * kLog2e;
       float zs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 32; ++c)
-        zs += (keep >> c) & 1u ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+      for (int c = 0; c < 64; ++c) {
+        const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
+        zs += kc ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+      }
       z = (m == -INFINITY ? 0.f : z * ex2((m - mn) * kLog2e)) + zs;
       m = mn;
     }
@@ -543,7 +552,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_free(tbase, 256);
+  if (warp == 0) tmem_free(tbase, 512);
 }
 
 // SG2: per tile, mix = W N - dst with W = exp(S - M) / Z recomputed block by
@@ -901,7 +910,7 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   shared_gather_kernel<<<(unsigned)(a.nch * (uint64_t)a.kpad / kPrepRows), 256, psm, st>>>(a);
   LGD_LAUNCH_CHECK();
   const size_t t = 128ull * dp * 4, b = (size_t)kNegBlk * dp * 4;
-  const size_t sm1 = t + 2 * b;
+  const size_t sm1 = t + 2 * (size_t)kStatBlk * dp * 4;
   const size_t sm2 = t + 4 * b;
   const size_t sm3 = t + 4 * (size_t)kPosSlice * dp * 4;
   static size_t set1 = 0, set2 = 0, set3 = 0;  // attributes only grow
