@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kNegBlk = 64;    // negatives per S block (SG2)
 constexpr int kStatBlk = 128;  // negatives per S block (SG1: one N = 128 MMA chain per block)
+constexpr int kMixBlk = 128;   // negatives per S / mix block (SG2)
 constexpr int kPosSlice = 64;  // positives per slice (SG3)
 
 // ------------------------------------------------------------ PTX helpers
@@ -426,6 +427,15 @@ __device__ __forceinline__ void mma_scores(uint32_t dcol, uint32_t acol, uint32_
   for (uint32_t ks = 0; ks < dp / 8; ++ks)
     mma_tf32_ts(dcol, acol + ks * 8, smem_desc(b0 + ks * 256, 128, kcore), id, ks > 0);
 }
+// the same with A in shared memory (K-major core-matrix tile at a0)
+__device__ __forceinline__ void mma_scores_ss(uint32_t dcol, uint32_t a0, uint32_t b0, uint32_t dp,
+                                              uint32_t n) {
+  const uint32_t kcore = (dp / 4) * 128;
+  const uint32_t id = instr_desc(128, n, false, false);
+  for (uint32_t ks = 0; ks < dp / 8; ++ks)
+    mma_tf32(dcol, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore), id,
+             ks > 0);
+}
 // D (+)= W . B^T with W [128 x 64] in TMEM at wcol and B^T [dpad x 64]
 // K-major in shared memory
 __device__ __forceinline__ void mma_weights(uint32_t dcol, uint32_t wcol, uint32_t t0, uint32_t dp,
@@ -556,30 +566,31 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
 }
 
 // SG2: per tile, mix = W N - dst with W = exp(S - M) / Z recomputed block by
-// block.  TMEM (512 columns): mix [0, 128), S buffers [128, 256), the IR1
-// tile [256, 256 + dpad) (A of the S MMA), W [384, 448) (A of the mix MMA).
-// smem: IR1 tile (staging for tcgen05.cp), N blocks x2, N^T blocks x2: the
-// MMAs read only their B operands from shared memory.
+// block (128 negatives per block: a tf32 MMA costs the same ~96 cycles at
+// N = 64 or 128).  TMEM (512 columns): mix [0, 128), S buffers [128, 384),
+// W [384, 512) (A of the mix MMA).  smem: IR1 tile (A of the S MMA), N blocks
+// x2 (x1 when dpad = 128 would not fit), one N^T block (two 64-column
+// core-matrix sub-tiles).
 __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uint32_t tcols,
-                                                                uint32_t scol) {
+                                                                uint32_t nbuf) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad, d = a.dim;
-  const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kNegBlk * dp * 4;
+  const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kMixBlk * dp * 4;
+  const uint32_t sub_bytes = 64 * dp * 4;    // one 64-negative N^T sub-tile
   unsigned char* sA = smem;
-  unsigned char* sN = sA + tile_bytes;       // 2 x N block
-  unsigned char* sT = sN + 2 * blk_bytes;    // 2 x N^T block
-  (void)scol;
-  // 0 ld_a, 1-2 ld_n, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
-  __shared__ uint64_t bars[11];
+  unsigned char* sN = sA + tile_bytes;       // nbuf x N block
+  unsigned char* sT = sN + nbuf * blk_bytes; // 1 x N^T block
+  // 0 ld_a, 1-2 ld_n, 3 ld_t, 4-5 mma_s, 6-7 epi, 8 wrdy, 9 mma_w
+  __shared__ uint64_t bars[10];
   __shared__ uint32_t tbase_s;
-  uint64_t *ld_a = bars, *ld_n = bars + 1, *ld_t = bars + 3, *mma_s = bars + 5, *epi = bars + 7,
-           *wrdy = bars + 9, *mma_w = bars + 10;
-  const uint32_t counts[11] = {1, 1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
+  uint64_t *ld_a = bars, *ld_n = bars + 1, *ld_t = bars + 3, *mma_s = bars + 4, *epi = bars + 6,
+           *wrdy = bars + 8, *mma_w = bars + 9;
+  const uint32_t counts[10] = {1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
-  sg_setup(&tbase_s, tcols, bars, 11, counts);
+  sg_setup(&tbase_s, tcols, bars, 10, counts);
   const uint32_t tbase = tbase_s;
-  const uint32_t nblk = kp / kNegBlk;
+  const uint32_t nblk = kp / kMixBlk;
   const int q = warp & 3, hf = warp >> 2;
   const uint32_t row = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
@@ -590,53 +601,54 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
           reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
       const unsigned char* gT =
           reinterpret_cast<const unsigned char*>(a.sh_BT) + g.c * (uint64_t)kp * dp * 4;
-      auto load_n = [&](uint32_t b) {
-        bar_expect(ld_n + (b & 1), blk_bytes);
-        bulk_load(sN + (b & 1) * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes,
-                  ld_n + (b & 1));
+      auto load_n = [&](uint32_t b) {  // N block b into buffer b % nbuf
+        const uint32_t i = b % nbuf;
+        bar_expect(ld_n + i, blk_bytes);
+        bulk_load(sN + i * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes, ld_n + i);
       };
       auto load_t = [&](uint32_t b) {
-        bar_expect(ld_t + (b & 1), blk_bytes);
-        bulk_load(sT + (b & 1) * blk_bytes, gT + (uint64_t)b * blk_bytes, blk_bytes,
-                  ld_t + (b & 1));
+        bar_expect(ld_t, blk_bytes);
+        bulk_load(sT, gT + (uint64_t)b * blk_bytes, blk_bytes, ld_t);
       };
       auto issue_s = [&](uint32_t b) {
-        bar_wait(ld_n + (b & 1), (b >> 1) & 1);
+        bar_wait(ld_n + b % nbuf, (b / nbuf) & 1);
         if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + 128 + (b & 1) * 64, tbase + 256, saddr(sN + (b & 1) * blk_bytes), dp,
-                   kNegBlk);
+        mma_scores_ss(tbase + 128 + (b & 1) * kMixBlk, saddr(sA),
+                      saddr(sN + (b % nbuf) * blk_bytes), dp, kMixBlk);
         mma_commit(mma_s + (b & 1));
       };
       bar_expect(ld_a, tile_bytes);
       bulk_load(sA, gA, tile_bytes, ld_a);
-      for (uint32_t b = 0; b < 2 && b < nblk; ++b) {
-        load_n(b);
-        load_t(b);
-      }
+      for (uint32_t b = 0; b < nbuf && b < nblk; ++b) load_n(b);
+      load_t(0);
       bar_wait(ld_a, 0);
-      tc_fence_after();
-      tile_to_tmem(tbase + 256, saddr(sA), dp);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
         SG_TRACE(b * 8 + 0);
-        if (b + 1 < nblk) issue_s(b + 1);
+        if (nbuf == 2 && b + 1 < nblk) issue_s(b + 1);
         SG_TRACE(b * 8 + 1);
         bar_wait(mma_s + (b & 1), (b >> 1) & 1);
-        if (b + 2 < nblk) load_n(b + 2);
+        if (b + nbuf < nblk) load_n(b + nbuf);  // S(b) is done with its buffer
+        if (nbuf == 1 && b + 1 < nblk) issue_s(b + 1);
         bar_wait(wrdy, b & 1);  // the epilogue wrote W(b)
         SG_TRACE(b * 8 + 2);
-        bar_wait(ld_t + (b & 1), (b >> 1) & 1);
+        bar_wait(ld_t, b & 1);
         tc_fence_after();
-        mma_weights(tbase, tbase + 384, saddr(sT + (b & 1) * blk_bytes), dp, b > 0);
+        // mix += W . N^T over the block's 128 negatives (two N^T sub-tiles)
+        const uint32_t id = instr_desc(128, dp, false, false);
+        for (uint32_t ks = 0; ks < kMixBlk / 8; ++ks)
+          mma_tf32_ts(tbase, tbase + 384 + ks * 8,
+                      smem_desc(saddr(sT) + (ks >> 3) * sub_bytes + (ks & 7) * 256, 128, 16 * 128),
+                      id, (b | ks) != 0);
         mma_commit(mma_w);
         SG_TRACE(b * 8 + 3);
         bar_wait(mma_w, b & 1);
         SG_TRACE(b * 8 + 4);
-        if (b + 2 < nblk) load_t(b + 2);
+        if (b + 1 < nblk) load_t(b + 1);
       }
     }
-  } else {  // epilogue
+  } else {  // epilogue: warp half hf covers 64 of a block's 128 columns
     const bool valid = row < g.valid;
     const float rm2 = valid ? a.sh_rowmax[g.row0 + row] * kLog2e : 0.f;
     const float ri = valid ? a.sh_rowinv[g.row0 + row] : 0.f;
@@ -645,18 +657,22 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
       tc_fence_after();
       SG_TRACE(nb * 8 + 1);
-      float v[32];
-      tmem_ld32(lane_addr + 128 + (nb & 1) * 64 + hf * 32, v);
+      const uint32_t scol0 = 128 + (nb & 1) * kMixBlk + hf * 64;
+      float v[32], w0[32], w1[32];
+      const uint32_t j0 = nb * kMixBlk + hf * 64;
+      tmem_ld32(lane_addr + scol0, v);
+      weights32(v, rm2, ri, valid ? keep_mask(j0, k) : 0u, w0);
+      tmem_ld32(lane_addr + scol0 + 32, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (nb & 1));
-      float w[32];
-      weights32(v, rm2, ri, valid ? keep_mask(nb * kNegBlk + hf * 32, k) : 0u, w);
+      weights32(v, rm2, ri, valid ? keep_mask(j0 + 32, k) : 0u, w1);
       SG_TRACE(nb * 8 + 2);
       if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W free again
       tc_fence_after();
       SG_TRACE(nb * 8 + 3);
-      tmem_st32(lane_addr + 384 + hf * 32, w);
+      tmem_st32(lane_addr + 384 + hf * 64, w0);
+      tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -886,7 +902,7 @@ SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P) {
 
 size_t shared_smem_bytes(uint32_t dpad) {
   const size_t t = 128ull * dpad * 4, b = (size_t)kNegBlk * dpad * 4;
-  const size_t sg2 = t + 4 * b;
+  const size_t sg2 = t + 2 * (size_t)kMixBlk * dpad * 4;
   const size_t sg3 = t + 4 * (size_t)kPosSlice * dpad * 4;
   return sg2 > sg3 ? sg2 : sg3;
 }
@@ -911,7 +927,10 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   LGD_LAUNCH_CHECK();
   const size_t t = 128ull * dp * 4, b = (size_t)kNegBlk * dp * 4;
   const size_t sm1 = t + 2 * (size_t)kStatBlk * dp * 4;
-  const size_t sm2 = t + 4 * b;
+  // SG2: two N buffers when they fit next to the tile and the N^T block
+  const size_t mblk = (size_t)kMixBlk * dp * 4;
+  const uint32_t nbuf2 = t + 3 * mblk <= 227 * 1024 ? 2 : 1;
+  const size_t sm2 = t + (nbuf2 + 1) * mblk;
   const size_t sm3 = t + 4 * (size_t)kPosSlice * dp * 4;
   static size_t set1 = 0, set2 = 0, set3 = 0;  // attributes only grow
   if (sm1 > set1) set_smem(sg1_stats_kernel, set1 = sm1);
@@ -922,7 +941,7 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
   sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);
   LGD_LAUNCH_CHECK();
-  sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, scol);
+  sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, nbuf2);
   LGD_LAUNCH_CHECK();
   sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, scol);
   LGD_LAUNCH_CHECK();
