@@ -38,10 +38,9 @@ namespace lgd {
 
 namespace {
 
-constexpr int kNegBlk = 64;    // negatives per S block (SG2)
 constexpr int kStatBlk = 128;  // negatives per S block (SG1: one N = 128 MMA chain per block)
 constexpr int kMixBlk = 128;   // negatives per S / mix block (SG2)
-constexpr int kPosSlice = 64;  // positives per slice (SG3)
+constexpr int kGradSlice = 128;  // positives per S^T / G slice (SG3)
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -733,26 +732,26 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
 }
 
 // SG3: per (chunk, 128 negatives): G = W^T IR1 over the chunk's positives in
-// 64-positive slices; S^T = N IR1^T is recomputed per slice (M = the 128
-// negatives, N = 64 positives).  TMEM (512 columns): G [0, 128), S^T buffers
-// [128, 256), the negative block [256, 256 + dpad), W^T [384, 448).
-// smem: the negative block (staging for tcgen05.cp), IR1 slices x2 (B of the
-// S^T MMA), IR1^T slices x2 (B of the G MMA).
+// 128-positive slices; S^T = N IR1^T is recomputed per slice (M = the 128
+// negatives, N = 128 positives).  TMEM (512 columns): G [0, 128), S^T buffers
+// [128, 384), W^T [384, 512) (A of the G MMA).  smem: the negative block (A of
+// the S^T MMA), IR1 tiles x2 (x1 when dpad = 128 would not fit), one IR1^T
+// slice pair (two 64-column core-matrix sub-tiles).
 __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, uint32_t tcols,
-                                                                 uint32_t scol) {
+                                                                 uint32_t nbuf) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad, d = a.dim;
-  const uint32_t nblk_bytes = 128 * dp * 4, sl_bytes = kPosSlice * dp * 4;
+  const uint32_t nblk_bytes = 128 * dp * 4, sl_bytes = kGradSlice * dp * 4;
+  const uint32_t sub_bytes = 64 * dp * 4;  // one 64-positive IR1^T sub-tile
   unsigned char* sN = smem;
-  unsigned char* sA = sN + nblk_bytes;     // 2 x IR1 slice
-  unsigned char* sT = sA + 2 * sl_bytes;   // 2 x IR1^T slice
-  (void)scol;
-  // 0 ld_n, 1-2 ld_a, 3-4 ld_t, 5-6 mma_s, 7-8 epi, 9 wrdy, 10 mma_w
-  __shared__ uint64_t bars[11];
+  unsigned char* sA = sN + nblk_bytes;      // nbuf x IR1 tile
+  unsigned char* sT = sA + nbuf * sl_bytes; // 1 x IR1^T slice
+  // 0 ld_n, 1-2 ld_a, 3 ld_t, 4-5 mma_s, 6-7 epi, 8 wrdy, 9 mma_w
+  __shared__ uint64_t bars[10];
   __shared__ uint32_t tbase_s;
-  uint64_t *ld_n = bars, *ld_a = bars + 1, *ld_t = bars + 3, *mma_s = bars + 5, *epi = bars + 7,
-           *wrdy = bars + 9, *mma_w = bars + 10;
-  const uint32_t counts[11] = {1, 1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
+  uint64_t *ld_n = bars, *ld_a = bars + 1, *ld_t = bars + 3, *mma_s = bars + 4, *epi = bars + 6,
+           *wrdy = bars + 8, *mma_w = bars + 9;
+  const uint32_t counts[10] = {1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, hf = warp >> 2;
   const uint32_t row = q * 32 + lane;  // negative n0 + row
@@ -761,9 +760,9 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   const uint32_t n0 = (blockIdx.x - c * nbpc) * 128;
   const uint64_t left = a.P - c * a.chunk;
   const uint64_t chunk_rows = left < a.chunk ? left : a.chunk;
-  const uint32_t nsl = (uint32_t)((chunk_rows + kPosSlice - 1) / kPosSlice);
+  const uint32_t nsl = (uint32_t)((chunk_rows + kGradSlice - 1) / kGradSlice);
   const uint64_t crow0 = c * (uint64_t)a.tpc * 128;
-  sg_setup(&tbase_s, tcols, bars, 11, counts);
+  sg_setup(&tbase_s, tcols, bars, 10, counts);
   const uint32_t tbase = tbase_s;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
   if (warp == kWarps) {  // control
@@ -773,72 +772,85 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       const unsigned char* gN =
           reinterpret_cast<const unsigned char*>(a.sh_B) + (c * (uint64_t)kp + n0) * dp * 4;
       auto load_a = [&](uint32_t s) {
-        bar_expect(ld_a + (s & 1), sl_bytes);
-        bulk_load(sA + (s & 1) * sl_bytes, gA + (uint64_t)s * sl_bytes, sl_bytes, ld_a + (s & 1));
+        const uint32_t i = s % nbuf;
+        bar_expect(ld_a + i, sl_bytes);
+        bulk_load(sA + i * sl_bytes, gA + (uint64_t)s * sl_bytes, sl_bytes, ld_a + i);
       };
       auto load_t = [&](uint32_t s) {
-        bar_expect(ld_t + (s & 1), sl_bytes);
-        bulk_load(sT + (s & 1) * sl_bytes, gT + (uint64_t)s * sl_bytes, sl_bytes, ld_t + (s & 1));
+        bar_expect(ld_t, sl_bytes);
+        bulk_load(sT, gT + (uint64_t)s * sl_bytes, sl_bytes, ld_t);
       };
       auto issue_s = [&](uint32_t s) {
-        bar_wait(ld_a + (s & 1), (s >> 1) & 1);
+        bar_wait(ld_a + s % nbuf, (s / nbuf) & 1);
         if (s >= 2) bar_wait(epi + (s & 1), ((s - 2) >> 1) & 1);
         tc_fence_after();
-        mma_scores(tbase + 128 + (s & 1) * 64, tbase + 256, saddr(sA + (s & 1) * sl_bytes), dp,
-                   kPosSlice);
+        mma_scores_ss(tbase + 128 + (s & 1) * kGradSlice, saddr(sN),
+                      saddr(sA + (s % nbuf) * sl_bytes), dp, kGradSlice);
         mma_commit(mma_s + (s & 1));
       };
       bar_expect(ld_n, nblk_bytes);
       bulk_load(sN, gN, nblk_bytes, ld_n);
-      for (uint32_t s = 0; s < 2 && s < nsl; ++s) {
-        load_a(s);
-        load_t(s);
-      }
+      for (uint32_t s = 0; s < nbuf && s < nsl; ++s) load_a(s);
+      load_t(0);
       bar_wait(ld_n, 0);
-      tc_fence_after();
-      tile_to_tmem(tbase + 256, saddr(sN), dp);
       issue_s(0);
+      const uint32_t id = instr_desc(128, dp, false, false);
       for (uint32_t s = 0; s < nsl; ++s) {
-        if (s + 1 < nsl) issue_s(s + 1);
+        if (nbuf == 2 && s + 1 < nsl) issue_s(s + 1);
         bar_wait(mma_s + (s & 1), (s >> 1) & 1);
-        if (s + 2 < nsl) load_a(s + 2);
+        if (s + nbuf < nsl) load_a(s + nbuf);
+        if (nbuf == 1 && s + 1 < nsl) issue_s(s + 1);
         bar_wait(wrdy, s & 1);
-        bar_wait(ld_t + (s & 1), (s >> 1) & 1);
+        bar_wait(ld_t, s & 1);
         tc_fence_after();
-        mma_weights(tbase, tbase + 384, saddr(sT + (s & 1) * sl_bytes), dp, s > 0);
+        // G += W^T . IR1 over the slice's 128 positives (two IR1^T sub-tiles)
+        for (uint32_t ks = 0; ks < kGradSlice / 8; ++ks)
+          mma_tf32_ts(tbase, tbase + 384 + ks * 8,
+                      smem_desc(saddr(sT) + (ks >> 3) * sub_bytes + (ks & 7) * 256, 128, 16 * 128),
+                      id, (s | ks) != 0);
         mma_commit(mma_w);
         bar_wait(mma_w, s & 1);
-        if (s + 2 < nsl) load_t(s + 2);
+        if (s + 1 < nsl) load_t(s + 1);
       }
     }
-  } else {  // epilogue: row = negative, columns = the slice's positives
+  } else {  // epilogue: row = negative, warp half hf covers 64 of the slice's positives
     const bool nvalid = n0 + row < k;
     for (uint32_t s = 0; s < nsl; ++s) {
-      // statistics of this half's 32 positives: lane i holds positive i
-      const uint64_t pq = (uint64_t)s * kPosSlice + hf * 32 + lane;
-      const bool pv = pq < chunk_rows;
-      const float my_m2 = pv ? a.sh_rowmax[crow0 + pq] * kLog2e : 0.f;
-      const float my_i = pv ? a.sh_rowinv[crow0 + pq] : 0.f;
-      const uint32_t pmask = __ballot_sync(0xffffffffu, pv);  // every lane: no divergent vote
-      const uint32_t keep = nvalid ? pmask : 0u;
+      // statistics of this half's 64 positives: lane i holds positives i and 32 + i
+      const uint64_t pq0 = (uint64_t)s * kGradSlice + hf * 64 + lane, pq1 = pq0 + 32;
+      const bool pv0 = pq0 < chunk_rows, pv1 = pq1 < chunk_rows;
+      const float m0 = pv0 ? a.sh_rowmax[crow0 + pq0] * kLog2e : 0.f;
+      const float i0 = pv0 ? a.sh_rowinv[crow0 + pq0] : 0.f;
+      const float m1 = pv1 ? a.sh_rowmax[crow0 + pq1] * kLog2e : 0.f;
+      const float i1 = pv1 ? a.sh_rowinv[crow0 + pq1] : 0.f;
+      const uint32_t pm0 = __ballot_sync(0xffffffffu, pv0);  // every lane: no divergent vote
+      const uint32_t pm1 = __ballot_sync(0xffffffffu, pv1);
+      const uint32_t keep0 = nvalid ? pm0 : 0u, keep1 = nvalid ? pm1 : 0u;
       bar_wait(mma_s + (s & 1), (s >> 1) & 1);
       tc_fence_after();
-      float v[32];
-      tmem_ld32(lane_addr + 128 + (s & 1) * 64 + hf * 32, v);
+      const uint32_t scol0 = 128 + (s & 1) * kGradSlice + hf * 64;
+      float v[32], w0[32], w1[32];
+      tmem_ld32(lane_addr + scol0, v);
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, m0, cc))) *
+                        __shfl_sync(0xffffffffu, i0, cc);
+        w0[cc] = (keep0 >> cc) & 1u ? tf32_pos(e) : 0.f;
+      }
+      tmem_ld32(lane_addr + scol0 + 32, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (s & 1));
-      float w[32];
 #pragma unroll
       for (int cc = 0; cc < 32; ++cc) {
-        const float m2 = __shfl_sync(0xffffffffu, my_m2, cc);
-        const float zi = __shfl_sync(0xffffffffu, my_i, cc);
-        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -m2)) * zi;
-        w[cc] = (keep >> cc) & 1u ? tf32_pos(e) : 0.f;
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, m1, cc))) *
+                        __shfl_sync(0xffffffffu, i1, cc);
+        w1[cc] = (keep1 >> cc) & 1u ? tf32_pos(e) : 0.f;
       }
       if (s >= 1) bar_wait(mma_w, (s - 1) & 1);  // W^T free again
       tc_fence_after();
-      tmem_st32(lane_addr + 384 + hf * 32, w);
+      tmem_st32(lane_addr + 384 + hf * 64, w0);
+      tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -901,9 +913,9 @@ SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P) {
 }
 
 size_t shared_smem_bytes(uint32_t dpad) {
-  const size_t t = 128ull * dpad * 4, b = (size_t)kNegBlk * dpad * 4;
+  const size_t t = 128ull * dpad * 4;
   const size_t sg2 = t + 2 * (size_t)kMixBlk * dpad * 4;
-  const size_t sg3 = t + 4 * (size_t)kPosSlice * dpad * 4;
+  const size_t sg3 = t + 2 * (size_t)kGradSlice * dpad * 4;
   return sg2 > sg3 ? sg2 : sg3;
 }
 
@@ -925,25 +937,26 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   LGD_LAUNCH_CHECK();
   shared_gather_kernel<<<(unsigned)(a.nch * (uint64_t)a.kpad / kPrepRows), 256, psm, st>>>(a);
   LGD_LAUNCH_CHECK();
-  const size_t t = 128ull * dp * 4, b = (size_t)kNegBlk * dp * 4;
+  const size_t t = 128ull * dp * 4;
   const size_t sm1 = t + 2 * (size_t)kStatBlk * dp * 4;
   // SG2: two N buffers when they fit next to the tile and the N^T block
   const size_t mblk = (size_t)kMixBlk * dp * 4;
   const uint32_t nbuf2 = t + 3 * mblk <= 227 * 1024 ? 2 : 1;
   const size_t sm2 = t + (nbuf2 + 1) * mblk;
-  const size_t sm3 = t + 4 * (size_t)kPosSlice * dp * 4;
+  const size_t gsl = (size_t)kGradSlice * dp * 4;
+  const uint32_t nbuf3 = t + 3 * gsl <= 227 * 1024 ? 2 : 1;
+  const size_t sm3 = t + (nbuf3 + 1) * gsl;
   static size_t set1 = 0, set2 = 0, set3 = 0;  // attributes only grow
   if (sm1 > set1) set_smem(sg1_stats_kernel, set1 = sm1);
   if (sm2 > set2) set_smem(sg2_mix_kernel, set2 = sm2);
   if (sm3 > set3) set_smem(sg3_grad_kernel, set3 = sm3);
   const unsigned tiles = (unsigned)(a.nch * a.tpc);
-  const uint32_t scol = 128;    // S buffers at [128, 256)
   const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
   sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);
   LGD_LAUNCH_CHECK();
   sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, nbuf2);
   LGD_LAUNCH_CHECK();
-  sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, scol);
+  sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, nbuf3);
   LGD_LAUNCH_CHECK();
 }
 
