@@ -148,10 +148,6 @@ __host__ __device__ constexpr uint32_t instr_desc(uint32_t M, uint32_t N, bool a
          | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-__device__ __forceinline__ uint32_t cm_offset(uint32_t r, uint32_t c, uint32_t cols) {
-  return ((r >> 3) * (cols >> 2) + (c >> 2)) * 128 + (r & 7) * 16 + (c & 3) * 4;
-}
-
 __device__ __forceinline__ uint32_t pool_index(const BatchArgs& a, uint32_t id) {
   uint64_t prev = 0;
   for (int i = 0; i < a.pool_n; ++i) {
