@@ -427,16 +427,6 @@ __device__ __forceinline__ void mma_scores_ss(uint32_t dcol, uint32_t a0, uint32
     mma_tf32(dcol, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore), id,
              ks > 0);
 }
-// D (+)= W . B^T with W [128 x 64] in TMEM at wcol and B^T [dpad x 64]
-// K-major in shared memory
-__device__ __forceinline__ void mma_weights(uint32_t dcol, uint32_t wcol, uint32_t t0, uint32_t dp,
-                                            bool accumulate) {
-  const uint32_t id = instr_desc(128, dp, false, false);
-  for (uint32_t ks = 0; ks < 64 / 8; ++ks)
-    mma_tf32_ts(dcol, wcol + ks * 8, smem_desc(t0 + ks * 256, 128, 16 * 128), id,
-                accumulate || ks > 0);
-}
-
 // barrier setup shared by the three kernels
 __device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint64_t* bars,
                                          int nbars, const uint32_t* counts) {
