@@ -866,11 +866,6 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   if (warp == 0) tmem_free(tbase, tcols);
 }
 
-uint32_t pow2_cols(uint32_t n) {
-  uint32_t c = 32;
-  while (c < n) c <<= 1;
-  return c;
-}
 
 template <class K>
 void set_smem(K kernel, size_t bytes) {
