@@ -34,7 +34,12 @@ inline void check(int rc) {
   }
 }
 
-enum class ScoreKind { kDot = LGD_MODEL_DOT, kDistMult = LGD_MODEL_DISTMULT, kComplEx = LGD_MODEL_COMPLEX };
+enum class ScoreKind {
+  kDot = LGD_MODEL_DOT,
+  kDistMult = LGD_MODEL_DISTMULT,
+  kComplEx = LGD_MODEL_COMPLEX,
+  kTransE = LGD_MODEL_TRANSE  // not in the reference (parity vs the restatement)
+};
 
 struct ScoreModel {  // train.hpp:15-23
   ScoreKind kind = ScoreKind::kDot;
@@ -48,9 +53,13 @@ struct TrainOptions {  // pipeline.hpp:89-97 (+ AdagradHyper, train.hpp:109-112)
   std::uint32_t negatives = 16;
   bool shuffle = true;
   std::uint64_t seed = 0;
+  // 0: the reference's per-positive negatives; C > 0: shared-negative chunks
+  // (lgd_train_options.shared_chunk; last, so reference-shaped aggregate
+  // initialisers keep their meaning)
+  std::uint32_t shared_chunk = 0;
   lgd_train_options c() const {
-    return lgd_train_options{learning_rate, adagrad_epsilon, batch_size, negatives, shuffle ? 1 : 0, 0,
-                             seed};
+    return lgd_train_options{learning_rate, adagrad_epsilon, batch_size, negatives,
+                             shuffle ? 1 : 0, shared_chunk, seed};
   }
 };
 
