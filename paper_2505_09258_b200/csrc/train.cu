@@ -935,7 +935,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
   if (lead_done) rest &= rest - 1;
   int t = lead_done ? 1 : 0;
   if (t < np) {
-    auto rowof = [&](uint32_t kk) { return REL ? kk : from_pool(a, kk); };
+    // row id of every item, lane-parallel once per chunk (pool index -> node)
+    const uint32_t myrow = REL ? key : from_pool(a, key);
+    auto rowof_at = [&](int s0) { return __shfl_sync(0xffffffffu, myrow, s0 & 31); };
     // theta / state rows of the next kSegDepth pieces are in flight at once:
     // cp.async into this warp's shared-memory ring (no registers held), one
     // commit group per piece.  The first contribution of the next piece is
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       if (u < np) {
         const int s0 = __ffs(srest) - 1;
         srest &= srest - 1;
-        const uint64_t off = (uint64_t)rowof(__shfl_sync(0xffffffffu, key, s0 & 31)) * d;
+        const uint64_t off = (uint64_t)rowof_at(s0) * d;
         const bool fin = finishing(u) && !gout;
         float* slot = ring + (u % kSegDepth) * slotf;
         L.cpa(slot, theta + off, fin || kOwn);
@@ -990,7 +992,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         add_loaded<KIND, NV, REL, SH>(x, L, it, x.k, acc, th);
       }
       K4_TRACE(4);
-      const uint32_t row = rowof(__shfl_sync(0xffffffffu, key, cur));
+      const uint32_t row = rowof_at(cur);
       if (t == 0 && cont_in) {
         L.std_(a.part_first + c * d, acc);
       } else if (!finishing(t)) {
