@@ -663,6 +663,48 @@ struct Lanes {
       }
     }
   }
+  // the same with 32-bit shared-state-space addresses (no generic conversion)
+  __device__ __forceinline__ void cpa_s(uint32_t s, const float* g, bool pred) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!ok[v]) continue;
+      const uint32_t n = pred ? (KIND == 2 ? 8u : 16u) : 0u;
+      if (KIND == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s + 4 * off[v]),
+                     "l"(g + off[v]), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s + 4 * (off[v] + h)),
+                     "l"(g + off[v] + h), "r"(n)
+                     : "memory");
+      } else {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s + 4 * off[v]),
+                     "l"(g + off[v]), "r"(n)
+                     : "memory");
+      }
+    }
+  }
+  __device__ __forceinline__ void lds_s(uint32_t s, float* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if (ok[v]) {
+        if (KIND == 2) {
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a0), "=f"(a1) : "r"(s + 4 * off[v]));
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                       : "=f"(a2), "=f"(a3)
+                       : "r"(s + 4 * (off[v] + h)));
+        } else {
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3)
+                       : "r"(s + 4 * off[v]));
+        }
+      }
+      x[4 * v] = a0;
+      x[4 * v + 1] = a1;
+      x[4 * v + 2] = a2;
+      x[4 * v + 3] = a3;
+    }
+  }
   __device__ __forceinline__ void lds(const float* s, float* x) const {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -945,7 +987,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     extern __shared__ __align__(16) float seg_ring[];
     const uint32_t rowf = (a.dim + 3) & ~3u;
     const uint32_t slotf = 2 * rowf;  // slot: theta, state
-    float* ring = seg_ring + (size_t)(threadIdx.x >> 5) * kSegDepth * slotf;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
+                          (threadIdx.x >> 5) * kSegDepth * slotf * 4;  // bytes
     const int t0 = t;
     // piece starts still to stage / to process, lowest bit first
     uint32_t srest = rest;
@@ -955,9 +998,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         srest &= srest - 1;
         const uint64_t off = (uint64_t)rowof_at(s0) * d;
         const bool fin = finishing(u) && !gout;
-        float* slot = ring + (u % kSegDepth) * slotf;
-        L.cpa(slot, theta + off, fin || kOwn);
-        L.cpa(slot + rowf, state + off, fin);
+        const uint32_t slot = ring + (u % kSegDepth) * slotf * 4;
+        L.cpa_s(slot, theta + off, fin || kOwn);
+        L.cpa_s(slot + rowf * 4, state + off, fin);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -977,9 +1020,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, nxt & 31), has_next, nit);
       asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
       float th[NE], st[NE];
-      const float* slot = ring + (t % kSegDepth) * slotf;
-      L.lds(slot, th);
-      L.lds(slot + rowf, st);
+      const uint32_t slot = ring + (t % kSegDepth) * slotf * 4;
+      L.lds_s(slot, th);
+      L.lds_s(slot + rowf * 4, st);
       K4_TRACE(2 + 16 * (pend - cur));
       double acc[NE];
 #pragma unroll
