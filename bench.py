@@ -180,7 +180,7 @@ def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
                               rE if R else None, rS if R else None, batch_size=batch, k=K_NEG,
                               max_batches=steps, lr=LR)
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "edges/s", "cores": 1,
+    return {"value": done / dt, "unit": "edges/s", "cores": 1, "host_cores": os.cpu_count(),
             "kind": "reference" if kind == "reference" else "port",
             "sample": (f"state {{0,1,2}} resident ({V_loc:,} rows), bucket (0,1): shuffle of "
                        f"{m:,} edges then {steps} batch(es) of {batch:,} positives, "
@@ -226,7 +226,8 @@ def reference_arm(args, cfg, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg["workload"], "step": (
                 f"{REF_SAMPLE_POSITIVES:,} positives of bucket (0,1)"), "storage": "f32"},
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "host_cores", "kind",
+                                                 "sample")},
             "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -456,7 +457,7 @@ def main():
         bucket = np.ascontiguousarray(allb[a0:a0 + min(a1 - a0, 4 * REF_SAMPLE_POSITIVES)])
         del allb
         cpu = cpu_sample(cfg, bucket, t.stride(), 4, REF_SAMPLE_POSITIVES, "reference")
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "host_cores", "kind", "sample")}
 
     if rank == 0:
         line = {
