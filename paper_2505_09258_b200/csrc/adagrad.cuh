@@ -7,10 +7,9 @@
 // division (~50 instructions per element with CUDA's inline sequences and
 // their slow-path branches).  The fast path computes q = lr g / (sqrt(a) +
 // eps) to ~2^-50 relative from FP64 MUFU seeds and two Newton steps each,
-// then t = theta - q and f = float(t).  float(t_exact) == f is guaranteed when
-// t lies farther than the error bound from the f32 rounding midpoints around
-// f; otherwise (and for zero / non-normal operands) the caller redoes the
-// element with the exact form.  Both forms take the products, sums and
+// then t = theta - q.  float(t_exact) is known when t minus and plus the error
+// bound round to the same float; otherwise (and for non-normal operands) the
+// caller redoes the element with the exact form.  Both forms take the products, sums and
 // conversions in the reference's order, so the result is the reference's to
 // the bit either way.
 #pragma once
@@ -53,9 +52,6 @@ __device__ __forceinline__ bool adagrad_try_fast(double g, float& th, float& st,
     th = (float)(t0 - num);
     return true;
   }
-  // a2 within the normal float range (the MUFU seeds flush denormals)
-  const uint32_t ab = __float_as_uint(af);
-  bool ok = ((ab >> 23) & 0xffu) - 1u < 0xfeu;
   // sqrt(a2): s = a2 * rsqrt(a2) from a ~2^-20 seed, two Newton (Heron)
   // steps: the error squares each time, so only the roundings of the last
   // steps remain (< 2^-50 relative)
@@ -71,25 +67,17 @@ __device__ __forceinline__ bool adagrad_try_fast(double g, float& th, float& st,
   const double r2 = __fma_rn(r1, __fma_rn(-den, r1, 1.0), r1);
   const double q = num * r2;
   const double t = t0 - q;
-  const float f = (float)t;
-  // distance of t from the f32 rounding midpoints around f
-  const uint32_t fb = __float_as_uint(f);
-  const uint32_t fe = (fb >> 23) & 0xffu;
-  ok = ok && fe - 1u < 0xfdu;  // f normal, not at the top binade
-  // ulp(f) as a double: 2^(fe - 127 - 23)
-  const double ulp = __longlong_as_double((long long)(fe - 150 + 1023) << 52);
-  const double dlt = t - (double)f;  // exact (t and f are within one f32 ulp)
-  const bool toward_zero = (dlt < 0.0) != ((fb >> 31) != 0u);
-  // below a power of two the spacing toward zero halves
-  const double half = (toward_zero && (fb & 0x7fffffu) == 0u) ? 0.25 * ulp : 0.5 * ulp;
-  // |t_ref - t| <= 2^-46 |q| + 2^-51 |t| (the Newton results are within a
+  // |t_ref - t| <= B = 2^-46 |q| + 2^-51 |t| (the Newton results are within a
   // few roundings, ~2^-50 |q|, of the exact quotient; t and t_ref each carry
-  // one more rounding of 2^-53 |t|)
+  // one more rounding of 2^-53 |t|).  Rounding to float is monotonic, so when
+  // t - B and t + B round to the same float, so does t_ref.  NaN from
+  // non-normal operands (the MUFU seeds flush denormals) fails the compare.
   const double bound = __fma_rn(0x1p-46, fabs(q), 0x1p-51 * fabs(t));
-  ok = ok && fabs(dlt) + bound < half;
+  const float lo = (float)(t - bound), hi = (float)(t + bound);
+  const bool ok = lo == hi;
   if (ok) {
     st = af;
-    th = f;
+    th = hi;
   }
   return ok;
 }
