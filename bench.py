@@ -292,6 +292,33 @@ def bench_rounds(args, cfg, rank, world, local, pg):
     dev_s = max_over_ranks(pg, ev0.elapsed_time(ev1) / 1e3, local)
     edges_all = sum_over_ranks(pg, edges, local)
     algo_all = sum_over_ranks(pg, algo, local)
+
+    e2e = None
+    if not args.no_e2e:  # the next K rounds with every bucket streamed from pinned host memory
+        import paper_2505_09258_b200 as lgd
+        host = lgd.PinnedArray((t.num_edges, 3), np.uint32)
+        t.bucketed_edges(host.array)
+        t.set_host_edges(host.array)
+        e, r, moves = cur.next()  # one warm-up round through the host path
+        mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+        barrier(pg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_edges = h2d = d2h = 0
+        for _ in range(args.steps):
+            e, r, moves = cur.next()
+            res = mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+            e_edges += res.edges_trained
+            h2d += res.h2d_bytes
+            d2h += res.d2h_bytes
+        torch.cuda.synchronize()
+        barrier(pg)
+        wall = max_over_ranks(pg, time.perf_counter() - t0, local)
+        t.set_host_edges(None)
+        host.free()
+        e2e = {"value": sum_over_ranks(pg, e_edges, local) / wall, "unit": "edges/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(pg, h2d, local)) // args.steps,
+               "d2h_bytes_per_step": int(sum_over_ranks(pg, d2h, local)) // args.steps}
     hbm, peak_kind = peaks()
     dom = "update"
     dstat = stats[dom]
@@ -320,7 +347,7 @@ def bench_rounds(args, cfg, rank, world, local, pg):
                          "traffic": (traffic_from_profiles() or {}).get(dom),
                          "step_achieved": algo_all / dev_s / 1e9 / world,
                          "step_frac": algo_all / dev_s / 1e9 / world / hbm},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     t.close()

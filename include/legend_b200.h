@@ -176,6 +176,11 @@ int lgd_train_buckets(lgd_context* ctx, uint32_t epoch, uint64_t g_begin, uint64
 int lgd_train_buckets_from_host(lgd_context* ctx, uint32_t epoch, uint64_t g_begin,
                                 uint64_t g_end, const uint32_t* host_bucketed_edges,
                                 lgd_epoch_result* out);
+/* Registers (or, with NULL, clears) a host copy of the edge list in bucket
+ * order: lgd_train_buckets, lgd_train_items and the lock-step rounds then copy
+ * every bucket H2D from it (the end-to-end path) instead of reading the
+ * device-resident copy.  The memory must stay valid while registered. */
+int lgd_set_host_edges(lgd_context* ctx, const uint32_t* host_bucketed_edges);
 /* The edge list in bucket order (edge_order applied), num_edges records. */
 int lgd_get_bucketed_edges(lgd_context* ctx, uint32_t* edges_out);
 /* Pinned host memory for the E||S blobs and edge lists. */

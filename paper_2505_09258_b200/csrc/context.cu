@@ -129,6 +129,11 @@ struct lgd_context {
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
+  // optional host copy of the bucket-ordered edges (lgd_set_host_edges): the
+  // bucket lists and rounds then stream every bucket H2D instead of reading
+  // the device copy
+  const uint32_t* host_edges = nullptr;
+  uint64_t round_h2d = 0;
   double score_bytes_total = 0.0;  // algorithmic score-phase bytes since the call began
 
   ~lgd_context() {
@@ -634,6 +639,7 @@ struct lgd_context {
 
   void train_range(uint32_t epoch, uint64_t g_begin, uint64_t g_end, lgd_epoch_result* out,
                    const uint32_t* host_bucketed = nullptr) {
+    if (!host_bucketed) host_bucketed = host_edges;
     check_ready();
     train_items(epoch, plan_items(g_begin, g_end), out, host_bucketed);
   }
@@ -667,6 +673,7 @@ struct lgd_context {
     round_epoch = epoch;
     round_prepared = ~size_t(0);
     round_nb = round_edges = round_buckets = 0;
+    round_h2d = 0;
     score_bytes_total = 0.0;
     LGD_CUDA(cudaMemsetAsync(counters.get(), 0, 2 * sizeof(unsigned long long), stream));
     LGD_CUDA(cudaEventRecord(ev_begin, stream));
@@ -686,7 +693,15 @@ struct lgd_context {
       uint64_t off;
       const uint64_t m = bucket_size(it, &off);
       if (round_prepared != i) {
-        prepare_bucket(it, round_epoch, edges_bucketed.get() + 3 * off, m, nullptr);
+        const uint32_t* src = edges_bucketed.get() + 3 * off;
+        if (host_edges) {  // this step's bucket from host memory
+          staging[0].reserve(max_bucket() * 3);
+          LGD_CUDA(cudaMemcpyAsync(staging[0].get(), host_edges + 3 * off, m * 12,
+                                   cudaMemcpyHostToDevice, stream));
+          src = staging[0].get();
+          round_h2d += m * 12;
+        }
+        prepare_bucket(it, round_epoch, src, m, nullptr);
         sample_bucket(it, round_epoch, m, nullptr);
         round_prepared = i;
         round_edges += m;
@@ -712,7 +727,7 @@ struct lgd_context {
   }
 
   void round_end(lgd_epoch_result* out) {
-    fill_result(out, round_nb, round_edges, round_buckets, 0, round_t0);
+    fill_result(out, round_nb, round_edges, round_buckets, round_h2d, round_t0);
   }
 
   // Operator-level batch on host inputs (validated like batch_loss,
@@ -1182,7 +1197,7 @@ int lgd_train_items(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* ite
     if (!ctx || (!items && count)) throw std::invalid_argument("null argument");
     if (!ctx->partitioned) throw std::invalid_argument("no partition plan");
     DeviceGuard g(ctx->device);
-    ctx->train_items(epoch, work_items(ctx, items, count), out);
+    ctx->train_items(epoch, work_items(ctx, items, count), out, ctx->host_edges);
   });
 }
 
@@ -1239,6 +1254,13 @@ int lgd_train_buckets_from_host(lgd_context* ctx, uint32_t epoch, uint64_t g_beg
     if (!ctx || !host_bucketed_edges) throw std::invalid_argument("null argument");
     DeviceGuard g(ctx->device);
     ctx->train_range(epoch, g_begin, g_end, out, host_bucketed_edges);
+  });
+}
+
+int lgd_set_host_edges(lgd_context* ctx, const uint32_t* host_bucketed_edges) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->host_edges = host_bucketed_edges;
   });
 }
 

@@ -99,6 +99,7 @@ def library():
         "lgd_train_buckets_from_host": (i32, [vp, u32, u64, u64, vp, vp]),
         "lgd_round_schedule": (i32, [u32, u64, vp, vp, vp, vp]),
         "lgd_train_items": (i32, [vp, u32, vp, u64, vp]),
+        "lgd_set_host_edges": (i32, [vp, vp]),
         "lgd_round_begin": (i32, [vp, u32, vp, u64, vp]),
         "lgd_round_step": (i32, [vp, u64, vp]),
         "lgd_round_apply_relations": (i32, [vp, vp]),
@@ -490,6 +491,13 @@ class Trainer:
         _check(library().lgd_train_buckets_from_host(self._h, epoch, g_begin, g_end,
                                                      _p(host_bucketed), C.byref(r)))
         return EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
+
+    def set_host_edges(self, host_bucketed=None):
+        """Stream every bucket H2D from this host copy of the bucket-ordered
+        edges (None: back to the device-resident copy); keep it alive."""
+        self._host_edges = host_bucketed
+        _check(library().lgd_set_host_edges(self._h, _p(host_bucketed) if host_bucketed is not None
+                                            else None))
 
     def bucketed_edges(self, out=None):
         """The edge list in bucket order (into `out`, e.g. a PinnedArray view)."""
