@@ -470,12 +470,8 @@ __device__ __forceinline__ float* row_state(const BatchArgs& a, uint32_t r) {
 }
 
 // adagrad_update (train.cpp:342-354): a = acc + g^2 (FP64), acc = f32(a),
-// theta = f32(theta - lr g / (sqrt(a) + eps)).  When lr*g is a (signed) zero
-// the quotient is that same signed zero, so it is used directly: IEEE double
-// division and sqrt of zero take CUDA's slow path, and idle lanes (d < 32
-// vectors) would otherwise send every warp through it.  Bit-identical to the
-// reference for all inputs.
-__device__ __forceinline__ double opaque_sel(bool p, double a, double b);
+// theta = f32(theta - lr g / (sqrt(a) + eps)), bit-identical through the
+// certified fast path of adagrad.cuh (exact fallback otherwise).
 __device__ __forceinline__ void adagrad_fast(double gi, float& th, float& st, double lr,
                                              double eps) {
   if (!adagrad_try_fast(gi, th, st, lr, eps)) adagrad_exact(gi, th, st, lr, eps);
@@ -767,24 +763,8 @@ struct Lanes {
   }
 };
 
-// A select the compiler cannot see through: keeps "sqrt(z ? 1 : a)" from
-// being rewritten into "z ? 1 : sqrt(a)", which would still run sqrt(0).
-__device__ __forceinline__ double opaque_sel(bool p, double a, double b) {
-  double r;
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
-      : "=d"(r)
-      : "d"(a), "d"(b), "r"((unsigned)p));
-  return r;
-}
-
-// adagrad_update (train.cpp:342-354) with the inline (fast-path) IEEE
-// division and square root; a zero quotient (lr*g == +-0) is selected, never
-// divided, since zero operands take CUDA's slow path.  Bit-identical.
-
-// adagrad_update (train.cpp:342-354) on the lane's elements: only vectors
-// the lane owns run it (an idle lane's zero gradient would otherwise send the
-// warp through the IEEE slow path of 0 / x and sqrt(0)); a genuinely zero
-// gradient is exact through that slow path.
+// adagrad_update (train.cpp:342-354) on the lane's elements (adagrad.cuh):
+// only the vectors the lane owns run it.
 template <int KIND, int NV>
 __device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const double* acc,
                                               float* th, float* st, double lr, double eps) {
