@@ -2,28 +2,31 @@
 // adagrad_step (train.cpp:217-363) as
 //
 //   K3 score_kernel    warp per positive.  The 2+k+t embedding rows land in
-//                      shared memory by TMA bulk copies (cp.async.bulk, one
-//                      per row, mbarrier-tracked), double buffered, with the
-//                      row ids fetched two positives ahead.  Lane j computes
+//                      the warp's shared memory by TMA bulk copies
+//                      (cp.async.bulk, one per row, mbarrier-tracked), the
+//                      next positive's row ids fetched ahead.  Lane j computes
 //                      the dot product of negative j (lane k: the positive)
-//                      sequentially over the dimension -- the reference's
-//                      own FP64 summation order (train.cpp:246-264) -- then
-//                      the softmax weights, the loss and mix = sum_j w_j neg_j
-//                      - dst (train.cpp:306-323) in the reference order.
+//                      sequentially over the dimension -- the reference's own
+//                      FP64 summation order (train.cpp:246-264) -- then the
+//                      softmax weights, the loss and mix = sum_j w_j neg_j -
+//                      dst (train.cpp:306-323) in the reference order.
 //   sort               CUB onesweep radix sort of the P(k+2) contribution
-//                      node ids.  Stable, so every node's contributions stay
-//                      in the reference's std::map visit order (positive
-//                      ascending; dst, negatives j ascending, src).
-//   K4 segment_pass1   warp per 32 sorted contributions.  The chunk's pieces
-//                      (node segments cut at chunk edges) are processed four
-//                      at a time, one 8-lane group each, in lockstep: the
-//                      contributions are summed in order in FP64 and complete
-//                      segments get their Adagrad row update (train.cpp:
-//                      342-354) right away -- a sort-by-node segmented
-//                      reduction, no atomics on rows.
-//   K4 segment_pass2   segments that cross chunks (hubs) are finished by one
-//                      block each from the per-chunk partial sums.
+//                      keys (pool indices).  Stable, so every node's
+//                      contributions stay in the reference's std::map visit
+//                      order (positive ascending; dst, negatives j, src).
+//   K4 segment_pass1   warp per 32 sorted contributions; the chunk's pieces
+//     (_vec)           (node segments cut at chunk edges) one after another,
+//                      lanes over 16-byte vectors of the row.  The theta /
+//                      state rows of the next four pieces are in flight in a
+//                      per-warp shared-memory ring (cp.async); contributions
+//                      are summed in order in FP64 and finished segments get
+//                      their Adagrad row update (adagrad.cuh) right away -- a
+//                      sort-by-node segmented reduction, no atomics on rows.
+//   K4 segment_pass2   segments that run past a chunk and its 32-item
+//                      lookahead (hubs) are finished by one block each from
+//                      the per-chunk partial sums, in a fixed order.
 //   relation path      the same segmented reduction over relation ids.
+//   shared negatives   shared.cu (tcgen05) replaces K3; the update is K4.
 // FP64 expressions are compiled with -fmad=false so products and sums round
 // exactly like the reference's unfused x86-64 double arithmetic.
 #include <cub/device/device_radix_sort.cuh>
