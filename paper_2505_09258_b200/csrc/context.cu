@@ -117,6 +117,14 @@ struct lgd_context {
   DevBuf<unsigned long long> counters;
   DevBuf<double> batch_losses;
   DevBuf<uint32_t> op_edges, op_negs;  // operator-level uploads
+  // relation pass on the side stream (train.cuh: BatchArgs::side)
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_scored = nullptr, ev_rel = nullptr;
+  DevBuf<uint32_t> r_skeys, r_svals, r_span_list;
+  DevBuf<unsigned char> r_sort_temp;
+  DevBuf<double> r_part_first, r_part_last, r_grad;
+  DevBuf<uint8_t> r_chunk_flags, r_touched;
+  DevBuf<unsigned int> r_span_count;
 
   // profiling
   bool profiling = false;
@@ -143,6 +151,9 @@ struct lgd_context {
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (ev_scored) cudaEventDestroy(ev_scored);
+    if (ev_rel) cudaEventDestroy(ev_rel);
     for (auto e : {copy_done[0], copy_done[1], stage_free[0], stage_free[1]})
       if (e) cudaEventDestroy(e);
   }
@@ -226,6 +237,19 @@ struct lgd_context {
       for (uint64_t i = 0; i < items; ++i) h[i] = (uint32_t)i;
       LGD_CUDA(cudaMemcpy(iota.get(), h.data(), items * 4, cudaMemcpyHostToDevice));
     }
+    if (typed()) {
+      const uint64_t rchunks = (P + 31) / 32;
+      r_skeys.reserve(P);
+      r_svals.reserve(P);
+      r_sort_temp.reserve(batch_sort_temp_bytes(P));
+      r_part_first.reserve(rchunks * dim);
+      r_part_last.reserve(rchunks * dim);
+      r_chunk_flags.reserve(rchunks);
+      r_span_list.reserve(rchunks);
+      r_span_count.reserve(1);
+      r_grad.reserve(std::max<uint64_t>(R, 1) * dim);
+      r_touched.reserve(std::max<uint64_t>(R, 1));
+    }
     batch_cap = P;
     k_cap = kk;
   }
@@ -287,6 +311,23 @@ struct lgd_context {
     }
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
+    if (typed() && R && side_stream && r_grad.get()) {  // overlapped relation pass
+      a.side = side_stream;
+      a.ev_scored = ev_scored;
+      a.ev_rel = ev_rel;
+      a.num_rels = R;
+      a.rel_skeys = r_skeys.get();
+      a.rel_svals = r_svals.get();
+      a.rel_sort_temp = r_sort_temp.get();
+      a.rel_sort_temp_bytes = r_sort_temp.bytes();
+      a.rel_part_first = r_part_first.get();
+      a.rel_part_last = r_part_last.get();
+      a.rel_chunk_flags = r_chunk_flags.get();
+      a.rel_span_list = r_span_list.get();
+      a.rel_span_count = r_span_count.get();
+      a.rel_grad = r_grad.get();
+      a.rel_touched = r_touched.get();
+    }
     if (chunk()) {
       const SharedShape sh = shared_shape(dim, a.k, chunk(), P);
       a.chunk = chunk();
@@ -379,6 +420,7 @@ struct lgd_context {
     if (rel_grad_out) {  // lock-step rounds: relation gradient only, applied later
       a.grad_rels = rel_grad_out;
       a.grad_rel_flag = rel_flag_out;
+      a.side = nullptr;  // the caller applies relation gradients itself
     }
     if (profiling) {
       const int slot = prof_slot(1);
@@ -798,6 +840,9 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       LGD_CUDA(cudaEventCreate(&c->ev_begin));
       LGD_CUDA(cudaEventCreate(&c->ev_end));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+      LGD_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+      LGD_CUDA(cudaEventCreateWithFlags(&c->ev_scored, cudaEventDisableTiming));
+      LGD_CUDA(cudaEventCreateWithFlags(&c->ev_rel, cudaEventDisableTiming));
       for (auto* e : {&c->copy_done[0], &c->copy_done[1], &c->stage_free[0], &c->stage_free[1]})
         LGD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
       c->pos.reserve(1);
@@ -1311,6 +1356,7 @@ int lgd_train_batch(lgd_context* ctx, const uint32_t* edges, uint64_t num_positi
       a.grad_node_flag = fn.get();
       a.grad_rels = gr.get();
       a.grad_rel_flag = fr.get();
+      a.side = nullptr;
     }
     launch_train_batch(a, ctx->stream, nullptr);
     ctx->launches += ctx->batch_launches();
@@ -1349,6 +1395,7 @@ int lgd_batch_gradients(lgd_context* ctx, const uint32_t* edges, uint64_t num_po
     a.grad_node_flag = fn.get();
     a.grad_rels = gr.get();
     a.grad_rel_flag = fr.get();
+    a.side = nullptr;
     launch_train_batch(a, ctx->stream, nullptr);
     std::vector<uint8_t> hf(V), hrf(R);
     std::vector<double> hg(V * d), hr(R * d);

@@ -1223,6 +1223,60 @@ void run_segments(const BatchArgs& a, uint64_t items, bool rel, cudaStream_t st)
   LGD_LAUNCH_CHECK();
 }
 
+__global__ void rel_apply_dense_kernel(const double* __restrict__ grad,
+                                       const uint8_t* __restrict__ touched, float* __restrict__ th,
+                                       float* __restrict__ st, uint64_t R, uint32_t d, double lr,
+                                       double eps) {
+  const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= R || !touched[r]) return;
+  for (uint32_t i = lane; i < d; i += 32) {
+    float tv = th[r * d + i], sv = st[r * d + i];
+    adagrad_fast(grad[r * d + i], tv, sv, lr, eps);
+    th[r * d + i] = tv;
+    st[r * d + i] = sv;
+  }
+}
+
+// Relation pass, part 1: sort + segmented sums.  With a side stream it
+// starts as soon as K3 is done and overlaps the node pass, writing dense
+// gradients; rel_pass_finish then applies them after K4.
+template <int KIND, int NC>
+void rel_pass_start(const BatchArgs& a, cudaStream_t st) {
+  if (KIND == 0) return;
+  if (!a.side) {
+    sort_items(a, a.P, a.rel_keys, a.iota, a.rel_key_bits, st);
+    run_segments<KIND, NC>(a, a.P, true, st);
+    return;
+  }
+  LGD_CUDA(cudaEventRecord(a.ev_scored, st));
+  LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_scored, 0));
+  BatchArgs r = a;
+  r.skeys = a.rel_skeys;
+  r.svals = a.rel_svals;
+  r.sort_temp = a.rel_sort_temp;
+  r.sort_temp_bytes = a.rel_sort_temp_bytes;
+  r.part_first = a.rel_part_first;
+  r.part_last = a.rel_part_last;
+  r.chunk_flags = a.rel_chunk_flags;
+  r.span_list = a.rel_span_list;
+  r.span_count = a.rel_span_count;
+  r.grad_rels = a.rel_grad;
+  r.grad_rel_flag = a.rel_touched;
+  LGD_CUDA(cudaMemsetAsync(a.rel_touched, 0, a.num_rels, a.side));
+  sort_items(r, a.P, a.rel_keys, a.iota, a.rel_key_bits, a.side);
+  run_segments<KIND, NC>(r, a.P, true, a.side);
+  LGD_CUDA(cudaEventRecord(a.ev_rel, a.side));
+}
+template <int KIND>
+void rel_pass_finish(const BatchArgs& a, cudaStream_t st) {
+  if (KIND == 0 || !a.side) return;
+  LGD_CUDA(cudaStreamWaitEvent(st, a.ev_rel, 0));
+  rel_apply_dense_kernel<<<ceil_div(a.num_rels * 32, 256), 256, 0, st>>>(
+      a.rel_grad, a.rel_touched, a.rel_theta, a.rel_state, a.num_rels, a.dim, a.lr, a.eps);
+  LGD_LAUNCH_CHECK();
+}
+
 template <int KIND, int NC>
 void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   auto rec = [&](int i) {
@@ -1261,13 +1315,15 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
   LGD_LAUNCH_CHECK();
   rec(1);
+  if (a.side) rel_pass_start<KIND, NC>(a, st);
   sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
   rec(2);
   run_segments<KIND, NC>(a, P * (k + 2), false, st);
   rec(3);
-  if (KIND != 0) {
-    sort_items(a, P, a.rel_keys, a.iota, a.rel_key_bits, st);
-    run_segments<KIND, NC>(a, P, true, st);
+  if (a.side) {
+    rel_pass_finish<KIND>(a, st);
+  } else {
+    rel_pass_start<KIND, NC>(a, st);
   }
   rec(4);
 }
@@ -1286,6 +1342,7 @@ void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev
   loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
   LGD_LAUNCH_CHECK();
   rec(1);
+  if (a.side) rel_pass_start<KIND, NC>(a, st);
   BatchArgs b = a;  // node items: (index << 2) | slot, slot 0 dst, 1 negative, 2 src
   b.k = 1;
   b.slot_bits = 2;
@@ -1295,9 +1352,10 @@ void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev
   rec(2);
   run_segments_shared<KIND>(b, items, st);
   rec(3);
-  if (KIND != 0) {
-    sort_items(a, P, a.rel_keys, a.iota, a.rel_key_bits, st);
-    run_segments<KIND, NC>(a, P, true, st);
+  if (a.side) {
+    rel_pass_finish<KIND>(a, st);
+  } else {
+    rel_pass_start<KIND, NC>(a, st);
   }
   rec(4);
 }

@@ -69,6 +69,24 @@ struct BatchArgs {
   float* sh_rowinv;
   double* sh_pos;             // P positive scores (FP64)
   float* sh_G;                // nch x kpad x dim: gradient of every shared negative
+  // relation pass on a side stream (typed models, updating batches): it needs
+  // only K3's outputs, so its sort and segmented sums overlap the node pass;
+  // the relation rows are updated after K4, which reads them pre-update.
+  // side == nullptr: sequential relation pass.
+  cudaStream_t side;
+  cudaEvent_t ev_scored, ev_rel;
+  uint64_t num_rels;
+  uint32_t* rel_skeys;
+  uint32_t* rel_svals;
+  void* rel_sort_temp;
+  size_t rel_sort_temp_bytes;
+  double* rel_part_first;
+  double* rel_part_last;
+  uint8_t* rel_chunk_flags;
+  uint32_t* rel_span_list;
+  unsigned int* rel_span_count;
+  double* rel_grad;           // R x dim, rows written for touched relations
+  uint8_t* rel_touched;       // R
 };
 
 struct SharedShape {
