@@ -1251,6 +1251,10 @@ void rel_pass_start(const BatchArgs& a, cudaStream_t st) {
   }
   LGD_CUDA(cudaEventRecord(a.ev_scored, st));
   LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_scored, 0));
+  // the batch loss is off the critical path too (K4 does not need it; the
+  // next batch's K3 waits for ev_rel before it rewrites the per-positive losses)
+  loss_reduce_kernel<<<1, 1024, 0, a.side>>>(a.loss, a.P, a.batch_loss_out);
+  LGD_LAUNCH_CHECK();
   BatchArgs r = a;
   r.skeys = a.rel_skeys;
   r.svals = a.rel_svals;
@@ -1312,8 +1316,10 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
     score_kernel<KIND><<<grid, kScoreWarps * 32, smem, st>>>(a, tma);
     LGD_LAUNCH_CHECK();
   }
-  loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
-  LGD_LAUNCH_CHECK();
+  if (!(KIND != 0 && a.side)) {
+    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
+    LGD_LAUNCH_CHECK();
+  }
   rec(1);
   if (a.side) rel_pass_start<KIND, NC>(a, st);
   sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
@@ -1339,8 +1345,10 @@ void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev
   const uint64_t P = a.P;
   rec(0);
   launch_shared_scores(a, st);
-  loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
-  LGD_LAUNCH_CHECK();
+  if (!(KIND != 0 && a.side)) {
+    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
+    LGD_LAUNCH_CHECK();
+  }
   rec(1);
   if (a.side) rel_pass_start<KIND, NC>(a, st);
   BatchArgs b = a;  // node items: (index << 2) | slot, slot 0 dst, 1 negative, 2 src
