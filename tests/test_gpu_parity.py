@@ -388,3 +388,30 @@ def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world):
     if Rm:
         rEg, rSg = trainers[0].get_relations()
         assert_tables_close(rEg, rE, "relE")
+
+
+# ------------------------------------------------ host-streamed bucket input
+def test_host_edges_path_matches_device_path():
+    """lgd_set_host_edges / train_buckets_from_host stream each bucket H2D; the
+    trained tables and losses equal the device-resident path bit for bit."""
+    rng = np.random.default_rng(8)
+    V, R, d, Ecnt, n = 3000, 6, 32, 60000, 4
+    edges = np.stack([rng.integers(0, V, Ecnt), rng.integers(0, R, Ecnt),
+                      rng.integers(0, V, Ecnt)], 1).astype(np.uint32)
+    a = make_trainer("distmult", d, V, R, edges, n, k=8, batch=4000)
+    b = make_trainer("distmult", d, V, R, edges, n, k=8, batch=4000)
+    a.init_store(3)
+    b.init_store(3)
+    ra = a.run_epoch(0)
+    host = lgd.PinnedArray((b.num_edges, 3), np.uint32)
+    b.bucketed_edges(host.array)
+    b.set_host_edges(host.array)
+    rb = b.run_epoch(0)
+    b.set_host_edges(None)
+    host.free()
+    assert rb.loss_sum == ra.loss_sum and rb.edges_trained == ra.edges_trained
+    assert rb.h2d_bytes == 12 * Ecnt
+    Ea, Sa = a.tables()
+    Eb, Sb = b.tables()
+    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    assert np.array_equal(a.get_relations()[0], b.get_relations()[0])
