@@ -191,7 +191,9 @@ __device__ __forceinline__ void write_core_layouts(const float* tile, uint32_t t
 }
 
 // IR1 (TF32) of 64 padded tile rows, the positive score in FP64, snap = the
-// src row, the dst / src contribution items and the relation key.
+// src row, the dst / src contribution items and the relation key.  Warp w
+// fills rows 8w .. 8w + 7: their edges are fetched lane-parallel, then every
+// row is read with 16-byte (ComplEx: 8-byte re / im pair) loads.
 template <int KIND>
 __global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
   extern __shared__ __align__(16) float ptile[];
@@ -199,35 +201,76 @@ __global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t rows_per_chunk = (uint64_t)a.tpc * 128;
   const uint64_t row0 = (uint64_t)blockIdx.x * kPrepRows;
-  for (int rr = warp; rr < kPrepRows; rr += 8) {
-    const uint64_t row = row0 + rr;
+  // lane i < 8: row 8 warp + i
+  uint32_t es = 0, er = 0, et = 0;
+  uint64_t ep = 0;
+  bool ev = false;
+  if (lane < 8) {
+    const uint64_t row = row0 + warp * 8 + lane;
     const uint64_t c = row / rows_per_chunk, r = row - c * rows_per_chunk;
-    const uint64_t p = c * C + r;
+    ep = c * C + r;
+    ev = r < C && ep < a.P;
+    if (ev) {
+      es = a.edges[3 * ep];
+      er = a.edges[3 * ep + 1];
+      et = a.edges[3 * ep + 2];
+    }
+  }
+  const uint32_t vmask = __ballot_sync(0xffffffffu, ev);
+#pragma unroll 2
+  for (int i = 0; i < 8; ++i) {
+    const int rr = warp * 8 + i;
     float* trow = ptile + rr * ts;
-    if (!(r < C && p < a.P)) {
-      for (uint32_t i = lane; i < dp; i += 32) trow[i] = 0.f;
+    if (!((vmask >> i) & 1u)) {
+      for (uint32_t e = lane; e < dp; e += 32) trow[e] = 0.f;
       continue;
     }
-    const uint32_t s = a.edges[3 * p], rel = a.edges[3 * p + 1], t = a.edges[3 * p + 2];
+    const uint32_t s = __shfl_sync(0xffffffffu, es, i);
+    const uint32_t rel = __shfl_sync(0xffffffffu, er, i);
+    const uint32_t t = __shfl_sync(0xffffffffu, et, i);
+    const uint64_t p = __shfl_sync(0xffffffffu, ep, i);
     const float* srow = a.theta + (size_t)s * d;
     const float* rrow = KIND != 0 ? a.rel_theta + (size_t)rel * d : nullptr;
     const float* drow = a.theta + (size_t)t * d;
     double pos = 0.0;
-    for (uint32_t i = lane; i < dp; i += 32) {
-      double x = 0.0;
-      if (i < d) {
-        if (KIND == 2) {
-          const uint32_t j = i < h ? i : i - h;
-          const double sr = srow[j], si = srow[j + h], qr = rrow[j], qi = rrow[j + h];
-          x = i < h ? sr * qr - si * qi : sr * qi + si * qr;
-        } else {
-          x = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
-        }
-        pos += x * (double)drow[i];
-        a.snap[p * d + i] = srow[i];
+    if (KIND == 2) {  // lane l: real indices 2l, 2l + 1 and their imaginary partners
+      if (2 * (uint32_t)lane < h) {
+        const uint32_t j = 2 * lane;
+        const float2 sr = *reinterpret_cast<const float2*>(srow + j);
+        const float2 si = *reinterpret_cast<const float2*>(srow + j + h);
+        const float2 qr = *reinterpret_cast<const float2*>(rrow + j);
+        const float2 qi = *reinterpret_cast<const float2*>(rrow + j + h);
+        const float2 dr = *reinterpret_cast<const float2*>(drow + j);
+        const float2 di = *reinterpret_cast<const float2*>(drow + j + h);
+        const double xr0 = (double)sr.x * qr.x - (double)si.x * qi.x;
+        const double xr1 = (double)sr.y * qr.y - (double)si.y * qi.y;
+        const double xi0 = (double)sr.x * qi.x + (double)si.x * qr.x;
+        const double xi1 = (double)sr.y * qi.y + (double)si.y * qr.y;
+        pos = xr0 * dr.x + xr1 * dr.y + xi0 * di.x + xi1 * di.y;
+        *reinterpret_cast<float2*>(a.snap + p * d + j) = sr;
+        *reinterpret_cast<float2*>(a.snap + p * d + j + h) = si;
+        trow[j] = to_tf32((float)xr0);
+        trow[j + 1] = to_tf32((float)xr1);
+        trow[j + h] = to_tf32((float)xi0);
+        trow[j + h + 1] = to_tf32((float)xi1);
       }
-      trow[i] = to_tf32((float)x);
+    } else if (4 * (uint32_t)lane < d) {  // lane l: elements 4l .. 4l + 3
+      const uint32_t e = 4 * lane;
+      const float4 sv = *reinterpret_cast<const float4*>(srow + e);
+      const float4 dv = *reinterpret_cast<const float4*>(drow + e);
+      float4 qv = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (KIND != 0) qv = *reinterpret_cast<const float4*>(rrow + e);
+      const double x0 = KIND == 0 ? (double)sv.x : (double)sv.x * qv.x;
+      const double x1 = KIND == 0 ? (double)sv.y : (double)sv.y * qv.y;
+      const double x2 = KIND == 0 ? (double)sv.z : (double)sv.z * qv.z;
+      const double x3 = KIND == 0 ? (double)sv.w : (double)sv.w * qv.w;
+      pos = x0 * dv.x + x1 * dv.y + x2 * dv.z + x3 * dv.w;
+      *reinterpret_cast<float4*>(a.snap + p * d + e) = sv;
+      *reinterpret_cast<float4*>(trow + e) =
+          make_float4(to_tf32((float)x0), to_tf32((float)x1), to_tf32((float)x2),
+                      to_tf32((float)x3));
     }
+    for (uint32_t e = d + lane; e < dp; e += 32) trow[e] = 0.f;
 #pragma unroll
     for (int off = 16; off; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
     if (lane == 0) {
@@ -245,29 +288,44 @@ __global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
 }
 
 // TF32 rows of 64 padded negative slots (chunk, j < kpad) and, for j < k,
-// the negatives' contribution items.
+// the negatives' contribution items (16-byte loads, ids lane-parallel).
 __global__ void __launch_bounds__(256) shared_gather_kernel(BatchArgs a) {
   extern __shared__ __align__(16) float ptile[];
   const uint32_t d = a.dim, dp = a.dpad, k = a.k, kp = a.kpad, ts = dp + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t slot0 = (uint64_t)blockIdx.x * kPrepRows;
-  for (int rr = warp; rr < kPrepRows; rr += 8) {
-    const uint64_t slot = slot0 + rr;
-    const uint64_t c = slot / kp;
-    const uint32_t j = (uint32_t)(slot - c * kp);
-    float* trow = ptile + rr * ts;
-    if (j >= k) {
-      for (uint32_t i = lane; i < dp; i += 32) trow[i] = 0.f;
+  uint32_t myid = 0;
+  bool mv = false;
+  uint64_t mc = 0;
+  uint32_t mj = 0;
+  if (lane < 8) {
+    const uint64_t slot = slot0 + warp * 8 + lane;
+    mc = slot / kp;
+    mj = (uint32_t)(slot - mc * kp);
+    mv = mj < k;
+    if (mv) myid = a.negs[mc * k + mj];
+  }
+  const uint32_t vmask = __ballot_sync(0xffffffffu, mv);
+#pragma unroll 4
+  for (int i = 0; i < 8; ++i) {
+    float* trow = ptile + (warp * 8 + i) * ts;
+    if (!((vmask >> i) & 1u)) {
+      for (uint32_t e = lane; e < dp; e += 32) trow[e] = 0.f;
       continue;
     }
-    const uint32_t id = a.negs[c * k + j];
+    const uint32_t id = __shfl_sync(0xffffffffu, myid, i);
     const float* row = a.theta + (size_t)id * d;
-    for (uint32_t i = lane; i < dp; i += 32) trow[i] = i < d ? to_tf32(row[i]) : 0.f;
-    if (lane == 0) {
-      const uint64_t item = 2 * a.P + c * k + j;
-      a.node_keys[item] = pool_index(a, id);
-      a.node_vals[item] = (uint32_t)((c * kp + j) << 2) | 1u;  // slot 1: shared negative
+    if (4 * (uint32_t)lane < d) {
+      const float4 v = *reinterpret_cast<const float4*>(row + 4 * lane);
+      *reinterpret_cast<float4*>(trow + 4 * lane) =
+          make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
     }
+    for (uint32_t e = d + lane; e < dp; e += 32) trow[e] = 0.f;
+  }
+  if (lane < 8 && mv) {
+    const uint64_t item = 2 * a.P + mc * k + mj;
+    a.node_keys[item] = pool_index(a, myid);
+    a.node_vals[item] = (uint32_t)((mc * kp + mj) << 2) | 1u;  // slot 1: shared negative
   }
   __syncthreads();
   write_core_layouts(ptile, ts, dp, reinterpret_cast<unsigned char*>(a.sh_B) + slot0 * dp * 4,
