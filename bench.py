@@ -153,8 +153,9 @@ def sum_over_ranks(pg, value, local):
 # ------------------------------------------------------------ CPU reference
 def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
     """Time the reference CPU trainer on a bounded sample: the first state's
-    resident partitions {0,1,2} (initialised exactly like the store), bucket
-    (0,1)'s edges, `steps` consecutive batches of `batch` positives."""
+    resident partitions {0,1,2} (all of them when n < 3; initialised exactly
+    like the store), bucket (0,1)'s edges (bucket 0 when n = 1), `steps`
+    consecutive batches of `batch` positives."""
     from oracle.oracle import Oracle, available
     kind = "reference" if (which != "port" and available("reference")) else "restatement"
     o = Oracle(kind)
@@ -171,7 +172,7 @@ def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
     if R:
         lo.init_rows(lo.derive_seed(SEED, 0x52454C53), R, d, rE)
     rS = np.zeros_like(rE)
-    first = [0, stride, 2 * stride]
+    first = [f for f in (0, stride, 2 * stride) if f < V_loc]  # n < 3: fewer partitions
     count = [min(stride, V_loc - f) for f in first]
     stream = lo.derive_seed(SEED, 0x62756B74, 0, 0)
     m = min(len(bucket_edges), steps * batch)
@@ -182,7 +183,9 @@ def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
     dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "edges/s", "cores": 1, "host_cores": os.cpu_count(),
             "kind": "reference" if kind == "reference" else "port",
-            "sample": (f"state {{0,1,2}} resident ({V_loc:,} rows), bucket (0,1): shuffle of "
+            "sample": (f"state {{{','.join(str(f // stride) for f in first)}}} resident "
+                       f"({V_loc:,} rows), bucket {'(0,1)' if len(first) > 1 else '(0,0)'}: "
+                       f"shuffle of "
                        f"{m:,} edges then {steps} batch(es) of {batch:,} positives, "
                        f"{cfg['model']} d={d} k={K_NEG}; {done:,} edges in {dt:.1f} s"),
             "seconds": dt, "edges": done}
@@ -398,28 +401,34 @@ def main():
     t_setup = time.perf_counter()
     t = setup_trainer(cfg, local, args.negatives, args.shared_chunk)
     G = cfg["n"] ** 2
-    # weak scaling: rank r trains its own K consecutive buckets of the plan
-    # (tables replicated per GPU)
-    g0 = args.warmup + rank * args.steps
-    if g0 + args.steps > G:
-        g0 = max(0, G - args.steps)
-    warm_lo = max(0, g0 - args.warmup)
+    # a step is one bucket of the plan; unit i is bucket i % G of epoch i // G
+    # (small plans wrap into the next epochs).  Weak scaling: rank r trains its
+    # own K consecutive units (tables replicated per GPU).
+    u0 = args.warmup + rank * args.steps
+    units = [(i // G, i % G) for i in range(u0, u0 + args.steps)]
     setup_s = time.perf_counter() - t_setup
 
-    t.train_buckets(0, warm_lo, g0)  # warm-up buckets (untimed)
+    for i in range(u0 - args.warmup, u0):  # warm-up buckets (untimed)
+        t.train_buckets(i // G, i % G, i % G + 1)
     t.reset_kernel_stats()
     t.set_profiling(True)
     clocks = Clocks(local)
     clocks.start()
     barrier(pg)
     t.synchronize()
-    res = t.train_buckets(0, g0, g0 + args.steps)
+    parts = [t.train_buckets(e, g, g + 1) for e, g in units]
     t.synchronize()
     barrier(pg)
     clk = clocks.stop()
     launches = t.launch_count()
     stats = t.kernel_stats()
     t.set_profiling(False)
+
+    class _Sum:  # the timed units as one EpochResult-like record
+        pass
+    res = _Sum()
+    for f in ("device_ms", "edges_trained", "algorithmic_bytes", "batches", "unique_nodes"):
+        setattr(res, f, sum(getattr(r, f) for r in parts))
 
     dev_s = max_over_ranks(pg, res.device_ms / 1e3, local)
     edges_all = sum_over_ranks(pg, res.edges_trained, local)
@@ -447,13 +456,13 @@ def main():
     if not args.no_e2e:
         host = lgd.PinnedArray((t.num_edges, 3), np.uint32)
         t.bucketed_edges(host.array)
-        for g in range(warm_lo, g0):  # warm-up calls through the same host path (untimed)
-            t.train_buckets_from_host(1, g, g + 1, host.array)
+        for i in range(u0 - args.warmup, u0):  # warm-up calls through the host path (untimed)
+            t.train_buckets_from_host(1 + i // G, i % G, i % G + 1, host.array)
         barrier(pg)
         t0 = time.perf_counter()
         h2d = d2h = 0
-        for g in range(g0, g0 + args.steps):  # per step: H2D edges, train, D2H losses
-            r = t.train_buckets_from_host(1, g, g + 1, host.array)
+        for e, g in units:  # per step: H2D edges, train, D2H losses (the next epoch's streams)
+            r = t.train_buckets_from_host(1 + e, g, g + 1, host.array)
             h2d += r.h2d_bytes
             d2h += r.d2h_bytes
         wall = time.perf_counter() - t0
@@ -502,7 +511,8 @@ def main():
                        "batch_size": BATCH, "storage": "f32 (E||S), FP64 arithmetic",
                        "graph": f"power-law alpha={ALPHA}, generator seed {GRAPH_SEED}",
                        "step": "one bucket of the reference iteration plan",
-                       "buckets_timed": [g0, g0 + args.steps],
+                       "buckets_timed": [[e, g] for e, g in units][:4] + (
+                           [["..."]] if len(units) > 4 else []),
                        "edges_per_rank": res.edges_trained, "batches": res.batches,
                        "unique_rows_per_batch": res.unique_nodes / max(res.batches, 1),
                        "l2": (f"inputs larger than L2 ({8 * cfg['nodes'] * cfg['dim'] / 1e9:.1f} GB "
