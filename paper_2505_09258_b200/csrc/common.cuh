@@ -30,6 +30,15 @@ constexpr int kWarp = 32;
 
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// Kernel attributes (dynamic shared memory limits) are per device: the
+// launch helpers cache what they set per device ordinal.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  LGD_CUDA(cudaGetDevice(&d));
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
+
 inline int bits_for(uint64_t max_value) {  // bits needed to represent values <= max_value
   int b = 0;
   while (b < 64 && (max_value >> b)) ++b;

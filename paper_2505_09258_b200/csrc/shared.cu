@@ -981,10 +981,11 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   const size_t gsl = (size_t)kGradSlice * dp * 4;
   const uint32_t nbuf3 = t + 3 * gsl <= 227 * 1024 ? 2 : 1;
   const size_t sm3 = t + (nbuf3 + 1) * gsl;
-  static size_t set1 = 0, set2 = 0, set3 = 0;  // attributes only grow
-  if (sm1 > set1) set_smem(sg1_stats_kernel, set1 = sm1);
-  if (sm2 > set2) set_smem(sg2_mix_kernel, set2 = sm2);
-  if (sm3 > set3) set_smem(sg3_grad_kernel, set3 = sm3);
+  static size_t set1[kMaxDevices], set2[kMaxDevices], set3[kMaxDevices];  // grow only
+  const int dev = current_device();
+  if (sm1 > set1[dev]) set_smem(sg1_stats_kernel, set1[dev] = sm1);
+  if (sm2 > set2[dev]) set_smem(sg2_mix_kernel, set2[dev] = sm2);
+  if (sm3 > set3[dev]) set_smem(sg3_grad_kernel, set3[dev] = sm3);
   const unsigned tiles = (unsigned)(a.nch * a.tpc);
   const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
   sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);

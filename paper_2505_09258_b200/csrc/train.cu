@@ -1126,9 +1126,9 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
 // ----------------------------------------------------------- dispatchers
 // score_kernel<KIND> is shared by every (dim, k): its dynamic-smem attribute
 // only grows; occupancy is cached per smem size.  (Host-side, per process.)
-size_t g_score_attr[4] = {0, 0, 0, 0};
-size_t g_score_occ_smem[4] = {0, 0, 0, 0};
-int g_score_occ[4] = {0, 0, 0, 0};
+size_t g_score_attr[kMaxDevices][4];
+size_t g_score_occ_smem[kMaxDevices][4];
+int g_score_occ[kMaxDevices][4];
 
 void sort_items(const BatchArgs& a, uint64_t items, const uint32_t* keys, const uint32_t* vals,
                 int key_bits, cudaStream_t st) {
@@ -1153,11 +1153,12 @@ int vec_width(uint32_t d) {
 template <int KIND, int NV, bool REL, bool SH = false>
 void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
   const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
-  static size_t attr = 0;  // per instantiation: grows only
-  if (smem > attr) {
+  static size_t attr[kMaxDevices];  // per instantiation and device: grows only
+  const int dev = current_device();
+  if (smem > attr[dev]) {
     LGD_CUDA(cudaFuncSetAttribute(segment_pass1_vec<KIND, NV, REL, SH>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+    attr[dev] = smem;
   }
   segment_pass1_vec<KIND, NV, REL, SH><<<grid, kSegThreads, smem, st>>>(
       a, items, a.skeys, a.svals, a.span_list, a.span_count);
@@ -1295,9 +1296,10 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
   {
     // the dynamic-smem attribute only ever grows (it is shared by every
     // dimension / k this kernel serves); occupancy is cached per smem size
-    size_t* attr_set = g_score_attr;
-    size_t* occ_smem = g_score_occ_smem;
-    int* occ_val = g_score_occ;
+    const int dev = current_device();
+    size_t* attr_set = g_score_attr[dev];
+    size_t* occ_smem = g_score_occ_smem[dev];
+    int* occ_val = g_score_occ[dev];
     if (smem > attr_set[KIND]) {
       LGD_CUDA(cudaFuncSetAttribute(score_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
