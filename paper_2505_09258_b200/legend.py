@@ -533,6 +533,12 @@ class Trainer:
         _check(library().lgd_round_step(self._h, step, ptr))
 
     def round_apply(self, summed):
+        """One relation Adagrad step from the summed [R x (d+1)] buffer.  The
+        trainer runs on its own CUDA stream: work torch queued on `summed`
+        (the NCCL all-reduce, a sum) is finished first."""
+        if getattr(summed, "is_cuda", False):
+            import torch
+            torch.cuda.current_stream(summed.device).synchronize()
         _check(library().lgd_round_apply_relations(self._h, C.c_void_p(summed.data_ptr())))
 
     def round_end(self) -> EpochResult:
@@ -546,13 +552,17 @@ class Trainer:
         return [x.value for x in ptrs]
 
     def partition_views(self, p):
-        """Zero-copy torch views (CUDA) of partition p's theta and state rows."""
+        """Zero-copy torch views (CUDA) of partition p's theta and state rows.
+        Trainer calls return with their stream drained; work torch queues on
+        these views (NCCL send / recv, copies) must be finished before the
+        next trainer call (multigpu.py synchronises after each exchange)."""
         import torch
         th, st, _, _ = self.device_tables()
         s = self.stride()
         a, b = s * p, min(s * (p + 1), self.num_nodes)
         d = self.model.dim
-        return [torch.as_tensor(_CudaArray(ptr + a * d * 4, ((b - a) * d,)), device="cuda")
+        return [torch.as_tensor(_CudaArray(ptr + a * d * 4, ((b - a) * d,)),
+                                device=f"cuda:{self.device}")
                 for ptr in (th, st)]
 
     def train_batch(self, edges, negatives, apply=True):

@@ -115,8 +115,16 @@ class DistComm:
         self.world = dist.get_world_size()
         self.device = device
 
+    def _drain(self, t=None):
+        # the trainer runs on its own stream: finish what torch queued first
+        dev = getattr(t, "device", None) if t is not None else self.device
+        if str(dev).startswith("cuda"):
+            import torch
+            torch.cuda.current_stream(dev).synchronize()
+
     def all_reduce_sum(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        self._drain(t)
 
     def all_reduce_max_int(self, v: int) -> int:
         import torch
@@ -135,6 +143,7 @@ class DistComm:
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+            self._drain()
 
 
 def run_epoch_distributed(trainer, sched: Schedule, epoch: int, comm, rel_buf=None):
@@ -176,9 +185,16 @@ def run_epoch_virtual(trainers, sched: Schedule, epoch: int, copy_partition, rel
     plan, owner = sched.handoffs()
     world = len(trainers)
     typed = trainers[0].typed
+
+    def drain():  # torch work on the trainers' memory (copies, sums) before they run
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+
     for r in range(sched.num_rounds):
         for p, src, dst in plan[r]:
             copy_partition(trainers[dst], trainers[src], p)
+        drain()
         mines = [sched.rank_items(r, q) for q in range(world)]
         if not typed:
             for q in range(world):
@@ -196,6 +212,7 @@ def run_epoch_virtual(trainers, sched: Schedule, epoch: int, copy_partition, rel
     for p, o in sorted(owner.items()):
         if o not in (None, 0):
             copy_partition(trainers[0], trainers[o], p)
+    drain()
 
 
 class RoundCursor:
