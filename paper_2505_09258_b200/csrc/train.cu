@@ -41,6 +41,11 @@ namespace {
 
 constexpr int kScoreWarps = 4;
 constexpr int kSegThreads = 256;
+// K4 blocks per SM: 4 (64 registers) -- the first contribution is read when
+// the piece is processed rather than prefetched, so 32 warps fit per SM
+#ifndef SEG_MINB
+#define SEG_MINB 4
+#endif
 constexpr int kSegDepth = 4;  // pieces whose theta / state rows are in flight per warp
 
 // Developer timeline of K4 warps (build with -DLGD_TRACE; not in the product .so)
@@ -901,7 +906,7 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
 }
 
 template <int KIND, int NV, bool REL, bool SH>
-__global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
+__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
     BatchArgs a, uint64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
   constexpr int NE = 4 * NV;
@@ -965,8 +970,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     auto rowof_at = [&](int s0) { return __shfl_sync(0xffffffffu, myrow, s0 & 31); };
     // theta / state rows of the next kSegDepth pieces are in flight at once:
     // cp.async into this warp's shared-memory ring (no registers held), one
-    // commit group per piece.  The first contribution of the next piece is
-    // prefetched in registers.
+    // commit group per piece.  A piece's first contribution is loaded when the
+    // piece is processed (no register prefetch: 64 registers, 32 warps per SM).
     extern __shared__ __align__(16) float seg_ring[];
     const uint32_t rowf = (a.dim + 3) & ~3u;
     const uint32_t slotf = 2 * rowf;  // slot: theta, state
@@ -989,10 +994,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
     };
 #pragma unroll
     for (int u = 0; u < kSegDepth; ++u) stage(t0 + u);
-    ItemRegs<NE> cit, nit;
     int cur = __ffs(rest) - 1;
     rest &= rest - 1;
-    load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
 #pragma unroll 1
     for (; t < np; ++t) {
       K4_TRACE(1);
@@ -1000,7 +1003,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
       const int nxt = has_next ? __ffs(rest) - 1 : nlive;
       rest &= rest - 1;
       const int pend = (t == np - 1 && ext_short) ? nlive + ext : nxt;
-      load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, nxt & 31), has_next, nit);
+      ItemRegs<NE> cit;
+      load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
       asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
       float th[NE], st[NE];
       const uint32_t slot = ring + (t % kSegDepth) * slotf * 4;
@@ -1033,7 +1037,6 @@ __global__ void __launch_bounds__(kSegThreads, 3) segment_pass1_vec(
         L.stf(state + (uint64_t)row * d, st);
       }
       stage(t + kSegDepth);  // the slot just read is free again
-      cit = nit;
       cur = nxt;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
