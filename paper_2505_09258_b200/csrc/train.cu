@@ -39,8 +39,14 @@ namespace lgd {
 
 namespace {
 
-constexpr int kScoreWarps = 4;
-constexpr int kSegThreads = 256;
+#ifndef SCORE_WARPS
+#define SCORE_WARPS 8
+#endif
+constexpr int kScoreWarps = SCORE_WARPS;
+#ifndef SEG_THREADS
+#define SEG_THREADS 256
+#endif
+constexpr int kSegThreads = SEG_THREADS;
 // K4 blocks per SM: 4 (64 registers) -- the first contribution is read when
 // the piece is processed rather than prefetched, so 32 warps fit per SM
 #ifndef SEG_MINB
