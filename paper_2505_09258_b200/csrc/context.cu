@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -137,6 +138,7 @@ struct lgd_context {
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
+  size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for the snapshot rows
   // optional host copy of the bucket-ordered edges (lgd_set_host_edges): the
   // bucket lists and rounds then stream every bucket H2D instead of reading
   // the device copy
@@ -252,6 +254,22 @@ struct lgd_context {
     }
     batch_cap = P;
     k_cap = kk;
+    pin_snapshot_in_l2();
+  }
+
+  // Every contribution of a positive reads its snapshot row (400 B at d = 100)
+  // at a scattered time during K4 while the theta / state rows stream through
+  // L2: a persisting access window keeps the snapshot on chip.
+  void pin_snapshot_in_l2() {
+    if (!l2_persist || !snap.get()) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = snap.get();
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(snap.bytes(), l2_window_max);
+    v.accessPolicyWindow.hitRatio =
+        (float)std::min(1.0, (double)l2_persist / (double)v.accessPolicyWindow.num_bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    LGD_CUDA(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v));
   }
 
   BatchArgs batch_args(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P,
@@ -837,6 +855,21 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       }
       LGD_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      {  // L2 set-aside for the snapshot rows (LGD_L2_PERSIST=0 disables)
+        int pmax = 0, wmax = 0;
+        cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        const char* env = std::getenv("LGD_L2_PERSIST");
+        const size_t want_mb = env ? std::strtoull(env, nullptr, 10) : 48;
+        if (want_mb && pmax > 0 && wmax > 0) {
+          const size_t want = std::min<size_t>((size_t)pmax, want_mb << 20);
+          if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+            c->l2_persist = want;
+            c->l2_window_max = (size_t)wmax;
+          }
+        }
+        cudaGetLastError();  // the set-aside is an optimisation only
+      }
       LGD_CUDA(cudaEventCreate(&c->ev_begin));
       LGD_CUDA(cudaEventCreate(&c->ev_end));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
