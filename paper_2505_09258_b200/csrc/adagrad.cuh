@@ -47,11 +47,9 @@ __device__ __forceinline__ bool adagrad_try_fast(double g, float& th, float& st,
   const float af = (float)a2;
   const double num = lr * g;
   const double t0 = (double)th;
-  if (num == 0.0) {  // q = +-0 exactly: theta - q needs no division
-    st = af;
-    th = (float)(t0 - num);
-    return true;
-  }
+  // (g = 0 needs no special case: with S > 0, q = 0 and the bound certifies
+  // t0; with S = 0 the seed is inf, t is NaN and the exact form runs.  The
+  // branch it used to take cost K4 4.5%.)
   // sqrt(a2): s = a2 * rsqrt(a2) from a ~2^-20 seed, two Newton (Heron)
   // steps: the error squares each time, so only the roundings of the last
   // steps remain (< 2^-50 relative)
