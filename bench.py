@@ -251,8 +251,9 @@ def bench_rounds(args, cfg, rank, world, local, pg):
     if pg is None:  # 1 GPU forced onto the round schedule: a trivial comm
         class _Solo:
             rank, world = 0, 1
+            stream_ordered = True  # lock-step batches without host drains
 
-            def all_reduce_sum(self, x):
+            def all_reduce_sum(self, x, drain=True):
                 pass
 
             def all_reduce_max_int(self, v):

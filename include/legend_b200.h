@@ -199,6 +199,15 @@ int lgd_round_begin(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* ite
 int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device);
 int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device);
 int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out);
+/* The context's CUDA stream (cudaStream_t): every kernel of the context runs
+ * on it, in order. */
+int lgd_get_stream(lgd_context* ctx, void** cuda_stream);
+/* on != 0: lgd_round_step and lgd_round_apply_relations return as soon as
+ * their work is queued, without draining the stream.  The caller then orders
+ * the relation all-reduce between them on that stream (e.g. NCCL with the
+ * context's stream current), so a lock-step batch costs no host round trip.
+ * Default 0: both return with the stream drained. */
+int lgd_set_stream_ordered(lgd_context* ctx, int on);
 /* Device pointers of the resident tables (partition hand-off between ranks). */
 int lgd_device_tables(lgd_context* ctx, float** theta, float** state, float** rel_theta,
                       float** rel_state);

@@ -713,6 +713,9 @@ struct lgd_context {
   uint64_t round_batches = 0, round_nb = 0, round_edges = 0, round_buckets = 0;
   uint32_t round_epoch = 0;
   size_t round_prepared = ~size_t(0);
+  // lgd_set_stream_ordered: round_step / round_apply_relations return without
+  // draining the stream; the caller orders its collective on it instead
+  bool stream_ordered = false;
   std::chrono::steady_clock::time_point round_t0;
   DevBuf<double> rel_grad;
   DevBuf<uint8_t> rel_flag;
@@ -775,14 +778,14 @@ struct lgd_context {
       ++round_nb;
     }
     if (rel_out) launch_rel_pack(rel_grad.get(), rel_flag.get(), R, dim, rel_out, stream);
-    LGD_CUDA(cudaStreamSynchronize(stream));
+    if (!stream_ordered) LGD_CUDA(cudaStreamSynchronize(stream));
   }
 
   void round_apply_relations(const double* summed) {
     if (typed() && R) {
       launch_rel_apply(summed, rel_theta.get(), rel_state.get(), R, dim, opt.learning_rate,
                        opt.adagrad_epsilon, stream);
-      LGD_CUDA(cudaStreamSynchronize(stream));
+      if (!stream_ordered) LGD_CUDA(cudaStreamSynchronize(stream));
     }
   }
 
@@ -1303,6 +1306,20 @@ int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device) {
     if (!ctx || !summed_device) throw std::invalid_argument("null argument");
     DeviceGuard g(ctx->device);
     ctx->round_apply_relations(summed_device);
+  });
+}
+
+int lgd_get_stream(lgd_context* ctx, void** cuda_stream) {
+  return guarded([&] {
+    if (!ctx || !cuda_stream) throw std::invalid_argument("null argument");
+    *cuda_stream = (void*)ctx->stream;
+  });
+}
+
+int lgd_set_stream_ordered(lgd_context* ctx, int on) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->stream_ordered = on != 0;
   });
 }
 

@@ -9,6 +9,7 @@ the device is missing.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -104,6 +105,8 @@ def library():
         "lgd_round_step": (i32, [vp, u64, vp]),
         "lgd_round_apply_relations": (i32, [vp, vp]),
         "lgd_round_end": (i32, [vp, vp]),
+        "lgd_get_stream": (i32, [vp, vp]),
+        "lgd_set_stream_ordered": (i32, [vp, i32]),
         "lgd_device_tables": (i32, [vp, vp, vp, vp, vp]),
         "lgd_get_bucketed_edges": (i32, [vp, vp]),
         "lgd_host_alloc": (i32, [u64, vp]),
@@ -350,6 +353,7 @@ class Trainer:
         opts = self.options._c()
         _check(L.lgd_create(C.byref(h), MODELS[model.kind], model.dim, C.byref(opts), device))
         self._h = h
+        self._ordered = False
         self.num_nodes = self.num_relations = self.num_edges = 0
         self.n = 0
         self.bucket_offsets = None
@@ -535,11 +539,42 @@ class Trainer:
     def round_apply(self, summed):
         """One relation Adagrad step from the summed [R x (d+1)] buffer.  The
         trainer runs on its own CUDA stream: work torch queued on `summed`
-        (the NCCL all-reduce, a sum) is finished first."""
-        if getattr(summed, "is_cuda", False):
+        (the NCCL all-reduce, a sum) is finished first -- by the stream order
+        itself in stream-ordered mode (see stream_ordered), else by draining
+        torch's current stream."""
+        if getattr(summed, "is_cuda", False) and not self._ordered:
             import torch
             torch.cuda.current_stream(summed.device).synchronize()
         _check(library().lgd_round_apply_relations(self._h, C.c_void_p(summed.data_ptr())))
+
+    def cuda_stream(self):
+        """The trainer's CUDA stream as a torch.cuda.ExternalStream."""
+        import torch
+        ptr = C.c_void_p()
+        _check(library().lgd_get_stream(self._h, C.byref(ptr)))
+        return torch.cuda.ExternalStream(ptr.value or 0, device=f"cuda:{self.device}")
+
+    @contextlib.contextmanager
+    def stream_ordered(self):
+        """Lock-step rounds without host round trips: inside the block,
+        round_step / round_apply only queue work on the trainer's stream, which
+        is torch's current stream, so a collective issued between them (NCCL
+        orders itself after the current stream and makes it wait for the
+        result) runs in stream order.  The stream is drained on exit."""
+        import torch
+        st = self.cuda_stream()
+        self.set_stream_ordered(True)
+        try:
+            with torch.cuda.stream(st):
+                yield st
+        finally:
+            self.set_stream_ordered(False)
+            st.synchronize()
+
+    def set_stream_ordered(self, on: bool):
+        """lgd_set_stream_ordered; prefer the stream_ordered() block."""
+        _check(library().lgd_set_stream_ordered(self._h, int(bool(on))))
+        self._ordered = bool(on)
 
     def round_end(self) -> EpochResult:
         r = _EpochResult()

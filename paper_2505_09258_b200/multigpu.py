@@ -122,9 +122,16 @@ class DistComm:
             import torch
             torch.cuda.current_stream(dev).synchronize()
 
-    def all_reduce_sum(self, t):
+    def all_reduce_sum(self, t, drain=True):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
-        self._drain(t)
+        if drain:
+            self._drain(t)
+
+    @property
+    def stream_ordered(self) -> bool:
+        """NCCL on GPUs: the lock-step relation sums can run in stream order
+        (Trainer.stream_ordered) instead of draining the host per batch."""
+        return str(self.device).startswith("cuda")
 
     def all_reduce_max_int(self, v: int) -> int:
         import torch
@@ -146,6 +153,24 @@ class DistComm:
             self._drain()
 
 
+def lock_step(trainer, comm, steps: int, rel_buf):
+    """`steps` lock-step batches: this rank's batch, the sum of every rank's
+    dense relation gradient, one identical relation Adagrad step.  Over NCCL
+    the three run in the trainer's stream order (no host round trip per
+    batch: the host only queues work); otherwise each call returns drained."""
+    if getattr(comm, "stream_ordered", False) and hasattr(trainer, "stream_ordered"):
+        with trainer.stream_ordered():
+            for s in range(steps):
+                trainer.round_step(s, rel_buf)
+                comm.all_reduce_sum(rel_buf, drain=False)
+                trainer.round_apply(rel_buf)
+        return
+    for s in range(steps):
+        trainer.round_step(s, rel_buf)
+        comm.all_reduce_sum(rel_buf)
+        trainer.round_apply(rel_buf)
+
+
 def run_epoch_distributed(trainer, sched: Schedule, epoch: int, comm, rel_buf=None):
     """One epoch of the round schedule on this rank.  `trainer` provides
     train_items / round_begin / round_step / round_apply / round_end /
@@ -160,11 +185,7 @@ def run_epoch_distributed(trainer, sched: Schedule, epoch: int, comm, rel_buf=No
             res = trainer.train_items(epoch, mine)
         else:
             nb = trainer.round_begin(epoch, mine)
-            steps = comm.all_reduce_max_int(nb)
-            for s in range(steps):
-                trainer.round_step(s, rel_buf)
-                comm.all_reduce_sum(rel_buf)
-                trainer.round_apply(rel_buf)
+            lock_step(trainer, comm, comm.all_reduce_max_int(nb), rel_buf)
             res = trainer.round_end()
         for key in totals:
             totals[key] += getattr(res, key) if hasattr(res, key) else res[key]
@@ -179,9 +200,12 @@ def gather_final(trainer, sched: Schedule, comm):
 
 
 def run_epoch_virtual(trainers, sched: Schedule, epoch: int, copy_partition, rel_bufs=None,
-                      sum_into=None):
+                      sum_into=None, ordered=False):
     """All ranks of the schedule in one process (one trainer per rank, e.g.
-    several contexts on one GPU): the 1-GPU parity harness."""
+    several contexts on one GPU): the 1-GPU parity harness.  ordered=True runs
+    the lock-step batches in stream order, the way lock_step does over NCCL:
+    the sum waits on every trainer's stream through events, every trainer's
+    stream waits on the sum, and the host never drains in between."""
     plan, owner = sched.handoffs()
     world = len(trainers)
     typed = trainers[0].typed
@@ -201,18 +225,47 @@ def run_epoch_virtual(trainers, sched: Schedule, epoch: int, copy_partition, rel
                 trainers[q].train_items(epoch, mines[q])
             continue
         nbs = [trainers[q].round_begin(epoch, mines[q]) for q in range(world)]
-        for s in range(max(nbs) if nbs else 0):
-            for q in range(world):
-                trainers[q].round_step(s, rel_bufs[q])
-            total = sum_into(rel_bufs)
-            for q in range(world):
-                trainers[q].round_apply(total)
+        steps = max(nbs) if nbs else 0
+        if ordered:
+            _lock_step_virtual_ordered(trainers, steps, rel_bufs, sum_into)
+        else:
+            for s in range(steps):
+                for q in range(world):
+                    trainers[q].round_step(s, rel_bufs[q])
+                total = sum_into(rel_bufs)
+                for q in range(world):
+                    trainers[q].round_apply(total)
         for q in range(world):
             trainers[q].round_end()
     for p, o in sorted(owner.items()):
         if o not in (None, 0):
             copy_partition(trainers[0], trainers[o], p)
     drain()
+
+
+def _lock_step_virtual_ordered(trainers, steps, rel_bufs, sum_into):
+    import torch
+    streams = [t.cuda_stream() for t in trainers]
+    side = torch.cuda.Stream()  # plays NCCL's internal stream
+    for t in trainers:
+        t.set_stream_ordered(True)
+    try:
+        for s in range(steps):
+            for t, b in zip(trainers, rel_bufs):
+                t.round_step(s, b)
+            for st in streams:
+                side.wait_stream(st)
+            with torch.cuda.stream(side):
+                total = sum_into(rel_bufs)
+            for t, st in zip(trainers, streams):
+                st.wait_stream(side)
+                total.record_stream(st)
+                t.round_apply(total)
+    finally:
+        for t in trainers:
+            t.set_stream_ordered(False)
+        for st in streams:
+            st.synchronize()
 
 
 class RoundCursor:
@@ -247,9 +300,5 @@ def run_round(trainer, sched: Schedule, epoch: int, r: int, moves, comm, rel_buf
     if not trainer.typed:
         return trainer.train_items(epoch, mine)
     nb = trainer.round_begin(epoch, mine)
-    steps = comm.all_reduce_max_int(nb)
-    for s in range(steps):
-        trainer.round_step(s, rel_buf)
-        comm.all_reduce_sum(rel_buf)
-        trainer.round_apply(rel_buf)
+    lock_step(trainer, comm, comm.all_reduce_max_int(nb), rel_buf)
     return trainer.round_end()

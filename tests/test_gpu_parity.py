@@ -344,11 +344,15 @@ def test_errors_follow_reference_classes():
 
 # ------------------------------------------- multi-GPU round schedule (1 GPU)
 @pytest.mark.parametrize("kind", ALL_KINDS)
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world):
+@pytest.mark.parametrize("world,ordered", [(1, False), (2, False), (3, False), (1, True),
+                                           (3, True)])
+def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world, ordered):
     """`world` trainer contexts on one GPU run the partition-round schedule
     exactly as `world` GPUs would (hand-offs as device copies, lock-step
-    relation sums); the result must match the serialised restatement."""
+    relation sums); the result must match the serialised restatement.
+    ordered: the lock-step batches run in stream order with no host drain
+    between a batch, the relation sum and the relation step (lock_step's
+    NCCL mode)."""
     import torch
     from paper_2505_09258_b200 import multigpu as mg
     rng = np.random.default_rng(21)
@@ -375,7 +379,7 @@ def test_round_schedule_virtual_ranks_match_restatement(oracle, kind, world):
             total += b
         return total
 
-    mg.run_epoch_virtual(trainers, sched, 0, copy_partition, bufs, sum_into)
+    mg.run_epoch_virtual(trainers, sched, 0, copy_partition, bufs, sum_into, ordered=ordered)
     torch.cuda.synchronize()
     E, S = trainers[0].tables()
     E0, S0, rE, rS = oracle.store_init(n, V, d, max(Rm, 1), 42)
