@@ -250,13 +250,30 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         ir1[j] = sr * rr - si * ri;
         ir1[j + h] = sr * ri + si * rr;
       }
-    } else if (KIND == 3) {  // TransE: u = s + r
-      for (uint32_t i = lane; i < d; i += 32) ir1[i] = (double)srow[i] + (double)rrow[i];
+      for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
+    } else if ((d & 3) == 0) {  // lane-owned float4 columns (TransE: u = s + r)
+      for (uint32_t i = 4 * lane; i < d; i += 128) {
+        const float4 sv = *reinterpret_cast<const float4*>(srow + i);
+        double u0 = sv.x, u1 = sv.y, u2 = sv.z, u3 = sv.w;
+        if (KIND != 0) {
+          const float4 rv = *reinterpret_cast<const float4*>(rrow + i);
+          if (KIND == 3) {
+            u0 += (double)rv.x, u1 += (double)rv.y, u2 += (double)rv.z, u3 += (double)rv.w;
+          } else {
+            u0 *= (double)rv.x, u1 *= (double)rv.y, u2 *= (double)rv.z, u3 *= (double)rv.w;
+          }
+        }
+        *reinterpret_cast<double2*>(ir1 + i) = make_double2(u0, u1);
+        *reinterpret_cast<double2*>(ir1 + i + 2) = make_double2(u2, u3);
+        *reinterpret_cast<float4*>(a.snap + p * d + i) = sv;
+      }
     } else {
       for (uint32_t i = lane; i < d; i += 32)
-        ir1[i] = KIND == 0 ? (double)srow[i] : (double)srow[i] * (double)rrow[i];
+        ir1[i] = KIND == 0   ? (double)srow[i]
+                 : KIND == 3 ? (double)srow[i] + (double)rrow[i]
+                             : (double)srow[i] * (double)rrow[i];
+      for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
     }
-    for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
     __syncwarp();
     // scores: lane q < k -> negative q, lane k -> the positive; sequential
     // over the dimension exactly as train.cpp:246-264
@@ -309,11 +326,31 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       const double cpos = dpos > 0.0 ? -1.0 / dpos : 0.0;
       if (lane == 0) a.w[a.P * k + p] = cpos;
       __syncwarp();
-      for (uint32_t i = lane; i < d; i += 32) {
-        const double u = ir1[i];
-        double mx = -(cpos * (u - (double)drow[i]));
-        for (uint32_t j = 0; j < k; ++j) mx -= ebuf[j] * (u - (double)R[(3 + j) * dpad + i]);
-        a.mix[p * d + i] = mx;
+      if ((d & 3) == 0) {  // lane-owned float4 columns: one pass for d <= 128
+        for (uint32_t i = 4 * lane; i < d; i += 128) {
+          const double2 u01 = *reinterpret_cast<const double2*>(ir1 + i);
+          const double2 u23 = *reinterpret_cast<const double2*>(ir1 + i + 2);
+          const float4 t = *reinterpret_cast<const float4*>(drow + i);
+          double m0 = -(cpos * (u01.x - (double)t.x)), m1 = -(cpos * (u01.y - (double)t.y));
+          double m2 = -(cpos * (u23.x - (double)t.z)), m3 = -(cpos * (u23.y - (double)t.w));
+          for (uint32_t j = 0; j < k; ++j) {
+            const double e = ebuf[j];
+            const float4 v = *reinterpret_cast<const float4*>(R + (3 + j) * dpad + i);
+            m0 -= e * (u01.x - (double)v.x);
+            m1 -= e * (u01.y - (double)v.y);
+            m2 -= e * (u23.x - (double)v.z);
+            m3 -= e * (u23.y - (double)v.w);
+          }
+          *reinterpret_cast<double2*>(a.mix + p * d + i) = make_double2(m0, m1);
+          *reinterpret_cast<double2*>(a.mix + p * d + i + 2) = make_double2(m2, m3);
+        }
+      } else {
+        for (uint32_t i = lane; i < d; i += 32) {
+          const double u = ir1[i];
+          double mx = -(cpos * (u - (double)drow[i]));
+          for (uint32_t j = 0; j < k; ++j) mx -= ebuf[j] * (u - (double)R[(3 + j) * dpad + i]);
+          a.mix[p * d + i] = mx;
+        }
       }
     } else {
       for (uint32_t j = lane; j < k; j += 32) {  // w_j = IR3_j / S as IR3_j * (1 / S)
@@ -322,10 +359,27 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       }
       __syncwarp();
       // mix = sum_j w_j neg_j - dst, j ascending (train.cpp:306-323)
-      for (uint32_t i = lane; i < d; i += 32) {
-        double mx = -(double)drow[i];
-        for (uint32_t j = 0; j < k; ++j) mx += ebuf[j] * (double)R[(3 + j) * dpad + i];
-        a.mix[p * d + i] = mx;
+      if ((d & 3) == 0) {  // lane-owned float4 columns: one pass for d <= 128
+        for (uint32_t i = 4 * lane; i < d; i += 128) {
+          const float4 t = *reinterpret_cast<const float4*>(drow + i);
+          double m0 = -(double)t.x, m1 = -(double)t.y, m2 = -(double)t.z, m3 = -(double)t.w;
+          for (uint32_t j = 0; j < k; ++j) {
+            const double e = ebuf[j];
+            const float4 v = *reinterpret_cast<const float4*>(R + (3 + j) * dpad + i);
+            m0 += e * (double)v.x;
+            m1 += e * (double)v.y;
+            m2 += e * (double)v.z;
+            m3 += e * (double)v.w;
+          }
+          *reinterpret_cast<double2*>(a.mix + p * d + i) = make_double2(m0, m1);
+          *reinterpret_cast<double2*>(a.mix + p * d + i + 2) = make_double2(m2, m3);
+        }
+      } else {
+        for (uint32_t i = lane; i < d; i += 32) {
+          double mx = -(double)drow[i];
+          for (uint32_t j = 0; j < k; ++j) mx += ebuf[j] * (double)R[(3 + j) * dpad + i];
+          a.mix[p * d + i] = mx;
+        }
       }
     }
     // contribution keys in the reference's visit order: dst, negatives, src
