@@ -968,7 +968,7 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
   }
 }
 
-template <int KIND, int NV, bool REL, bool SH>
+template <int KIND, int NV, bool REL, bool SH, bool GRAD>
 __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
     BatchArgs a, uint64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     uint32_t* __restrict__ span_list, unsigned int* __restrict__ span_count) {
@@ -985,7 +985,8 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
   constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
   float* __restrict__ theta = REL ? a.rel_theta : a.theta;
   float* __restrict__ state = REL ? a.rel_state : a.state;
-  double* gout = REL ? a.grad_rels : a.grad_nodes;
+  // GRAD: gradients out (lgd_batch_gradients, the relation side pass), no update
+  double* gout = GRAD ? (REL ? a.grad_rels : a.grad_nodes) : nullptr;
   const uint64_t d = a.dim;
   const double lr = a.lr, eps = a.eps;
   const uint64_t end = min(base + 32, n);
@@ -1043,20 +1044,20 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
     const int t0 = t;
     // piece starts still to stage / to process, lowest bit first
     uint32_t srest = rest;
-    auto stage = [&](int u) {
+    auto stage = [&](int u, uint32_t slot) {
       if (u < np) {
         const int s0 = __ffs(srest) - 1;
         srest &= srest - 1;
         const uint64_t off = (uint64_t)rowof_at(s0) * d;
         const bool fin = finishing(u) && !gout;
-        const uint32_t slot = ring + (u % kSegDepth) * slotf * 4;
         L.cpa_s(slot, theta + off, fin || kOwn);
         L.cpa_s(slot + rowf * 4, state + off, fin);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
-    for (int u = 0; u < kSegDepth; ++u) stage(t0 + u);
+    for (int u = 0; u < kSegDepth; ++u) stage(t0 + u, ring + u * slotf * 4);
+    uint32_t slot = ring;  // piece t's slot, restaged with piece t + kSegDepth
     int cur = __ffs(rest) - 1;
     rest &= rest - 1;
 #pragma unroll 1
@@ -1070,7 +1071,6 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
       load_item<KIND, NV, REL, SH>(x, L, __shfl_sync(0xffffffffu, val, cur), true, cit);
       asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
       float th[NE], st[NE];
-      const uint32_t slot = ring + (t % kSegDepth) * slotf * 4;
       L.lds_s(slot, th);
       L.lds_s(slot + rowf * 4, st);
       K4_TRACE(2 + 16 * (pend - cur));
@@ -1099,7 +1099,8 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
         L.stf(theta + (uint64_t)row * d, th);
         L.stf(state + (uint64_t)row * d, st);
       }
-      stage(t + kSegDepth);  // the slot just read is free again
+      stage(t + kSegDepth, slot);  // the slot just read is free again
+      slot = slot + slotf * 4 == ring + kSegDepth * slotf * 4 ? ring : slot + slotf * 4;
       cur = nxt;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1216,18 +1217,25 @@ int vec_width(uint32_t d) {
   return d <= 128 ? 1 : (d <= 256 ? 2 : 0);
 }
 
-template <int KIND, int NV, bool REL, bool SH = false>
-void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
+template <int KIND, int NV, bool REL, bool SH, bool GRAD>
+void launch_vec_pass1_(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
   const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
   static size_t attr[kMaxDevices];  // per instantiation and device: grows only
   const int dev = current_device();
   if (smem > attr[dev]) {
-    LGD_CUDA(cudaFuncSetAttribute(segment_pass1_vec<KIND, NV, REL, SH>,
+    LGD_CUDA(cudaFuncSetAttribute(segment_pass1_vec<KIND, NV, REL, SH, GRAD>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[dev] = smem;
   }
-  segment_pass1_vec<KIND, NV, REL, SH><<<grid, kSegThreads, smem, st>>>(
+  segment_pass1_vec<KIND, NV, REL, SH, GRAD><<<grid, kSegThreads, smem, st>>>(
       a, items, a.skeys, a.svals, a.span_list, a.span_count);
+}
+template <int KIND, int NV, bool REL, bool SH = false>
+void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStream_t st) {
+  if (REL ? a.grad_rels : a.grad_nodes)
+    launch_vec_pass1_<KIND, NV, REL, SH, true>(a, items, grid, st);
+  else
+    launch_vec_pass1_<KIND, NV, REL, SH, false>(a, items, grid, st);
 }
 
 // shared-negative mode: node items are dst / shared negative / src (slots 0-2)
