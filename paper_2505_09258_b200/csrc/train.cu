@@ -121,12 +121,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // ------------------------------------------------------- pool indices
-__device__ __forceinline__ uint32_t to_pool(const BatchArgs& a, uint32_t id) {
+// (pool ranges hold < 2^32 rows: 32-bit offsets; an id below a range's first
+// wraps to a large offset and fails the size test.  K3 of TransE keeps the
+// loop form, measured faster there through its register allocation.)
+__device__ __forceinline__ uint32_t to_pool_loop(const BatchArgs& a, uint32_t id) {
   uint64_t prev = 0;
   for (int i = 0; i < a.pool_n; ++i) {
     const uint64_t cnt = a.pool_end[i] - prev;
     if (id >= a.pool_first[i] && id - a.pool_first[i] < cnt) return (uint32_t)(prev + id - a.pool_first[i]);
     prev = a.pool_end[i];
+  }
+  return 0xffffffffu;
+}
+__device__ __forceinline__ uint32_t to_pool(const BatchArgs& a, uint32_t id) {
+  const uint32_t e0 = (uint32_t)a.pool_end[0];
+  const uint32_t o0 = id - (uint32_t)a.pool_first[0];
+  if (o0 < e0) return o0;
+  if (a.pool_n > 1) {
+    const uint32_t e1 = (uint32_t)a.pool_end[1];
+    const uint32_t o1 = id - (uint32_t)a.pool_first[1];
+    if (o1 < e1 - e0) return e0 + o1;
+    if (a.pool_n > 2) {
+      const uint32_t o2 = id - (uint32_t)a.pool_first[2];
+      if (o2 < (uint32_t)a.pool_end[2] - e1) return e1 + o2;
+    }
   }
   return 0xffffffffu;  // not resident (validated on the host)
 }
@@ -302,10 +320,23 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       fbuf[q] = f;
     }
     __syncwarp();
+    // std::max over the negatives' scores (train.cpp:262-264): for the
+    // non-NaN scores the max is order-free, so a butterfly over lanes gives
+    // the sequential fold's value
+    // (Dot and TransE keep the sequential fold: measured faster there, by
+    // their register allocation)
+    constexpr bool kFly = KIND == 1 || KIND == 2;
     double row_max = -INFINITY;
-    for (uint32_t j = 0; j < k; ++j) {
+    for (uint32_t j = kFly ? lane : 0; j < k; j += kFly ? 32 : 1) {
       const double f = fbuf[j];
-      row_max = row_max < f ? f : row_max;  // std::max(row_max, f)
+      row_max = row_max < f ? f : row_max;
+    }
+    if (kFly) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double f = __shfl_xor_sync(0xffffffffu, row_max, o);
+        row_max = row_max < f ? f : row_max;
+      }
     }
     for (uint32_t j = lane; j < k; j += 32) ebuf[j] = exp(fbuf[j] - row_max);  // IR3
     __syncwarp();
@@ -390,15 +421,15 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       const uint32_t pv = ((uint32_t)p << (a.slot_bits + a.rel_bits)) |
                           (a.rel_bits ? pid[1] << a.slot_bits : 0u);
       if (r == 0) {
-        a.node_keys[kb + k + 1] = to_pool(a, id);
+        a.node_keys[kb + k + 1] = KIND == 3 ? to_pool_loop(a, id) : to_pool(a, id);
         a.node_vals[kb + k + 1] = pv | (k + 1);
       } else if (r == 1) {
         if (typed) a.rel_keys[p] = id;
       } else if (r == 2) {
-        a.node_keys[kb] = to_pool(a, id);
+        a.node_keys[kb] = KIND == 3 ? to_pool_loop(a, id) : to_pool(a, id);
         a.node_vals[kb] = pv;
       } else {
-        a.node_keys[kb + (r - 2)] = to_pool(a, id);
+        a.node_keys[kb + (r - 2)] = KIND == 3 ? to_pool_loop(a, id) : to_pool(a, id);
         a.node_vals[kb + (r - 2)] = pv | (r - 2);
       }
     }
