@@ -220,7 +220,7 @@ struct lgd_context {
     }
     mix.reserve(P * dim);
     snap.reserve(P * dim);
-    loss.reserve(P);
+    loss.reserve(3 * P);  // K3's loss parts (loss_reduce takes the log)
     node_keys.reserve(items);
     node_vals.reserve(items);
     rel_keys.reserve(P);
@@ -291,6 +291,7 @@ struct lgd_context {
     a.mix = mix.get();
     a.snap = snap.get();
     a.loss = loss.get();
+    a.loss_parts = 0;  // run_batch turns them on where K3 writes them
     a.node_keys = node_keys.get();
     a.node_vals = node_vals.get();
     a.slot_bits = bits_for(a.k + 1);

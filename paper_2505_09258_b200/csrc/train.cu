@@ -343,7 +343,18 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
     double sum = 0.0;
     for (uint32_t j = 0; j < k; ++j) sum += ebuf[j];  // sequential j (train.cpp:266-270)
     const double inv_sum = 1.0 / sum;
-    if (lane == 0) a.loss[p] = -(fbuf[k] - (row_max + log(sum)));  // train.cpp:274
+    // loss = -(f_pos - (row_max + log(sum))), train.cpp:274.  With loss parts
+    // (DistMult / ComplEx with the side-stream relation pass: run_batch) the
+    // log runs lane-parallel in loss_reduce_kernel, off the critical path
+    if (lane == 0) {
+      if (!((KIND == 1 || KIND == 2) && a.loss_parts)) {
+        a.loss[p] = -(fbuf[k] - (row_max + log(sum)));
+      } else {
+        a.loss[p] = fbuf[k];
+        a.loss[a.P + p] = row_max;
+        a.loss[2 * a.P + p] = sum;
+      }
+    }
     if (KIND == 3) {
       // TransE coefficients (oracle lo_batch_ex): c_j = w_j / D_j, c_pos =
       // -1 / D_pos (0 at D = 0), stored where w lives (c_pos after P x k);
@@ -442,11 +453,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
 }
 
 // --------------------------------------------------------- loss reduction
+// parts: loss holds K3's f_pos | row_max | sum (3 x P) and the per-positive
+// loss -(f_pos - (row_max + log(sum))) (train.cpp:274) is formed here
 __global__ void __launch_bounds__(1024) loss_reduce_kernel(const double* __restrict__ loss,
-                                                           uint64_t P, double* out) {
+                                                           uint64_t P, double* out, int parts) {
   __shared__ double part[1024];
   double s = 0.0;
-  for (uint64_t i = threadIdx.x; i < P; i += 1024) s += loss[i];
+  for (uint64_t i = threadIdx.x; i < P; i += 1024)
+    s += parts ? -(loss[i] - (loss[P + i] + log(loss[2 * P + i]))) : loss[i];
   part[threadIdx.x] = s;
   __syncthreads();
   for (int w = 512; w; w >>= 1) {
@@ -1359,7 +1373,7 @@ void rel_pass_start(const BatchArgs& a, cudaStream_t st) {
   LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_scored, 0));
   // the batch loss is off the critical path too (K4 does not need it; the
   // next batch's K3 waits for ev_rel before it rewrites the per-positive losses)
-  loss_reduce_kernel<<<1, 1024, 0, a.side>>>(a.loss, a.P, a.batch_loss_out);
+  loss_reduce_kernel<<<1, 1024, 0, a.side>>>(a.loss, a.P, a.batch_loss_out, a.loss_parts);
   LGD_LAUNCH_CHECK();
   BatchArgs r = a;
   r.skeys = a.rel_skeys;
@@ -1388,7 +1402,9 @@ void rel_pass_finish(const BatchArgs& a, cudaStream_t st) {
 }
 
 template <int KIND, int NC>
-void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
+void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
+  BatchArgs a = a_in;
+  a.loss_parts = (KIND == 1 || KIND == 2) && a.side ? 1 : 0;
   auto rec = [&](int i) {
     if (ev && ev->enabled) LGD_CUDA(cudaEventRecord(ev->ev[i], st));
   };
@@ -1424,7 +1440,7 @@ void run_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev) {
     LGD_LAUNCH_CHECK();
   }
   if (!(KIND != 0 && a.side)) {
-    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
+    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out, a.loss_parts);
     LGD_LAUNCH_CHECK();
   }
   rec(1);
@@ -1453,7 +1469,7 @@ void run_batch_shared(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev
   rec(0);
   launch_shared_scores(a, st);
   if (!(KIND != 0 && a.side)) {
-    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out);
+    loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out, a.loss_parts);
     LGD_LAUNCH_CHECK();
   }
   rec(1);

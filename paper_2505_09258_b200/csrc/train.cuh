@@ -24,7 +24,9 @@ struct BatchArgs {
   double* w;                  // P x k softmax weights
   double* mix;                // P x d  sum_j w_j neg_j - dst
   float* snap;                // P x d  pre-update source rows
-  double* loss;               // P per-positive loss
+  double* loss;               // per-positive loss: P values (shared mode), or K3's
+                              // parts f_pos | row_max | sum (3 x P, loss_parts)
+  int loss_parts;
   uint32_t* node_keys;        // P x (k+2) contribution node ids (dst, negs, src)
   uint32_t* node_vals;        // P x (k+2) payloads (p << slot_bits) | slot
   uint32_t* rel_keys;         // P relation ids
