@@ -111,6 +111,16 @@ struct lgd_context {
   DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowmax, sn_rowinv, sn_G;
   DevBuf<double> sn_pos;
   DevBuf<uint32_t> node_keys, node_vals, rel_keys, iota, skeys, svals;
+  // bucket-level presort (presort_bucket): keys / payloads and their
+  // double-buffer partners; the batches of the bucket read runs of the result
+  DevBuf<uint32_t> bk_keys[2], bk_vals[2];
+  DevBuf<unsigned char> bk_temp;
+  bool presort = true;  // LGD_PRESORT=0 turns it off (per-batch sorts)
+  struct Presorted {
+    const uint32_t* keys = nullptr;
+    const uint32_t* vals = nullptr;
+    uint32_t mask = 0;
+  } bk;
   DevBuf<uint8_t> chunk_flags;
   DevBuf<uint32_t> span_list;
   DevBuf<unsigned int> span_count;
@@ -304,6 +314,8 @@ struct lgd_context {
       if (bits_for(P ? P - 1 : 0) + a.slot_bits + rb <= 32) a.rel_bits = rb;
     }
     a.rel_keys = rel_keys.get();
+    a.presorted = 0;
+    a.key_mask = 0xffffffffu;
     a.iota = iota.get();
     a.skeys = skeys.get();
     a.svals = svals.get();
@@ -410,10 +422,10 @@ struct lgd_context {
   void prof_drain(int slot) {
     cudaEvent_t* e = prof_ev(slot);
     const int kind = prof_pending[slot];
-    const int nint = kind == 1 ? 4 : 2;
+    const int nint = kind == 1 ? 4 : 3;
     LGD_CUDA(cudaEventSynchronize(e[nint]));
     const int batch_cls[4] = {LGD_KSTAT_SCORE, LGD_KSTAT_SORT, LGD_KSTAT_UPDATE, LGD_KSTAT_REL};
-    const int bucket_cls[2] = {LGD_KSTAT_SHUFFLE, LGD_KSTAT_SAMPLE};
+    const int bucket_cls[3] = {LGD_KSTAT_SHUFFLE, LGD_KSTAT_SAMPLE, LGD_KSTAT_SORT};
     for (int i = 0; i < nint; ++i) {
       const int cls = kind == 1 ? batch_cls[i] : bucket_cls[i];
       if (cls == LGD_KSTAT_REL && !typed()) continue;
@@ -433,8 +445,14 @@ struct lgd_context {
 
   void run_batch(const uint32_t* bedges, const uint32_t* bnegs, uint64_t P, double* loss_out,
                  const Pool* pool = nullptr, double* rel_grad_out = nullptr,
-                 uint8_t* rel_flag_out = nullptr) {
+                 uint8_t* rel_flag_out = nullptr, uint64_t bucket_item = ~uint64_t(0)) {
     BatchArgs a = batch_args(bedges, bnegs, P, loss_out, pool);
+    if (bk.keys && bucket_item != ~uint64_t(0)) {  // this batch's run of the bucket sort
+      a.presorted = 1;
+      a.key_mask = bk.mask;
+      a.skeys = const_cast<uint32_t*>(bk.keys) + bucket_item;
+      a.svals = const_cast<uint32_t*>(bk.vals) + bucket_item;
+    }
     score_bytes_total += score_bytes(P);
     if (rel_grad_out) {  // lock-step rounds: relation gradient only, applied later
       a.grad_rels = rel_grad_out;
@@ -455,6 +473,45 @@ struct lgd_context {
       launch_train_batch(a, stream, nullptr);
     }
     launches += batch_launches(a.node_key_bits);
+    if (a.presorted) launches -= 2 + (a.node_key_bits + 7) / 8;
+  }
+
+  // Bucket-level presort: every batch's node contributions keyed once as
+  // (batch << pool bits) | pool index and sorted in one radix sort over the
+  // bucket (train.cu: presort_keys_kernel).  The stable sort keeps each batch's
+  // contributions in K3's order, so batch b's run equals its own sort; one
+  // large sort runs near HBM speed where ~50 per-batch sorts of 1.8M items
+  // are launch- and lookback-bound.  Off (bk.keys = nullptr) for shared
+  // negatives, when the keys would not fit 32 bits, or when the relation id
+  // rides in the payload of some batches only.
+  void presort_bucket(const Pool& pool, uint64_t m, cudaEvent_t* bev) {
+    bk = Presorted{};
+    if (presort && !chunk() && m) {
+      const uint64_t B = opt.batch_size;
+      const BatchArgs a = batch_args(shuffled.get(), negs.get(), std::min(B, m), nullptr, &pool);
+      const uint64_t nb = (m + B - 1) / B;
+      const int bbits = bits_for(nb - 1);
+      const bool rel_ok = !(typed() && R) || a.rel_bits > 0;
+      if (rel_ok && a.node_key_bits + bbits <= 32) {
+        const uint64_t items = m * (k() + 2);
+        for (int i = 0; i < 2; ++i) {
+          bk_keys[i].reserve(items);
+          bk_vals[i].reserve(items);
+        }
+        const size_t tb = bucket_sort_temp_bytes(items);
+        if (bk_temp.bytes() < tb) bk_temp.reserve(tb);
+        launch_bucket_keys(a, m, B, bk_keys[0].get(), bk_vals[0].get(), stream);
+        uint32_t* kk[2] = {bk_keys[0].get(), bk_keys[1].get()};
+        uint32_t* vv[2] = {bk_vals[0].get(), bk_vals[1].get()};
+        const int sel = sort_bucket(bk_temp.get(), bk_temp.bytes(), kk, vv, items,
+                                    a.node_key_bits + bbits, stream);
+        bk.keys = kk[sel];
+        bk.vals = vv[sel];
+        bk.mask = a.node_key_bits >= 32 ? 0xffffffffu : (1u << a.node_key_bits) - 1u;
+        launches += 1 + 2 + (a.node_key_bits + bbits + 7) / 8;
+      }
+    }
+    if (bev) LGD_CUDA(cudaEventRecord(bev[3], stream));
   }
 
   // algorithmic bytes of the score phase: the edge record and
@@ -588,6 +645,14 @@ struct lgd_context {
     }
     ensure_bucket(max_m);
     ensure_batch(std::min<uint64_t>(opt.batch_size, std::max<uint64_t>(max_m, 1)));
+    if (presort && !chunk() && max_m) {  // bucket sort buffers, sized once
+      const uint64_t items = max_m * (k() + 2);
+      for (int i = 0; i < 2; ++i) {
+        bk_keys[i].reserve(items);
+        bk_vals[i].reserve(items);
+      }
+      bk_temp.reserve(bucket_sort_temp_bytes(items));
+    }
     batch_losses.reserve(std::max<uint64_t>(tb, 1));
     if (total_batches) *total_batches = tb;
   }
@@ -686,10 +751,11 @@ struct lgd_context {
         stage ^= 1;
       }
       sample_bucket(it, epoch, m, bev);
+      presort_bucket(it.pool, m, bev);
       for (uint64_t o = 0; o < m; o += opt.batch_size) {
         const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
         run_batch(shuffled.get() + 3 * o, negs.get() + (o / opt.batch_size) * batch_negs(opt.batch_size),
-                  P, batch_losses.get() + nb, &it.pool);
+                  P, batch_losses.get() + nb, &it.pool, nullptr, nullptr, o * (k() + 2));
         ++nb;
       }
       edges_trained += m;
@@ -767,6 +833,7 @@ struct lgd_context {
         }
         prepare_bucket(it, round_epoch, src, m, nullptr);
         sample_bucket(it, round_epoch, m, nullptr);
+        presort_bucket(it.pool, m, nullptr);
         round_prepared = i;
         round_edges += m;
         ++round_buckets;
@@ -775,7 +842,8 @@ struct lgd_context {
       const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
       run_batch(shuffled.get() + 3 * o, negs.get() + (o / opt.batch_size) * batch_negs(opt.batch_size),
                 P, batch_losses.get() + round_nb,
-                &it.pool, typed() ? rel_grad.get() : nullptr, typed() ? rel_flag.get() : nullptr);
+                &it.pool, typed() ? rel_grad.get() : nullptr, typed() ? rel_flag.get() : nullptr,
+                o * (k() + 2));
       ++round_nb;
     }
     if (rel_out) launch_rel_pack(rel_grad.get(), rel_flag.get(), R, dim, rel_out, stream);
@@ -874,6 +942,7 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
         }
         cudaGetLastError();  // the set-aside is an optimisation only
       }
+      if (const char* env = std::getenv("LGD_PRESORT")) c->presort = std::strtol(env, nullptr, 10) != 0;
       LGD_CUDA(cudaEventCreate(&c->ev_begin));
       LGD_CUDA(cudaEventCreate(&c->ev_end));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));

@@ -149,6 +149,7 @@ __device__ __forceinline__ uint32_t to_pool(const BatchArgs& a, uint32_t id) {
   return 0xffffffffu;  // not resident (validated on the host)
 }
 __device__ __forceinline__ uint32_t from_pool(const BatchArgs& a, uint32_t idx) {
+  idx &= a.key_mask;  // presorted keys carry the batch index above the pool index
   if (idx < a.pool_end[0]) return (uint32_t)(a.pool_first[0] + idx);
   if (a.pool_n > 1 && idx < a.pool_end[1]) return (uint32_t)(a.pool_first[1] + (idx - a.pool_end[0]));
   return (uint32_t)(a.pool_first[2] + (idx - a.pool_end[1]));
@@ -431,7 +432,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       // payload: positive, (relation,) slot
       const uint32_t pv = ((uint32_t)p << (a.slot_bits + a.rel_bits)) |
                           (a.rel_bits ? pid[1] << a.slot_bits : 0u);
-      if (r == 0) {
+      if (r != 1 && a.presorted) {
+        // keyed and sorted for the whole bucket already (presort_keys_kernel)
+      } else if (r == 0) {
         a.node_keys[kb + k + 1] = KIND == 3 ? to_pool_loop(a, id) : to_pool(a, id);
         a.node_vals[kb + k + 1] = pv | (k + 1);
       } else if (r == 1) {
@@ -1445,7 +1448,7 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   }
   rec(1);
   if (a.side) rel_pass_start<KIND, NC>(a, st);
-  sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
+  if (!a.presorted) sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
   rec(2);
   run_segments<KIND, NC>(a, P * (k + 2), false, st);
   rec(3);
@@ -1559,6 +1562,55 @@ size_t batch_sort_temp_bytes(uint64_t max_items) {
                                            (uint32_t*)nullptr, (int64_t)(max_items ? max_items : 1),
                                            0, 32));
   return bytes;
+}
+
+// Bucket-level contribution keys, item i = e (k + 2) + s of the bucket's
+// shuffled edge e (batch b = e / B, positive p = e - b B): s = 0 dst, 1..k
+// negative s - 1, k + 1 src -- K3's per-batch layout (kb + slot), so a stable
+// sort of (b, pool index) reproduces every batch's own sort.
+__global__ void presort_keys_kernel(BatchArgs a, uint64_t m, uint64_t B, uint32_t* __restrict__ keys,
+                                   uint32_t* __restrict__ vals) {
+  const uint32_t k = a.k, k2 = k + 2;
+  const uint64_t n = m * k2;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = i / k2;
+    const uint32_t s = (uint32_t)(i - e * k2);
+    const uint64_t b = e / B;
+    const uint32_t p = (uint32_t)(e - b * B);
+    const uint32_t id = s == 0 ? __ldg(a.edges + 3 * e + 2)
+                        : s == k + 1 ? __ldg(a.edges + 3 * e)
+                                     : __ldg(a.negs + e * k + (s - 1));
+    const uint32_t rel = a.rel_bits ? __ldg(a.edges + 3 * e + 1) << a.slot_bits : 0u;
+    keys[i] = ((uint32_t)b << a.node_key_bits) | to_pool(a, id);
+    vals[i] = ((uint32_t)p << (a.slot_bits + a.rel_bits)) | rel | s;
+  }
+}
+
+void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* keys,
+                        uint32_t* vals, cudaStream_t st) {
+  const uint64_t n = m * (a.k + 2);
+  if (!n) return;
+  const uint64_t blocks = ceil_div(n, 256);
+  const unsigned grid = (unsigned)(blocks < (uint64_t)a.sm_count * 16 ? blocks : (uint64_t)a.sm_count * 16);
+  presort_keys_kernel<<<grid, 256, 0, st>>>(a, m, B, keys, vals);
+  LGD_LAUNCH_CHECK();
+}
+
+size_t bucket_sort_temp_bytes(uint64_t max_items) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+  LGD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v,
+                                           (int64_t)(max_items ? max_items : 1), 0, 32));
+  return bytes;
+}
+
+int sort_bucket(void* temp, size_t temp_bytes, uint32_t* keys[2], uint32_t* vals[2],
+                uint64_t items, int key_bits, cudaStream_t st) {
+  cub::DoubleBuffer<uint32_t> k(keys[0], keys[1]), v(vals[0], vals[1]);
+  size_t bytes = temp_bytes;
+  LGD_CUDA(cub::DeviceRadixSort::SortPairs(temp, bytes, k, v, (int64_t)items, 0, key_bits, st));
+  return k.selector;
 }
 
 size_t score_smem_bytes(uint32_t dim, uint32_t k) { return ScoreSmem(dim, k).block_bytes(); }

@@ -30,6 +30,12 @@ struct BatchArgs {
   uint32_t* node_keys;        // P x (k+2) contribution node ids (dst, negs, src)
   uint32_t* node_vals;        // P x (k+2) payloads (p << slot_bits) | slot
   uint32_t* rel_keys;         // P relation ids
+  // presorted: the node contributions were keyed and sorted once for the whole
+  // bucket (launch_bucket_keys / sort_bucket): skeys / svals point at this
+  // batch's run of the bucket's sorted arrays, whose keys carry the batch
+  // index above key_mask; K3 writes no node keys and the batch sorts nothing
+  int presorted;
+  uint32_t key_mask;          // pool-index bits of a sorted key (all ones unless presorted)
   const uint32_t* iota;       // 0..P*(k+2)-1
   uint32_t* skeys;            // sorted keys
   uint32_t* svals;            // sorted contribution indices
@@ -106,6 +112,16 @@ struct BatchEvents {  // optional per-phase timing (profiling mode)
 };
 
 size_t batch_sort_temp_bytes(uint64_t max_items);
+// Bucket-level node contributions: keys (batch << node_key_bits) | pool index
+// and payloads of every batch of an m-edge bucket (batches of B positives;
+// a = the bucket's batch arguments), then one stable radix sort of them all.
+// The sorted run of batch b starts at item b * B * (k + 2) and equals the
+// per-batch sort of K3's keys.  Returns the buffer holding the result.
+void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* keys,
+                        uint32_t* vals, cudaStream_t st);
+size_t bucket_sort_temp_bytes(uint64_t max_items);
+int sort_bucket(void* temp, size_t temp_bytes, uint32_t* keys[2], uint32_t* vals[2],
+                uint64_t items, int key_bits, cudaStream_t st);
 size_t score_smem_bytes(uint32_t dim, uint32_t k);
 // K3 -> loss reduce -> sort -> K4 (pass 1, 2) -> relation path.
 void launch_train_batch(const BatchArgs& a, cudaStream_t st, const BatchEvents* ev);

@@ -419,3 +419,30 @@ def test_host_edges_path_matches_device_path():
     Eb, Sb = b.tables()
     assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
     assert np.array_equal(a.get_relations()[0], b.get_relations()[0])
+
+
+# --------------------------------------------------- bucket-level presort
+@pytest.mark.parametrize("kind", ALL_KINDS)
+def test_bucket_presort_matches_per_batch_sort(kind, monkeypatch):
+    """The bucket-level contribution sort (one radix sort of (batch, pool
+    index) keys per bucket) gives every batch the run its own sort would:
+    losses, counts and tables equal the per-batch-sort path bit for bit,
+    ragged last batches included."""
+    rng = np.random.default_rng(11)
+    V, R, d, Ecnt, n = 2500, 5, 16, 50000, 4
+    edges = np.stack([rng.integers(0, V, Ecnt), rng.integers(0, R, Ecnt),
+                      rng.integers(0, V, Ecnt)], 1).astype(np.uint32)
+    R = R if kind != "dot" else 0
+    runs = []
+    for presort in ("1", "0"):
+        monkeypatch.setenv("LGD_PRESORT", presort)
+        t = make_trainer(kind, d, V, R, edges, n, k=8, batch=700)
+        t.init_store(5)
+        res = t.run_epoch(0)
+        runs.append((res, t.tables(), t.get_relations() if R else None))
+    (ra, (Ea, Sa), rela), (rb, (Eb, Sb), relb) = runs
+    assert ra.loss_sum == rb.loss_sum and ra.batches == rb.batches
+    assert ra.unique_nodes == rb.unique_nodes and ra.unique_rels == rb.unique_rels
+    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    if R:
+        assert np.array_equal(rela[0], relb[0]) and np.array_equal(rela[1], relb[1])
