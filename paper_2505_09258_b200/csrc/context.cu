@@ -120,6 +120,7 @@ struct lgd_context {
     const uint32_t* keys = nullptr;
     const uint32_t* vals = nullptr;
     uint32_t mask = 0;
+    int rel_bits = 0;  // payload layout of the whole bucket
   } bk;
   DevBuf<uint8_t> chunk_flags;
   DevBuf<uint32_t> span_list;
@@ -358,6 +359,10 @@ struct lgd_context {
       a.rel_span_count = r_span_count.get();
       a.rel_grad = r_grad.get();
       a.rel_touched = r_touched.get();
+    } else if (!typed() && side_stream && !chunk()) {  // Dot: the loss reduction only
+      a.side = side_stream;
+      a.ev_scored = ev_scored;
+      a.ev_rel = ev_rel;
     }
     if (chunk()) {
       const SharedShape sh = shared_shape(dim, a.k, chunk(), P);
@@ -450,6 +455,7 @@ struct lgd_context {
     if (bk.keys && bucket_item != ~uint64_t(0)) {  // this batch's run of the bucket sort
       a.presorted = 1;
       a.key_mask = bk.mask;
+      a.rel_bits = bk.rel_bits;  // the payloads were written with the full batch's layout
       a.skeys = const_cast<uint32_t*>(bk.keys) + bucket_item;
       a.svals = const_cast<uint32_t*>(bk.vals) + bucket_item;
     }
@@ -482,8 +488,7 @@ struct lgd_context {
   // contributions in K3's order, so batch b's run equals its own sort; one
   // large sort runs near HBM speed where ~50 per-batch sorts of 1.8M items
   // are launch- and lookback-bound.  Off (bk.keys = nullptr) for shared
-  // negatives, when the keys would not fit 32 bits, or when the relation id
-  // rides in the payload of some batches only.
+  // negatives and when the keys would not fit 32 bits.
   void presort_bucket(const Pool& pool, uint64_t m, cudaEvent_t* bev) {
     bk = Presorted{};
     if (presort && !chunk() && m) {
@@ -491,8 +496,9 @@ struct lgd_context {
       const BatchArgs a = batch_args(shuffled.get(), negs.get(), std::min(B, m), nullptr, &pool);
       const uint64_t nb = (m + B - 1) / B;
       const int bbits = bits_for(nb - 1);
-      const bool rel_ok = !(typed() && R) || a.rel_bits > 0;
-      if (rel_ok && a.node_key_bits + bbits <= 32) {
+      // the relation id rides in the payload when it fits the full batch B
+      // (then also every smaller last batch); otherwise no batch carries it
+      if (a.node_key_bits + bbits <= 32) {
         const uint64_t items = m * (k() + 2);
         for (int i = 0; i < 2; ++i) {
           bk_keys[i].reserve(items);
@@ -508,6 +514,7 @@ struct lgd_context {
         bk.keys = kk[sel];
         bk.vals = vv[sel];
         bk.mask = a.node_key_bits >= 32 ? 0xffffffffu : (1u << a.node_key_bits) - 1u;
+        bk.rel_bits = a.rel_bits;
         launches += 1 + 2 + (a.node_key_bits + bbits + 7) / 8;
       }
     }
@@ -946,7 +953,13 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       LGD_CUDA(cudaEventCreate(&c->ev_begin));
       LGD_CUDA(cudaEventCreate(&c->ev_end));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-      LGD_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+      {  // the relation pass / loss reduction is small and overlaps K4, which
+         // fills every SM: at the highest priority its blocks are scheduled as
+         // soon as K4 blocks retire instead of after K4's whole grid
+        int lo = 0, hi = 0;
+        LGD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LGD_CUDA(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi));
+      }
       LGD_CUDA(cudaEventCreateWithFlags(&c->ev_scored, cudaEventDisableTiming));
       LGD_CUDA(cudaEventCreateWithFlags(&c->ev_rel, cudaEventDisableTiming));
       for (auto* e : {&c->copy_done[0], &c->copy_done[1], &c->stage_free[0], &c->stage_free[1]})

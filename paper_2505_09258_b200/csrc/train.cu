@@ -1442,7 +1442,13 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
     score_kernel<KIND><<<grid, kScoreWarps * 32, smem, st>>>(a, tma);
     LGD_LAUNCH_CHECK();
   }
-  if (!(KIND != 0 && a.side)) {
+  if (KIND == 0 && a.side) {  // Dot: the batch loss on the side stream, off K4's path
+    LGD_CUDA(cudaEventRecord(a.ev_scored, st));
+    LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_scored, 0));
+    loss_reduce_kernel<<<1, 1024, 0, a.side>>>(a.loss, P, a.batch_loss_out, a.loss_parts);
+    LGD_LAUNCH_CHECK();
+    LGD_CUDA(cudaEventRecord(a.ev_rel, a.side));
+  } else if (!(KIND != 0 && a.side)) {
     loss_reduce_kernel<<<1, 1024, 0, st>>>(a.loss, P, a.batch_loss_out, a.loss_parts);
     LGD_LAUNCH_CHECK();
   }
@@ -1452,7 +1458,10 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   rec(2);
   run_segments<KIND, NC>(a, P * (k + 2), false, st);
   rec(3);
-  if (a.side) {
+  if (KIND == 0 && a.side) {
+    // the next batch's K3 rewrites the per-positive losses
+    LGD_CUDA(cudaStreamWaitEvent(st, a.ev_rel, 0));
+  } else if (a.side) {
     rel_pass_finish<KIND>(a, st);
   } else {
     rel_pass_start<KIND, NC>(a, st);
