@@ -155,6 +155,16 @@ int lgd_round_schedule(uint32_t n, uint64_t capacity, uint64_t* count, lgd_bucke
 int lgd_init_store(lgd_context* ctx, uint64_t seed);
 int lgd_load_partition(lgd_context* ctx, uint32_t p, const float* e_s, uint64_t rows);
 int lgd_store_partition(lgd_context* ctx, uint32_t p, float* e_s, uint64_t rows);
+/* Asynchronous write-back of partition p into e_s (E then S, the layout above;
+ * pinned memory from lgd_host_alloc makes it truly asynchronous): the copy sees
+ * the tables as the work queued so far leaves them and overlaps whatever is
+ * queued next that only reads them (lgd_evaluate). Every later call that writes
+ * the tables orders itself after the pending copies; lgd_device_tables waits
+ * for them on the host. e_s must stay valid until lgd_wait_stores returns.
+ * Replaces the epoch-end partition writes of pipeline.cpp:173-193 /
+ * store.cpp:27-57 (EmbeddingStore::write_partition). */
+int lgd_store_partition_async(lgd_context* ctx, uint32_t p, float* e_s, uint64_t rows);
+int lgd_wait_stores(lgd_context* ctx);
 int lgd_set_relations(lgd_context* ctx, const float* e_s, uint64_t count);
 int lgd_get_relations(lgd_context* ctx, float* e_s, uint64_t count);
 

@@ -146,6 +146,12 @@ struct lgd_context {
   lgd_kernel_stats kstats[LGD_KSTAT_COUNT]{};
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   cudaStream_t copy_stream = nullptr;
+  // asynchronous partition write-back (lgd_store_partition_async): D2H copies
+  // on their own stream, ordered after the training stream's work so far;
+  // the next call that writes the tables first orders itself after them
+  cudaStream_t store_stream = nullptr;
+  cudaEvent_t ev_store_src = nullptr, ev_store_done = nullptr;
+  bool stores_pending = false;
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
@@ -159,6 +165,10 @@ struct lgd_context {
 
   ~lgd_context() {
     cudaSetDevice(device);
+    if (store_stream) cudaStreamSynchronize(store_stream);  // before the tables are freed
+    if (store_stream) cudaStreamDestroy(store_stream);
+    if (ev_store_src) cudaEventDestroy(ev_store_src);
+    if (ev_store_done) cudaEventDestroy(ev_store_done);
     if (stream) cudaStreamDestroy(stream);
     for (auto e : prof_events) cudaEventDestroy(e);
     if (ev_begin) cudaEventDestroy(ev_begin);
@@ -169,6 +179,19 @@ struct lgd_context {
     if (ev_rel) cudaEventDestroy(ev_rel);
     for (auto e : {copy_done[0], copy_done[1], stage_free[0], stage_free[1]})
       if (e) cudaEventDestroy(e);
+  }
+
+  // Orders every later launch on `stream` (the only stream that writes the
+  // tables) after the pending asynchronous write-backs.
+  void fence_stores() {
+    if (!stores_pending) return;
+    LGD_CUDA(cudaStreamWaitEvent(stream, ev_store_done, 0));
+    stores_pending = false;
+  }
+  // The same on the host, for writes that do not go through `stream`.
+  void wait_stores() {
+    if (store_stream) LGD_CUDA(cudaStreamSynchronize(store_stream));
+    stores_pending = false;
   }
 
   bool typed() const { return kind != LGD_MODEL_DOT; }
@@ -1213,6 +1236,7 @@ int lgd_init_store(lgd_context* ctx, uint64_t seed) {
     if (!ctx) throw std::invalid_argument("null context");
     if (!ctx->partitioned) throw std::invalid_argument("set a partition plan first");
     DeviceGuard g(ctx->device);
+    ctx->wait_stores();  // its copies do not run on the training stream
     const uint64_t V = ctx->V, d = ctx->dim;
     ctx->theta.reserve(V * d);
     ctx->state.reserve(V * d);
@@ -1251,6 +1275,7 @@ int lgd_load_partition(lgd_context* ctx, uint32_t p, const float* e_s, uint64_t 
     if (!ctx->partitioned || p >= ctx->n) throw std::invalid_argument("partition out of range");
     if (rows != ctx->part_rows(p)) throw std::invalid_argument("partition row count mismatch");
     DeviceGuard g(ctx->device);
+    ctx->wait_stores();  // its copies do not run on the training stream
     ensure_tables(ctx);
     const uint64_t off = ctx->part_begin(p) * ctx->dim, cnt = rows * ctx->dim;
     LGD_CUDA(cudaMemcpyAsync(ctx->theta.get() + off, e_s, cnt * 4, cudaMemcpyHostToDevice,
@@ -1278,12 +1303,46 @@ int lgd_store_partition(lgd_context* ctx, uint32_t p, float* e_s, uint64_t rows)
   });
 }
 
+int lgd_store_partition_async(lgd_context* ctx, uint32_t p, float* e_s, uint64_t rows) {
+  return guarded([&] {
+    if (!ctx || !e_s) throw std::invalid_argument("null argument");
+    if (!ctx->partitioned || p >= ctx->n) throw std::invalid_argument("partition out of range");
+    if (rows != ctx->part_rows(p)) throw std::invalid_argument("partition row count mismatch");
+    if (!ctx->tables_ready) throw std::invalid_argument("embedding store not initialised");
+    DeviceGuard g(ctx->device);
+    if (!ctx->store_stream) {
+      LGD_CUDA(cudaStreamCreateWithFlags(&ctx->store_stream, cudaStreamNonBlocking));
+      LGD_CUDA(cudaEventCreateWithFlags(&ctx->ev_store_src, cudaEventDisableTiming));
+      LGD_CUDA(cudaEventCreateWithFlags(&ctx->ev_store_done, cudaEventDisableTiming));
+    }
+    // the partition as the training stream's work so far leaves it
+    LGD_CUDA(cudaEventRecord(ctx->ev_store_src, ctx->stream));
+    LGD_CUDA(cudaStreamWaitEvent(ctx->store_stream, ctx->ev_store_src, 0));
+    const uint64_t off = ctx->part_begin(p) * ctx->dim, cnt = rows * ctx->dim;
+    LGD_CUDA(cudaMemcpyAsync(e_s, ctx->theta.get() + off, cnt * 4, cudaMemcpyDeviceToHost,
+                             ctx->store_stream));
+    LGD_CUDA(cudaMemcpyAsync(e_s + cnt, ctx->state.get() + off, cnt * 4, cudaMemcpyDeviceToHost,
+                             ctx->store_stream));
+    LGD_CUDA(cudaEventRecord(ctx->ev_store_done, ctx->store_stream));
+    ctx->stores_pending = true;
+  });
+}
+
+int lgd_wait_stores(lgd_context* ctx) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard g(ctx->device);
+    ctx->wait_stores();
+  });
+}
+
 int lgd_set_relations(lgd_context* ctx, const float* e_s, uint64_t count) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
     if (count != ctx->R) throw std::invalid_argument("relation count mismatch");
     if (!count) return;
     DeviceGuard g(ctx->device);
+    ctx->wait_stores();  // its copies do not run on the training stream
     ensure_tables(ctx);
     const uint64_t cnt = count * ctx->dim;
     LGD_CUDA(cudaMemcpy(ctx->rel_theta.get(), e_s, cnt * 4, cudaMemcpyHostToDevice));
@@ -1307,6 +1366,7 @@ int lgd_train_epoch(lgd_context* ctx, uint32_t epoch, lgd_epoch_result* out) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->train_range(epoch, 0, ctx->plan.bucket_order.size(), out);
   });
 }
@@ -1316,6 +1376,7 @@ int lgd_train_buckets(lgd_context* ctx, uint32_t epoch, uint64_t g_begin, uint64
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->train_range(epoch, g_begin, g_end, out);
   });
 }
@@ -1361,6 +1422,7 @@ int lgd_train_items(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* ite
     if (!ctx || (!items && count)) throw std::invalid_argument("null argument");
     if (!ctx->partitioned) throw std::invalid_argument("no partition plan");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->train_items(epoch, work_items(ctx, items, count), out, ctx->host_edges);
   });
 }
@@ -1371,6 +1433,7 @@ int lgd_round_begin(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* ite
     if (!ctx || (!items && count)) throw std::invalid_argument("null argument");
     if (!ctx->partitioned) throw std::invalid_argument("no partition plan");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     const uint64_t b = ctx->round_begin(epoch, work_items(ctx, items, count));
     if (my_batches) *my_batches = b;
   });
@@ -1380,6 +1443,7 @@ int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->round_step(step, rel_grad_device);
   });
 }
@@ -1388,6 +1452,7 @@ int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device) {
   return guarded([&] {
     if (!ctx || !summed_device) throw std::invalid_argument("null argument");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->round_apply_relations(summed_device);
   });
 }
@@ -1418,6 +1483,10 @@ int lgd_device_tables(lgd_context* ctx, float** theta, float** state, float** re
                       float** rel_state) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
+    {
+      DeviceGuard g(ctx->device);
+      ctx->wait_stores();  // the caller may write through these on any stream
+    }
     if (theta) *theta = ctx->theta.get();
     if (state) *state = ctx->state.get();
     if (rel_theta) *rel_theta = ctx->rel_theta.get();
@@ -1431,6 +1500,7 @@ int lgd_train_buckets_from_host(lgd_context* ctx, uint32_t epoch, uint64_t g_beg
   return guarded([&] {
     if (!ctx || !host_bucketed_edges) throw std::invalid_argument("null argument");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->train_range(epoch, g_begin, g_end, out, host_bucketed_edges);
   });
 }
@@ -1471,6 +1541,7 @@ int lgd_train_batch(lgd_context* ctx, const uint32_t* edges, uint64_t num_positi
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
+    ctx->fence_stores();
     ctx->upload_batch(edges, num_positives, negatives);
     LGD_CUDA(cudaMemsetAsync(ctx->counters.get(), 0, 16, ctx->stream));
     LGD_CUDA(cudaMemsetAsync(ctx->batch_losses.get(), 0, 8, ctx->stream));

@@ -93,6 +93,8 @@ def library():
         "lgd_init_store": (i32, [vp, u64]),
         "lgd_load_partition": (i32, [vp, u32, vp, u64]),
         "lgd_store_partition": (i32, [vp, u32, vp, u64]),
+        "lgd_store_partition_async": (i32, [vp, u32, vp, u64]),
+        "lgd_wait_stores": (i32, [vp]),
         "lgd_set_relations": (i32, [vp, vp, u64]),
         "lgd_get_relations": (i32, [vp, vp, u64]),
         "lgd_train_epoch": (i32, [vp, u32, vp]),
@@ -354,6 +356,7 @@ class Trainer:
         _check(L.lgd_create(C.byref(h), MODELS[model.kind], model.dim, C.byref(opts), device))
         self._h = h
         self._ordered = False
+        self._stores = []  # host buffers of pending asynchronous write-backs
         self.num_nodes = self.num_relations = self.num_edges = 0
         self.n = 0
         self.bucket_offsets = None
@@ -445,6 +448,22 @@ class Trainer:
         out = np.zeros(2 * rows * self.model.dim, np.float32)
         _check(library().lgd_store_partition(self._h, p, _p(out), rows))
         return out
+
+    def store_partition_async(self, p, out):
+        """Queue the write-back of partition p into `out` (a float32 array of
+        2 * rows * dim, ideally PinnedArray.array) and return at once; the copy
+        overlaps later read-only work (evaluate).  `out` is filled when
+        wait_stores() returns (EmbeddingStore::write_partition, store.cpp:27-57)."""
+        rows = self.part_rows(p)
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous
+                and out.size == 2 * rows * self.model.dim):
+            raise ValueError("out must be a contiguous float32 array of 2 * rows * dim")
+        _check(library().lgd_store_partition_async(self._h, p, _p(out), rows))
+        self._stores.append(out)
+
+    def wait_stores(self):
+        _check(library().lgd_wait_stores(self._h))
+        self._stores.clear()
 
     def load_tables(self, E, S):
         """Whole-graph E and S (V x d) split into the n E||S partition blobs."""

@@ -446,3 +446,38 @@ def test_bucket_presort_matches_per_batch_sort(kind, monkeypatch):
     assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
     if R:
         assert np.array_equal(rela[0], relb[0]) and np.array_equal(rela[1], relb[1])
+
+
+# ------------------------------------------- asynchronous partition write-back
+@pytest.mark.parametrize("kind", ["distmult", "dot"])
+def test_async_store_overlaps_eval_and_orders_before_training(kind):
+    """lgd_store_partition_async (the epoch-end writes of pipeline.cpp:173-193):
+    the pinned copies see the tables exactly as the epoch left them, an
+    evaluate queued behind them runs unchanged, and the next epoch -- which
+    rewrites every partition -- is ordered after the copies."""
+    g = golden(f"epoch_{kind}_n4")
+    V, R, d = int(g["V"]), int(g["R"]), int(g["d"])
+    t = make_trainer(kind, d, V, R if kind != "dot" else 0, g["edges"], 4, k=int(g["k"]),
+                     batch=int(g["batch"]), seed=int(g["seed"]))
+    t.init_store(int(g["store_seed"]))
+    t.run_epoch(0)
+    want = [t.store_partition(p) for p in range(4)]
+    test = np.asarray(g["edges"][:200])
+    ev = lgd.EvalOptions(hits_k=10, num_candidates=99, seed=7)
+    mrr0, hits0 = t.evaluate(test, ev)
+    bufs = [lgd.PinnedArray(w.shape, np.float32) for w in want]
+    for p, b in enumerate(bufs):
+        b.array[:] = np.nan
+        t.store_partition_async(p, b.array)
+    mrr1, hits1 = t.evaluate(test, ev)  # read-only: may overlap the copies
+    t.run_epoch(1)  # writes the tables: ordered after the copies
+    t.wait_stores()
+    for p in range(4):
+        np.testing.assert_array_equal(bufs[p].array, want[p])
+    assert (mrr1, hits1) == (mrr0, hits0)
+    assert not np.array_equal(t.store_partition(0), want[0])  # epoch 1 did train
+    with pytest.raises(ValueError):
+        t.store_partition_async(0, np.zeros(3, np.float32))
+    t.close()
+    for b in bufs:
+        b.free()
