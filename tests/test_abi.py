@@ -45,3 +45,12 @@ def test_argument_validation_before_device():
         lgd.Trainer(lgd.ScoreModel("complex", 7))
     with pytest.raises(lgd.InvalidArgument):
         lgd.Trainer(lgd.ScoreModel("dot", 0))
+
+
+def test_store_calls_reject_null_context_without_gpu():
+    """The write-back entry points validate before touching a device."""
+    L = lgd.library()
+    assert L.lgd_store_partition_async(None, 0, None, 0) != 0
+    assert b"null" in lgd.library().lgd_last_error()
+    assert L.lgd_wait_stores(None) != 0
+    assert b"null" in lgd.library().lgd_last_error()
