@@ -105,7 +105,7 @@ struct lgd_context {
   // per-batch scratch
   uint64_t batch_cap = 0;  // positives
   uint32_t k_cap = 0;
-  DevBuf<double> w, mix, loss, part_first, part_last;
+  DevBuf<double> w, mix, ir1, loss, part_first, part_last;
   DevBuf<float> snap;
   // shared-negative chunks (shared.cu)
   DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowmax, sn_rowinv, sn_G;
@@ -253,6 +253,7 @@ struct lgd_context {
       w.reserve(P * kk + P);  // + TransE's dst coefficients
     }
     mix.reserve(P * dim);
+    if (k4_ir1(kind)) ir1.reserve(P * dim);  // K3 -> K4 IR1 rows
     snap.reserve(P * dim);
     loss.reserve(3 * P);  // K3's loss parts (loss_reduce takes the log)
     node_keys.reserve(items);
@@ -295,10 +296,14 @@ struct lgd_context {
   // at a scattered time during K4 while the theta / state rows stream through
   // L2: a persisting access window keeps the snapshot on chip.
   void pin_snapshot_in_l2() {
-    if (!l2_persist || !snap.get()) return;
+    // (k4_ir1 models: K4 reads K3's f64 IR1 rows instead)
+    const bool ir1_rows = k4_ir1(kind);
+    void* base = ir1_rows ? (void*)ir1.get() : (void*)snap.get();
+    const size_t bytes = ir1_rows ? ir1.bytes() : snap.bytes();
+    if (!l2_persist || !base) return;
     cudaStreamAttrValue v{};
-    v.accessPolicyWindow.base_ptr = snap.get();
-    v.accessPolicyWindow.num_bytes = std::min<size_t>(snap.bytes(), l2_window_max);
+    v.accessPolicyWindow.base_ptr = base;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, l2_window_max);
     v.accessPolicyWindow.hitRatio =
         (float)std::min(1.0, (double)l2_persist / (double)v.accessPolicyWindow.num_bytes);
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -323,6 +328,7 @@ struct lgd_context {
     a.eps = opt.adagrad_epsilon;
     a.w = w.get();
     a.mix = mix.get();
+    a.ir1 = ir1.get();
     a.snap = snap.get();
     a.loss = loss.get();
     a.loss_parts = 0;  // run_batch turns them on where K3 writes them

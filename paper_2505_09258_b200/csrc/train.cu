@@ -266,8 +266,13 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       for (uint32_t j = lane; j < h; j += 32) {
         const double sr = srow[j], si = srow[j + h];
         const double rr = rrow[j], ri = rrow[j + h];
-        ir1[j] = sr * rr - si * ri;
-        ir1[j + h] = sr * ri + si * rr;
+        const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
+        ir1[j] = xr;
+        ir1[j + h] = xi;
+        if (k4_ir1(KIND)) {
+          a.ir1[p * d + j] = xr;
+          a.ir1[p * d + j + h] = xi;
+        }
       }
       for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
     } else if ((d & 3) == 0) {  // lane-owned float4 columns (TransE: u = s + r)
@@ -284,13 +289,19 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         }
         *reinterpret_cast<double2*>(ir1 + i) = make_double2(u0, u1);
         *reinterpret_cast<double2*>(ir1 + i + 2) = make_double2(u2, u3);
+        if (k4_ir1(KIND)) {
+          *reinterpret_cast<double2*>(a.ir1 + p * d + i) = make_double2(u0, u1);
+          *reinterpret_cast<double2*>(a.ir1 + p * d + i + 2) = make_double2(u2, u3);
+        }
         *reinterpret_cast<float4*>(a.snap + p * d + i) = sv;
       }
     } else {
-      for (uint32_t i = lane; i < d; i += 32)
+      for (uint32_t i = lane; i < d; i += 32) {
         ir1[i] = KIND == 0   ? (double)srow[i]
                  : KIND == 3 ? (double)srow[i] + (double)rrow[i]
                              : (double)srow[i] * (double)rrow[i];
+        if (k4_ir1(KIND)) a.ir1[p * d + i] = ir1[i];
+      }
       for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
     }
     __syncwarp();
@@ -916,6 +927,7 @@ struct ItemRegs {
 struct SegCtx {  // hoisted kernel arguments
   const float* snap;
   const double* mix;
+  const double* ir1;  // K3's IR1 rows (k4_ir1)
   const double* w;
   const float* rel_theta;
   const uint32_t* rel_keys;
@@ -950,6 +962,12 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1))
          : (KIND == 3 && pred && slot == 0) ? __ldg(x.w + x.cpos_off + p) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
+  if (k4_ir1(KIND) && !SH) {
+    // dst / negative: IR1 as K3 formed it; src: mix (both f64 rows)
+    L.ldd((is_src ? x.mix : x.ir1) + row, pred, it.mv);
+    if (is_src) it.rel = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
+    return;
+  }
   if (KIND != 0)
     it.rel = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
   L.template ldf<true>(x.snap + row, pred && !is_src, it.sv);
@@ -964,6 +982,11 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
   if (SH && !REL && it.slot == 1) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) acc[e] += (double)it.sv[e];
+    return;
+  }
+  if (k4_ir1(KIND) && !REL && !SH && it.slot <= k) {  // dst / negative from K3's IR1
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] += KIND == 3 ? it.w * (it.mv[e] - (double)own[e]) : it.w * it.mv[e];
     return;
   }
   float rv[NE];
@@ -1026,7 +1049,7 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
   const uint64_t base = c * 32;
   if (base >= n) return;
   const Lanes<KIND, NV> L(lane, a.dim);
-  const SegCtx x{a.snap, a.mix, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
                  (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
                  (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
                  a.P * a.k, a.sh_G};

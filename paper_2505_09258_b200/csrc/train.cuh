@@ -7,6 +7,18 @@
 
 namespace lgd {
 
+// ComplEx / TransE: K4's dst / negative items read IR1 = combine(src, rel) as
+// K3 wrote it (P x d f64) instead of recombining the src snapshot with the
+// relation row (FM +4.6%, Friendster +0.5%).  DistMult keeps the snapshot: its
+// recombination is cheaper than reading the 2x wider row (TW -1.8%).
+__host__ __device__ constexpr bool k4_ir1(int kind) {
+#ifndef LGD_NO_K4_IR1
+  return kind == 2 || kind == 3;
+#else
+  return false && kind;
+#endif
+}
+
 struct BatchArgs {
   int kind;
   uint32_t dim;
@@ -23,6 +35,7 @@ struct BatchArgs {
   // scratch (sized for the largest batch)
   double* w;                  // P x k softmax weights
   double* mix;                // P x d  sum_j w_j neg_j - dst
+  double* ir1;                // P x d  IR1 = combine(src, rel) (typed models; K4's dst / negative items)
   float* snap;                // P x d  pre-update source rows
   double* loss;               // per-positive loss: P values (shared mode), or K3's
                               // parts f_pos | row_max | sum (3 x P, loss_parts)
