@@ -10,9 +10,12 @@ namespace lgd {
 // ComplEx / TransE: K4's dst / negative items read IR1 = combine(src, rel) as
 // K3 wrote it (P x d f64) instead of recombining the src snapshot with the
 // relation row (FM +4.6%, Friendster +0.5%).  DistMult keeps the snapshot: its
-// recombination is cheaper than reading the 2x wider row (TW -1.8%).
+// recombination is cheaper than reading the 2x wider row (TW -1.8% with the
+// snapshot's 48 MB L2 window on IR1, -2.0% without; -DLGD_K4_IR1_ALL to measure).
 __host__ __device__ constexpr bool k4_ir1(int kind) {
-#ifndef LGD_NO_K4_IR1
+#if defined(LGD_K4_IR1_ALL)
+  return kind != 0;
+#elif !defined(LGD_NO_K4_IR1)
   return kind == 2 || kind == 3;
 #else
   return false && kind;
