@@ -44,7 +44,8 @@ CONFIGS = {
                        n=32),
 }
 K_NEG, BATCH, LR, SEED, ALPHA, GRAPH_SEED = 16, 100_000, 0.1, 42, 2.3, 20250509
-REF_SAMPLE_POSITIVES = 25_000  # positives per reference step (bounded CPU sample)
+CPU_BASELINE_BATCHES = 4  # cpu_baseline leg: 4 reference batches of P = 100,000 (~35 s)
+REF_BUDGET_S = 120.0  # --impl reference: timed batches stop after ~2 min of CPU work
 
 
 def peaks_tensor():
@@ -113,12 +114,29 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def dist_setup(gpus):
+def launch_command(argv, gpus, port):
+    """`bench.py --gpus N` without a torchrun environment re-launches itself
+    as N ranks (one process per GPU), exactly as the driver would."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def dist_setup(gpus, init=True):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}")
     pg = None
-    if world > 1:
+    if world > 1 and init:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -151,44 +169,73 @@ def sum_over_ranks(pg, value, local):
 
 
 # ------------------------------------------------------------ CPU reference
-def cpu_sample(cfg, bucket_edges, stride, steps, batch, which):
-    """Time the reference CPU trainer on a bounded sample: the first state's
-    resident partitions {0,1,2} (all of them when n < 3; initialised exactly
-    like the store), bucket (0,1)'s edges (bucket 0 when n = 1), `steps`
-    consecutive batches of `batch` positives."""
-    from oracle.oracle import Oracle, available
-    kind = "reference" if (which != "port" and available("reference")) else "restatement"
-    o = Oracle(kind)
+REF_BATCH = BATCH  # the reference CLI's batch (legend_main.cpp:29-38): same config as the GPU arm
+
+
+def ref_workload(cfg):
+    """The first bucket of the reference plan -- bucket (0,1) at position g = 0,
+    pool = state 0's partitions {0,1,2} (bucket 0 / the whole graph when n = 1)
+    -- of the benchmark graph, built on the host by the generator's C
+    restatement (oracle/graphgen.c, bit-identical to lgd_generate_graph: see
+    tests/test_gpu_graph.py), and the pool's initial rows (store init,
+    store.cpp:59-86).  Loads nothing from the product package."""
+    from oracle.oracle import Oracle
     lo = Oracle("restatement")
-    d, R = cfg["dim"], cfg["rels"]
-    V_loc = min(3 * stride, cfg["nodes"])
+    n, V, R, d = cfg["n"], cfg["nodes"], cfg["rels"], cfg["dim"]
+    stride = -(-V // n)
+    bi, bj = (0, 1) if n > 1 else (0, 0)
+    bucket = lo.powerlaw_bucket(V, R, cfg["edges"], ALPHA, GRAPH_SEED, n, bi, bj)
+    nparts = min(3, n)
+    V_loc = min(nparts * stride, V)
     E = np.zeros((V_loc, d), np.float32)
-    for p in range(3):
+    first, count = [], []
+    for p in range(nparts):
         a, b = p * stride, min((p + 1) * stride, V_loc)
-        if b > a:
-            lo.init_rows(lo.derive_seed(SEED, p), b - a, d, E[a:b])
+        lo.init_rows(lo.derive_seed(SEED, p), b - a, d, E[a:b])
+        first.append(a)
+        count.append(b - a)
     S = np.zeros_like(E)
-    rE = np.zeros((max(R, 1), d), np.float32)
+    rE = rS = None
     if R:
+        rE = np.zeros((R, d), np.float32)
         lo.init_rows(lo.derive_seed(SEED, 0x52454C53), R, d, rE)
-    rS = np.zeros_like(rE)
-    first = [f for f in (0, stride, 2 * stride) if f < V_loc]  # n < 3: fewer partitions
-    count = [min(stride, V_loc - f) for f in first]
-    stream = lo.derive_seed(SEED, 0x62756B74, 0, 0)
-    m = min(len(bucket_edges), steps * batch)
+        rS = np.zeros_like(rE)
+    stream = lo.derive_seed(SEED, 0x62756B74, 0, 0)  # pipeline.cpp:296, epoch 0, g = 0
+    sample = (f"bucket ({bi},{bj}) of the plan (g = 0, {len(bucket):,} edges, shuffled in full), "
+              f"pool {{{','.join(str(p) for p in range(nparts))}}} ({V_loc:,} rows), "
+              f"{cfg['model']} d={d} k={K_NEG}, batches of {REF_BATCH:,} positives")
+    return dict(bucket=bucket, first=first, count=count, E=E, S=S, rE=rE, rS=rS, stream=stream,
+                sample=sample)
+
+
+def cpu_sample(cfg, warmup, steps, budget_s=0.0, w=None):
+    """Time the reference CPU trainer (oracle/_ref: the unmodified reference
+    sources; single-threaded by design) on `warmup` + `steps` consecutive
+    batches of the workload above, or fewer once `budget_s` seconds of batch
+    time are spent; returns edges/s over the timed batches' wall time (each
+    batch: sample_negatives + batch_loss + batch_gradients + adagrad_step)."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("reference") else "restatement"
+    w = w or ref_workload(cfg)
+    o = Oracle(kind)
     t0 = time.perf_counter()
-    _, done = o.bucket_sample(cfg["model"], bucket_edges[:m], first, count, stream, E, S,
-                              rE if R else None, rS if R else None, batch_size=batch, k=K_NEG,
-                              max_batches=steps, lr=LR)
-    dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "edges/s", "cores": 1, "host_cores": os.cpu_count(),
+    losses, extra = o.bucket_sample_batches(
+        cfg["model"], w["bucket"], w["first"], w["count"], w["stream"], w["E"], w["S"], w["rE"],
+        w["rS"], batch_size=REF_BATCH, k=K_NEG, max_batches=warmup + steps, budget_s=budget_s)
+    wall = time.perf_counter() - t0
+    nb = len(losses)
+    sizes = [min(REF_BATCH, len(w["bucket"]) - b * REF_BATCH) for b in range(nb)]
+    timed = range(min(warmup, nb - 1), nb)
+    edges = sum(sizes[b] for b in timed)
+    if kind == "reference":
+        secs = sum(int(extra[b]) for b in timed) / 1e9
+    else:  # the restatement reports no per-batch times: whole call, all batches
+        secs, edges = wall, sum(sizes)
+    return {"value": edges / secs, "unit": "edges/s", "cores": 1, "host_cores": os.cpu_count(),
             "kind": "reference" if kind == "reference" else "port",
-            "sample": (f"state {{{','.join(str(f // stride) for f in first)}}} resident "
-                       f"({V_loc:,} rows), bucket {'(0,1)' if len(first) > 1 else '(0,0)'}: "
-                       f"shuffle of "
-                       f"{m:,} edges then {steps} batch(es) of {batch:,} positives, "
-                       f"{cfg['model']} d={d} k={K_NEG}; {done:,} edges in {dt:.1f} s"),
-            "seconds": dt, "edges": done}
+            "sample": (w["sample"] + f": {len(timed)} timed batch(es) after "
+                       f"{nb - len(timed)} warm-up, {edges:,} edges in {secs:.1f} s"),
+            "seconds": secs, "edges": edges, "batches": len(timed)}
 
 
 def setup_trainer(cfg, device, k=K_NEG, chunk=0):
@@ -203,32 +250,26 @@ def setup_trainer(cfg, device, k=K_NEG, chunk=0):
 
 
 def reference_arm(args, cfg, rank):
+    """--impl reference: the reference CPU trainer (oracle/_ref) on the same
+    config -- TW-shaped DistMult d=100, n=16, P=100,000, k=16 -- one batch of
+    the plan's first bucket per step, W warm-up then K timed steps.  Rank 0
+    only; the product library is never loaded here."""
     if rank != 0:
         return
-    import paper_2505_09258_b200 as lgd
-    # bucket (0,1) of the same synthetic graph: generated on the GPU (the
-    # generator is part of the workload definition, not of the timed path)
-    t = lgd.Trainer(lgd.ScoreModel(cfg["model"], cfg["dim"]),
-                    lgd.TrainOptions(batch_size=BATCH, negatives=K_NEG, seed=SEED))
-    t.generate_graph(cfg["nodes"], cfg["rels"], cfg["edges"], ALPHA, GRAPH_SEED)
-    offsets, _ = t.make_partition_plan(cfg["n"])
-    stride = t.stride()
-    b = 0 * cfg["n"] + 1 if cfg["n"] > 1 else 0
-    a0, a1 = int(offsets[b]), int(offsets[b + 1])
-    need = min(a1 - a0, (args.steps + args.warmup) * REF_SAMPLE_POSITIVES)
-    allb = t.bucketed_edges()
-    bucket = np.ascontiguousarray(allb[a0:a0 + max(need, 1)])
-    del allb
-    t.close()
-    # warmup steps run first (untimed) on the leading batches, then K timed
-    res = cpu_sample(cfg, bucket, stride, args.steps + args.warmup, REF_SAMPLE_POSITIVES,
-                     "reference")
+    # warm-up: one batch (a CPU loop has no JIT; the first batch pays the
+    # table's first touch); timed: up to K batches within REF_BUDGET_S
+    res = cpu_sample(cfg, min(args.warmup, 1), args.steps, budget_s=REF_BUDGET_S)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "edges/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * res["seconds"] / (args.steps + args.warmup),
+            "n_gpus": args.gpus, "steps": res["batches"], "warmup": min(args.warmup, 1),
+            "ms_per_step": 1e3 * res["seconds"] / max(res["batches"], 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg["workload"], "step": (
-                f"{REF_SAMPLE_POSITIVES:,} positives of bucket (0,1)"), "storage": "f32"},
+            "data": "synthetic",
+            "config": {"workload": cfg["workload"], "num_nodes": cfg["nodes"],
+                       "num_edges": cfg["edges"], "num_relations": cfg["rels"],
+                       "dim": cfg["dim"], "partitions": cfg["n"], "negatives": K_NEG,
+                       "batch_size": REF_BATCH, "storage": "f32 (E||S), FP64 arithmetic",
+                       "graph": f"power-law alpha={ALPHA}, generator seed {GRAPH_SEED}",
+                       "step": f"one batch of {REF_BATCH:,} positives of the plan's first bucket"},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "host_cores", "kind",
                                                  "sample")},
             "e2e": {"value": res["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -348,7 +389,7 @@ def bench_rounds(args, cfg, rank, world, local, pg):
             "roofline": {"bound": "hbm", "kernel": "segment_pass1+2 (K4), rank 0",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_source": peak_kind,
-                         "traffic": (traffic_from_profiles() or {}).get(dom),
+                         "traffic": (traffic_from_profiles(args.config) or {}).get(dom),
                          "step_achieved": algo_all / dev_s / 1e9 / world,
                          "step_frac": algo_all / dev_s / 1e9 / world / hbm},
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
@@ -359,11 +400,13 @@ def bench_rounds(args, cfg, rank, world, local, pg):
         pg.destroy_process_group()
 
 
-def traffic_from_profiles():
+def traffic_from_profiles(config):
+    """ncu DRAM bytes per launch of this config's kernels (profiles/ncu_traffic.json,
+    one capture per config), or None when this config was not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get(config)
     except Exception:
         return None
 
@@ -387,10 +430,13 @@ def main():
                          "cores (not a reference mode: no CPU baseline)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    rank, world, local, pg = dist_setup(args.gpus)
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(subprocess.call(launch_command(sys.argv[1:], args.gpus, free_port())))
+    if args.impl == "reference":  # CPU only: no process group
+        rank, _, _, _ = dist_setup(args.gpus, init=False)
         reference_arm(args, cfg, rank)
         return
+    rank, world, local, pg = dist_setup(args.gpus)
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 
@@ -441,7 +487,7 @@ def main():
     dom = max(cand, key=lambda k: cand[k]["total_ms"])
     dstat = stats[dom]
     achieved = dstat["algorithmic_bytes"] / (dstat["total_ms"] / 1e3) / 1e9
-    traffic = traffic_from_profiles()
+    traffic = traffic_from_profiles(args.config)
     roofline = {"bound": "hbm", "kernel": {"score": "score_kernel (K3)",
                                            "update": "segment_pass1+2 (K4)"}[dom],
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -487,13 +533,7 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and not args.shared_chunk:
-        offsets = t.bucket_offsets
-        b = 1 if cfg["n"] > 1 else 0
-        a0, a1 = int(offsets[b]), int(offsets[b + 1])
-        allb = t.bucketed_edges()
-        bucket = np.ascontiguousarray(allb[a0:a0 + min(a1 - a0, 4 * REF_SAMPLE_POSITIVES)])
-        del allb
-        cpu = cpu_sample(cfg, bucket, t.stride(), 4, REF_SAMPLE_POSITIVES, "reference")
+        cpu = cpu_sample(cfg, 0, CPU_BASELINE_BATCHES)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "host_cores", "kind", "sample")}
 
     if rank == 0:

@@ -113,6 +113,18 @@ int lgd_generate_graph(lgd_context* ctx, uint64_t num_nodes, uint64_t num_relati
                        uint64_t num_edges, double zipf_exponent, uint64_t seed);
 int lgd_get_graph(lgd_context* ctx, uint32_t* edges_out);
 
+/* write_graph / read_graph (graph.cpp:152-192), host only (no context, no
+ * device): dir/edges.bin = the raw 12-byte records, dir/graph_meta.json =
+ * {"num_edges", "num_nodes", "num_relations"} in the reference's exact text
+ * (nlohmann dump(2) + newline).  Read the metadata first to size edges_out.
+ * I/O failures are LGD_RUNTIME_ERROR (std::runtime_error), as in the
+ * reference. */
+int lgd_write_graph(const char* dir, const uint32_t* edges, uint64_t num_edges, uint64_t num_nodes,
+                    uint64_t num_relations);
+int lgd_read_graph_meta(const char* dir, uint64_t* num_edges, uint64_t* num_nodes,
+                        uint64_t* num_relations);
+int lgd_read_graph(const char* dir, uint32_t* edges_out, uint64_t num_edges);
+
 /* make_partition_plan (graph.cpp:120-150), computed on the device.  Outputs
  * may be NULL; bucket_offsets has n*n+1 entries, edge_order num_edges. */
 int lgd_make_partition_plan(lgd_context* ctx, uint32_t n, uint64_t* bucket_offsets_out,
@@ -180,6 +192,15 @@ int lgd_train_epoch(lgd_context* ctx, uint32_t epoch, lgd_epoch_result* out);
 int lgd_train_buckets(lgd_context* ctx, uint32_t epoch, uint64_t g_begin, uint64_t g_end,
                       lgd_epoch_result* out);
 
+/* The bucket at plan position g alone, cut after its first max_batches
+ * batches (0 = all): the loop of pipeline.cpp:289-312 over a bounded prefix,
+ * with the bucket's full shuffle and its stream consumed exactly as far as
+ * the reference's.  Optional outputs (capacity = the batches run): per-batch
+ * loss (batch_loss, train.cpp:217-278) and |GradientSet.nodes|.  Used to check
+ * full-scale shapes against a CPU restatement in seconds. */
+int lgd_train_bucket_prefix(lgd_context* ctx, uint32_t epoch, uint64_t g, uint64_t max_batches,
+                            double* batch_losses, uint64_t* batch_nodes, lgd_epoch_result* out);
+
 /* Same, streaming each bucket's edges from a host copy of the edge list in
  * bucket order (lgd_get_bucketed_edges; pinned memory from lgd_host_alloc for
  * full bandwidth): the H2D copy of bucket g+1 overlaps the training of g. */
@@ -210,7 +231,10 @@ int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device);
 int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device);
 int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out);
 /* The context's CUDA stream (cudaStream_t): every kernel of the context runs
- * on it, in order. */
+ * on it, in order.  The call orders the stream after pending asynchronous
+ * write-backs (lgd_store_partition_async), so work the caller then queues on
+ * it may write the tables; writers on other streams, or through pointers
+ * taken earlier, must call lgd_wait_stores first. */
 int lgd_get_stream(lgd_context* ctx, void** cuda_stream);
 /* on != 0: lgd_round_step and lgd_round_apply_relations return as soon as
  * their work is queued, without draining the stream.  The caller then orders

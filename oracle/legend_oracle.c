@@ -833,12 +833,32 @@ void lo_shuffle_perm(uint64_t seed, uint64_t m, uint32_t* perm, uint64_t* consum
  * for ONE bucket: copy, seeded Fisher-Yates shuffle, then up to max_batches
  * batches of sample_negatives + batch_loss + batch_gradients + adagrad_step.
  * The table holds rows [0, num_nodes); the pool lists the resident ranges. */
+int lo_bucket_sample_ex(const uint32_t* bucket_edges, uint64_t m, const uint64_t* first,
+                        const uint64_t* count, int nparts, uint64_t stream_seed, int shuffle,
+                        uint32_t batch_size, uint32_t k, uint64_t max_batches, int kind,
+                        uint32_t d, float* E, float* S, uint64_t num_nodes, float* relE,
+                        float* relS, uint64_t num_rels, double lr, double eps, double* loss_sum,
+                        uint64_t* edges_trained, double* batch_losses, uint64_t* batch_nodes);
+
 int lo_bucket_sample(const uint32_t* bucket_edges, uint64_t m, const uint64_t* first,
                      const uint64_t* count, int nparts, uint64_t stream_seed, int shuffle,
                      uint32_t batch_size, uint32_t k, uint64_t max_batches, int kind, uint32_t d,
                      float* E, float* S, uint64_t num_nodes, float* relE, float* relS,
                      uint64_t num_rels, double lr, double eps, double* loss_sum,
                      uint64_t* edges_trained) {
+  return lo_bucket_sample_ex(bucket_edges, m, first, count, nparts, stream_seed, shuffle,
+                             batch_size, k, max_batches, kind, d, E, S, num_nodes, relE, relS,
+                             num_rels, lr, eps, loss_sum, edges_trained, NULL, NULL);
+}
+
+/* The same with optional per-batch outputs (max_batches entries each): the
+ * loss of every batch and |GradientSet.nodes|. */
+int lo_bucket_sample_ex(const uint32_t* bucket_edges, uint64_t m, const uint64_t* first,
+                        const uint64_t* count, int nparts, uint64_t stream_seed, int shuffle,
+                        uint32_t batch_size, uint32_t k, uint64_t max_batches, int kind,
+                        uint32_t d, float* E, float* S, uint64_t num_nodes, float* relE,
+                        float* relS, uint64_t num_rels, double lr, double eps, double* loss_sum,
+                        uint64_t* edges_trained, double* batch_losses, uint64_t* batch_nodes) {
   uint32_t* edges = (uint32_t*)malloc((m ? m : 1) * 3 * sizeof(uint32_t));
   uint32_t* negs = (uint32_t*)malloc((uint64_t)batch_size * k * sizeof(uint32_t));
   if (!edges || !negs) {
@@ -865,9 +885,12 @@ int lo_bucket_sample(const uint32_t* bucket_edges, uint64_t m, const uint64_t* f
     rc = lo_sample_negatives_rng(first, count, nparts, k, cnt, &rng, negs);
     if (rc) break;
     double l = 0.0;
+    uint64_t nodes = 0;
     rc = lo_batch(kind, d, E, S, num_nodes, relE, relS, num_rels, edges + 3 * off, cnt, negs, k,
-                  lr, eps, 1, &l, NULL, NULL, NULL, NULL, NULL, NULL);
+                  lr, eps, 1, &l, &nodes, NULL, NULL, NULL, NULL, NULL);
     if (rc) break;
+    if (batch_losses) batch_losses[nb] = l;
+    if (batch_nodes) batch_nodes[nb] = nodes;
     total += l;
     done += cnt;
   }

@@ -68,6 +68,15 @@ class Oracle:
         bind("bucket_sample", i32, [vp, u64, vp, vp, i32, u64, i32, u32, u32, u64, i32, u32, vp,
                                     vp, u64, vp, vp, u64, f64, f64, vp, vp])
         if which == "restatement":
+            bind("bucket_sample_ex", i32, [vp, u64, vp, vp, i32, u64, i32, u32, u32, u64, i32,
+                                           u32, vp, vp, u64, vp, vp, u64, f64, f64, vp, vp, vp,
+                                           vp])
+            bind("det_pow", f64, [f64, f64])
+            bind("det_log", f64, [f64])
+            bind("det_exp", f64, [f64])
+            bind("powerlaw_edges", i32, [u64, u64, f64, u64, u64, u64, vp])
+            bind("powerlaw_bucket", i32, [u64, u64, u64, f64, u64, u32, u32, u32, i32, vp, u64,
+                                          vp])
             bind("shuffle_perm", None, [u64, u64, vp, vp])
             bind("batch_split", i32, [i32, u32, vp, vp, u64, vp, vp, u64, vp, u64, vp, u32, f64,
                                       f64, i32, i32, vp, vp, vp, vp])
@@ -91,6 +100,11 @@ class Oracle:
             bind("plan_json", i32, [u32, C.c_char_p, u64, vp])
             bind("verify_prefetchable", i32, [u32, u64, vp, vp, vp, vp, vp, vp])
             bind("last_error", C.c_char_p, [])
+            bind("bucket_sample_timed", i32, [vp, u64, vp, vp, i32, u64, i32, u32, u32, u64,
+                                              i32, u32, vp, vp, u64, vp, vp, u64, f64, f64, vp,
+                                              vp, vp, u64])
+            bind("write_graph", i32, [C.c_char_p, vp, u64, u64, u64])
+            bind("read_graph", i32, [C.c_char_p, vp, u64, vp, vp, vp])
 
     def _check(self, rc):
         if rc:
@@ -98,6 +112,29 @@ class Oracle:
             if "last_error" in self._fn:
                 msg = self._fn["last_error"]().decode()
             raise ERRORS.get(rc, RuntimeError)(f"{self.which} oracle error {rc}: {msg}")
+
+    # ------------------------------------------------- synthetic graphs
+    def powerlaw_edges(self, num_nodes, num_rels, alpha, seed, begin, end):
+        """Edges [begin, end) of the benchmark's power-law graph (graphgen.c),
+        bit-identical to lgd_generate_graph's (restatement only)."""
+        out = np.zeros((max(end - begin, 1), 3), np.uint32)
+        self._check(self._fn["powerlaw_edges"](num_nodes, num_rels, alpha, seed, begin, end,
+                                               _ptr(out)))
+        return out[:end - begin]
+
+    def powerlaw_bucket(self, num_nodes, num_rels, num_edges, alpha, seed, n, bi, bj,
+                        threads=None):
+        """Bucket (bi, bj) of make_partition_plan(graph, n) of the power-law
+        graph, in ingest order, scanned with `threads` host threads."""
+        threads = threads or os.cpu_count() or 1
+        cnt = np.zeros(1, np.uint64)
+        self._check(self._fn["powerlaw_bucket"](num_nodes, num_rels, num_edges, alpha, seed, n,
+                                                bi, bj, threads, None, 0, _ptr(cnt)))
+        out = np.zeros((max(int(cnt[0]), 1), 3), np.uint32)
+        self._check(self._fn["powerlaw_bucket"](num_nodes, num_rels, num_edges, alpha, seed, n,
+                                                bi, bj, threads, _ptr(out), int(cnt[0]),
+                                                _ptr(cnt)))
+        return out[:int(cnt[0])]
 
     # ---------------------------------------------------------------- RNG
     def derive_seed(self, base, a, b=0, c=0):
@@ -264,6 +301,57 @@ class Oracle:
             batch_size, k, max_batches, kind, d, _ptr(E), _ptr(S), V, _ptr(relE), _ptr(relS), R,
             lr, eps, _ptr(loss), _ptr(done)))
         return float(loss[0]), int(done[0])
+
+    def bucket_sample_batches(self, kind, bucket_edges, first, count, stream_seed, E, S, relE,
+                              relS, *, batch_size, k, max_batches, shuffle=True, lr=0.1,
+                              eps=1e-10, budget_s=0.0):
+        """bucket_sample with per-batch outputs.  Restatement: (losses, unique
+        nodes per batch); reference: (losses, wall ns per batch), stopping once
+        budget_s > 0 seconds of batch time are spent.  In place."""
+        kind = KINDS.get(kind, kind)
+        V, d = E.shape
+        R = relE.shape[0] if relE is not None else 0
+        if relE is None:
+            relE = np.zeros((1, d), np.float32)
+            relS = np.zeros((1, d), np.float32)
+        be = np.ascontiguousarray(bucket_edges, np.uint32).reshape(-1, 3)
+        first = np.ascontiguousarray(first, np.uint64)
+        count = np.ascontiguousarray(count, np.uint64)
+        losses = np.zeros(max(max_batches, 1), np.float64)
+        extra = np.zeros(max(max_batches, 1), np.uint64)
+        done = np.zeros(1, np.uint64)
+        if self.which == "restatement":
+            total = np.zeros(1, np.float64)
+            self._check(self._fn["bucket_sample_ex"](
+                _ptr(be), len(be), _ptr(first), _ptr(count), len(first), stream_seed,
+                int(shuffle), batch_size, k, max_batches, kind, d, _ptr(E), _ptr(S), V,
+                _ptr(relE), _ptr(relS), R, lr, eps, _ptr(total), _ptr(done), _ptr(losses),
+                _ptr(extra)))
+            nb = -(-int(done[0]) // batch_size) if done[0] else 0
+        else:
+            self._check(self._fn["bucket_sample_timed"](
+                _ptr(be), len(be), _ptr(first), _ptr(count), len(first), stream_seed,
+                int(shuffle), batch_size, k, max_batches, kind, d, _ptr(E), _ptr(S), V,
+                _ptr(relE), _ptr(relS), R, lr, eps, _ptr(losses), _ptr(extra), _ptr(done),
+                int(budget_s * 1e9)))
+            nb = int(done[0])
+        return losses[:nb], extra[:nb]
+
+    def write_graph(self, directory, edges, num_nodes, num_relations=0):
+        """write_graph (graph.cpp:152-171) of the reference itself."""
+        edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
+        self._check(self._fn["write_graph"](os.fsencode(directory), _ptr(edges), len(edges),
+                                            num_nodes, num_relations))
+
+    def read_graph(self, directory):
+        """read_graph (graph.cpp:173-192) of the reference itself."""
+        cnt, V, R = (np.zeros(1, np.uint64) for _ in range(3))
+        d = os.fsencode(directory)
+        self._check(self._fn["read_graph"](d, None, 0, _ptr(cnt), _ptr(V), _ptr(R)))
+        out = np.zeros((max(int(cnt[0]), 1), 3), np.uint32)
+        self._check(self._fn["read_graph"](d, _ptr(out), int(cnt[0]), _ptr(cnt), _ptr(V),
+                                           _ptr(R)))
+        return out[:int(cnt[0])], int(V[0]), int(R[0])
 
     def init_rows(self, stream_seed, rows, dim, out):
         """fill_uniform_rows (store.cpp:19-25) into a float32 slice (restatement)."""

@@ -9,6 +9,7 @@
 // except ref_run_epoch_inmem, which is the reference test suite's own
 // all-resident restatement of run_epoch (test_pipeline.cpp:227-269) driven
 // through the reference primitives.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <filesystem>
@@ -472,6 +473,86 @@ int ref_bucket_sample(const std::uint32_t* bucket_edges, std::uint64_t m,
     }
     *loss_sum = total;
     *edges_trained = done;
+  });
+}
+
+// The same bounded bucket sample with per-batch outputs: the loss of every
+// batch (batch_loss) and its wall time in ns around sample_negatives +
+// batch_loss + batch_gradients + adagrad_step (the reference arm of bench.py
+// times these).  Arrays hold max_batches entries (or fewer when the bucket
+// ends first, or once budget_ns > 0 of batch time is spent); the table copy-in
+// above the loop is not timed.
+int ref_bucket_sample_timed(const std::uint32_t* bucket_edges, std::uint64_t m,
+                            const std::uint64_t* first, const std::uint64_t* count, int nparts,
+                            std::uint64_t stream_seed, int shuffle, std::uint32_t batch_size,
+                            std::uint32_t k, std::uint64_t max_batches, int kind, std::uint32_t d,
+                            float* E, float* S, std::uint64_t num_nodes, float* relE, float* relS,
+                            std::uint64_t num_rels, double lr, double eps, double* batch_losses,
+                            std::uint64_t* batch_ns, std::uint64_t* batches_done,
+                            std::uint64_t budget_ns) {
+  return guarded([&] {
+    const ScoreModel model = model_of(kind, d);
+    ResidentTable table = table_of(d, E, S, num_nodes, relE, relS, num_rels);
+    ResidentTable pool(1);
+    for (int i = 0; i < nparts; ++i) {
+      EmbeddingPartition p;
+      p.id = static_cast<PartitionId>(i);
+      p.dim = 1;
+      p.node_count = count[i];
+      p.embeddings.assign(count[i], 0.0f);
+      p.opt_states.assign(count[i], 0.0f);
+      pool.add_partition(std::move(p), first[i]);
+    }
+    std::vector<Edge> edges = edges_of(bucket_edges, m);
+    Rng rng(stream_seed);
+    if (shuffle)
+      for (std::size_t i = edges.size(); i > 1; --i) std::swap(edges[i - 1], edges[rng.next_below(i)]);
+    const AdagradHyper hyper{lr, eps};
+    std::uint64_t nb = 0, spent = 0;
+    for (std::size_t off = 0; off < edges.size() && nb < max_batches && (!budget_ns || spent < budget_ns);
+         off += batch_size, ++nb) {
+      const std::size_t cnt = std::min<std::size_t>(batch_size, edges.size() - off);
+      const auto t0 = std::chrono::steady_clock::now();
+      TrainBatch batch;
+      batch.positives.assign(edges.begin() + off, edges.begin() + off + cnt);
+      batch.negatives_per_positive = k;
+      batch.negative_dst = sample_negatives(pool, k, cnt, rng);
+      batch_losses[nb] = batch_loss(model, batch, table);
+      adagrad_step(table, batch_gradients(model, batch, table), hyper);
+      batch_ns[nb] = (std::uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - t0)
+                         .count();
+      spent += batch_ns[nb];
+    }
+    *batches_done = nb;
+  });
+}
+
+// write_graph / read_graph (graph.cpp:152-192) through the reference itself
+int ref_write_graph(const char* dir, const std::uint32_t* edges, std::uint64_t num_edges,
+                    std::uint64_t num_nodes, std::uint64_t num_relations) {
+  return guarded([&] {
+    Graph g;
+    g.num_nodes = num_nodes;
+    g.num_relations = num_relations;
+    g.edges = edges_of(edges, num_edges);
+    write_graph(g, dir);
+  });
+}
+
+int ref_read_graph(const char* dir, std::uint32_t* edges_out, std::uint64_t cap,
+                   std::uint64_t* num_edges, std::uint64_t* num_nodes,
+                   std::uint64_t* num_relations) {
+  return guarded([&] {
+    const Graph g = read_graph(dir);
+    *num_edges = g.edges.size();
+    *num_nodes = g.num_nodes;
+    *num_relations = g.num_relations;
+    for (std::uint64_t i = 0; i < g.edges.size() && i < cap; ++i) {
+      edges_out[3 * i] = g.edges[i].src;
+      edges_out[3 * i + 1] = g.edges[i].rel;
+      edges_out[3 * i + 2] = g.edges[i].dst;
+    }
   });
 }
 

@@ -24,6 +24,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/legend_b200.h"
+#include "abi.hpp"
 #include "common.cuh"
 #include "evaluate.cuh"
 #include "internal.hpp"
@@ -33,30 +34,15 @@
 
 using namespace lgd;
 
-namespace {
-
+namespace lgd {
 thread_local std::string g_last_error;
-
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace lgd
 
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return LGD_OK;
-  } catch (const std::invalid_argument& e) {
-    return fail(LGD_INVALID_ARGUMENT, e.what());
-  } catch (const std::out_of_range& e) {
-    return fail(LGD_OUT_OF_RANGE, e.what());
-  } catch (const std::logic_error& e) {
-    return fail(LGD_LOGIC_ERROR, e.what());
-  } catch (const std::exception& e) {
-    return fail(LGD_RUNTIME_ERROR, e.what());
-  }
-}
+namespace {
 
 struct DeviceGuard {
   int prev = 0;
@@ -116,11 +102,19 @@ struct lgd_context {
   DevBuf<uint32_t> bk_keys[2], bk_vals[2];
   DevBuf<unsigned char> bk_temp;
   bool presort = true;  // LGD_PRESORT=0 turns it off (per-batch sorts)
+  // K4 v2 (train.cu: segment_rows) over a segment list; LGD_K4=1 selects the
+  // chunked pass 1 / pass 2 kernels instead (A/B)
+  bool seg_rows = true;
+  DevBuf<uint32_t> seg_start, batch_seg, seg_nseg;
+  DevBuf<unsigned int> seg_work;
+  DevBuf<unsigned char> seg_temp;
+  bool bucket_segs = false;  // the current bucket's segment list is built
   struct Presorted {
     const uint32_t* keys = nullptr;
     const uint32_t* vals = nullptr;
     uint32_t mask = 0;
     int rel_bits = 0;  // payload layout of the whole bucket
+    uint64_t items = 0;
   } bk;
   DevBuf<uint8_t> chunk_flags;
   DevBuf<uint32_t> span_list;
@@ -155,6 +149,7 @@ struct lgd_context {
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
+  double eval_ms = 0.0;  // device time of the last lgd_evaluate (profiling mode)
   size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for the snapshot rows
   // optional host copy of the bucket-ordered edges (lgd_set_host_edges): the
   // bucket lists and rounds then stream every bucket H2D instead of reading
@@ -253,7 +248,7 @@ struct lgd_context {
       w.reserve(P * kk + P);  // + TransE's dst coefficients
     }
     mix.reserve(P * dim);
-    if (k4_ir1(kind)) ir1.reserve(P * dim);  // K3 -> K4 IR1 rows
+    if (use_ir1()) ir1.reserve(P * dim);  // K3 -> K4 IR1 rows
     snap.reserve(P * dim);
     loss.reserve(3 * P);  // K3's loss parts (loss_reduce takes the log)
     node_keys.reserve(items);
@@ -287,9 +282,29 @@ struct lgd_context {
       r_grad.reserve(std::max<uint64_t>(R, 1) * dim);
       r_touched.reserve(std::max<uint64_t>(R, 1));
     }
+    if (seg_rows) ensure_segments(items, 1);
     batch_cap = P;
     k_cap = kk;
     pin_snapshot_in_l2();
+  }
+
+  // K3 stores IR1 rows for K4 only where K4 reads them: ComplEx / TransE
+  // (k4_ir1), the exact path, vector-lane dims; LGD_K4_IR1=0 recombines the
+  // snapshot instead (same bits; tests A/B the two).  The chunked K4 kernels
+  // always read them.
+  bool ir1_rows = true;
+  bool use_ir1() const {
+    return k4_ir1(kind) && !chunk() && k4_vec_width(kind, dim) != 0 && (ir1_rows || !seg_rows);
+  }
+
+  // segment-list scratch for up to `items` sorted contributions in `nb` batches
+  void ensure_segments(uint64_t items, uint64_t nb) {
+    seg_start.reserve(items + 1);
+    batch_seg.reserve(nb + 1);
+    seg_work.reserve(std::max<uint64_t>(nb, 1));
+    seg_nseg.reserve(1);
+    const size_t tb = segment_list_temp_bytes(items);
+    if (seg_temp.bytes() < tb) seg_temp.reserve(tb);
   }
 
   // Every contribution of a positive reads its snapshot row (400 B at d = 100)
@@ -297,9 +312,9 @@ struct lgd_context {
   // L2: a persisting access window keeps the snapshot on chip.
   void pin_snapshot_in_l2() {
     // (k4_ir1 models: K4 reads K3's f64 IR1 rows instead)
-    const bool ir1_rows = k4_ir1(kind);
-    void* base = ir1_rows ? (void*)ir1.get() : (void*)snap.get();
-    const size_t bytes = ir1_rows ? ir1.bytes() : snap.bytes();
+    const bool rows = use_ir1();
+    void* base = rows ? (void*)ir1.get() : (void*)snap.get();
+    const size_t bytes = rows ? ir1.bytes() : snap.bytes();
     if (!l2_persist || !base) return;
     cudaStreamAttrValue v{};
     v.accessPolicyWindow.base_ptr = base;
@@ -328,7 +343,7 @@ struct lgd_context {
     a.eps = opt.adagrad_epsilon;
     a.w = w.get();
     a.mix = mix.get();
-    a.ir1 = ir1.get();
+    a.ir1 = use_ir1() ? ir1.get() : nullptr;
     a.snap = snap.get();
     a.loss = loss.get();
     a.loss_parts = 0;  // run_batch turns them on where K3 writes them
@@ -372,6 +387,13 @@ struct lgd_context {
     }
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
+    a.seg_mode = seg_rows ? 2 : 0;  // run_batch switches to the bucket's list
+    a.seg_start = seg_start.get();
+    a.batch_seg = batch_seg.get();
+    a.seg_work = seg_work.get();
+    a.seg_nseg = seg_nseg.get();
+    a.seg_temp = seg_temp.get();
+    a.seg_temp_bytes = seg_temp.bytes();
     if (typed() && R && side_stream && r_grad.get()) {  // overlapped relation pass
       a.side = side_stream;
       a.ev_scored = ev_scored;
@@ -487,6 +509,13 @@ struct lgd_context {
       a.rel_bits = bk.rel_bits;  // the payloads were written with the full batch's layout
       a.skeys = const_cast<uint32_t*>(bk.keys) + bucket_item;
       a.svals = const_cast<uint32_t*>(bk.vals) + bucket_item;
+      if (bucket_segs) {  // K4 v2 reads the bucket's segment list
+        a.seg_mode = 1;
+        a.seg_keys = bk.keys;
+        a.seg_vals = bk.vals;
+        a.seg_n = bk.items;
+        a.seg_batch = (uint32_t)(bucket_item / (uint64_t(opt.batch_size) * (k() + 2)));
+      }
     }
     score_bytes_total += score_bytes(P);
     if (rel_grad_out) {  // lock-step rounds: relation gradient only, applied later
@@ -520,6 +549,7 @@ struct lgd_context {
   // negatives and when the keys would not fit 32 bits.
   void presort_bucket(const Pool& pool, uint64_t m, cudaEvent_t* bev) {
     bk = Presorted{};
+    bucket_segs = false;
     if (presort && !chunk() && m) {
       const uint64_t B = opt.batch_size;
       const BatchArgs a = batch_args(shuffled.get(), negs.get(), std::min(B, m), nullptr, &pool);
@@ -544,7 +574,17 @@ struct lgd_context {
         bk.vals = vv[sel];
         bk.mask = a.node_key_bits >= 32 ? 0xffffffffu : (1u << a.node_key_bits) - 1u;
         bk.rel_bits = a.rel_bits;
+        bk.items = items;
         launches += 1 + 2 + (a.node_key_bits + bbits + 7) / 8;
+        if (seg_rows) {  // K4 v2: every batch's segments, listed once for the bucket
+          ensure_segments(items, nb);
+          LGD_CUDA(cudaMemsetAsync(seg_work.get(), 0, nb * sizeof(unsigned int), stream));
+          launch_segment_list(bk.keys, items, a.node_key_bits, (uint32_t)nb, seg_start.get(),
+                              batch_seg.get(), seg_nseg.get(), seg_temp.get(), seg_temp.bytes(),
+                              sm_count, stream);
+          bucket_segs = true;
+          launches += 3;
+        }
       }
     }
     if (bev) LGD_CUDA(cudaEventRecord(bev[3], stream));
@@ -688,6 +728,7 @@ struct lgd_context {
         bk_vals[i].reserve(items);
       }
       bk_temp.reserve(bucket_sort_temp_bytes(items));
+      if (seg_rows) ensure_segments(items, (max_m + opt.batch_size - 1) / opt.batch_size);
     }
     batch_losses.reserve(std::max<uint64_t>(tb, 1));
     if (total_batches) *total_batches = tb;
@@ -734,8 +775,12 @@ struct lgd_context {
   // Trains a list of buckets in order.  host_bucketed: optional host copy
   // (pinned for full speed) of the edges in bucket order; each bucket is then
   // streamed H2D on a side stream, one bucket ahead of the compute.
+  // batch_limit: at most that many batches per bucket (a bounded prefix of the
+  // reference loop, for parity at full scale); node_trace (device, one slot
+  // per batch): the running unique-node counter after every batch.
   void train_items(uint32_t epoch, const std::vector<WorkItem>& items, lgd_epoch_result* out,
-                   const uint32_t* host_bucketed = nullptr) {
+                   const uint32_t* host_bucketed = nullptr, uint64_t batch_limit = ~uint64_t(0),
+                   unsigned long long* node_trace = nullptr) {
     check_ready();
     const auto t0 = std::chrono::steady_clock::now();
     reserve_for(items, nullptr);
@@ -788,13 +833,18 @@ struct lgd_context {
       }
       sample_bucket(it, epoch, m, bev);
       presort_bucket(it.pool, m, bev);
-      for (uint64_t o = 0; o < m; o += opt.batch_size) {
+      uint64_t done = 0;
+      for (uint64_t o = 0, b = 0; o < m && b < batch_limit; o += opt.batch_size, ++b) {
         const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
         run_batch(shuffled.get() + 3 * o, negs.get() + (o / opt.batch_size) * batch_negs(opt.batch_size),
                   P, batch_losses.get() + nb, &it.pool, nullptr, nullptr, o * (k() + 2));
+        if (node_trace)
+          LGD_CUDA(cudaMemcpyAsync(node_trace + nb, counters.get(), sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToDevice, stream));
         ++nb;
+        done += P;
       }
-      edges_trained += m;
+      edges_trained += done;
       ++buckets;
     }
     fill_result(out, nb, edges_trained, buckets, h2d_bytes, t0);
@@ -981,6 +1031,8 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
         cudaGetLastError();  // the set-aside is an optimisation only
       }
       if (const char* env = std::getenv("LGD_PRESORT")) c->presort = std::strtol(env, nullptr, 10) != 0;
+      if (const char* env = std::getenv("LGD_K4")) c->seg_rows = std::strtol(env, nullptr, 10) != 1;
+      if (const char* env = std::getenv("LGD_K4_IR1")) c->ir1_rows = std::strtol(env, nullptr, 10) != 0;
       LGD_CUDA(cudaEventCreate(&c->ev_begin));
       LGD_CUDA(cudaEventCreate(&c->ev_end));
       LGD_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -1389,6 +1441,31 @@ int lgd_train_buckets(lgd_context* ctx, uint32_t epoch, uint64_t g_begin, uint64
   });
 }
 
+int lgd_train_bucket_prefix(lgd_context* ctx, uint32_t epoch, uint64_t g, uint64_t max_batches,
+                            double* batch_losses, uint64_t* batch_nodes, lgd_epoch_result* out) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    DeviceGuard dg(ctx->device);
+    ctx->fence_stores();
+    ctx->check_ready();
+    if (g >= ctx->plan.bucket_order.size()) throw std::invalid_argument("bucket position out of range");
+    const uint64_t limit = max_batches ? max_batches : ~uint64_t(0);
+    const auto items = ctx->plan_items(g, g + 1);
+    const uint64_t m = ctx->bucket_size(items[0]);
+    const uint64_t nb = std::min<uint64_t>(limit, (m + ctx->opt.batch_size - 1) / ctx->opt.batch_size);
+    DevBuf<unsigned long long> trace;
+    trace.reserve(std::max<uint64_t>(nb, 1));
+    ctx->train_items(epoch, items, out, ctx->host_edges, limit, batch_nodes ? trace.get() : nullptr);
+    if (batch_losses && nb)
+      LGD_CUDA(cudaMemcpy(batch_losses, ctx->batch_losses.get(), nb * 8, cudaMemcpyDeviceToHost));
+    if (batch_nodes && nb) {
+      std::vector<unsigned long long> c(nb);
+      LGD_CUDA(cudaMemcpy(c.data(), trace.get(), nb * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t b = 0; b < nb; ++b) batch_nodes[b] = c[b] - (b ? c[b - 1] : 0);
+    }
+  });
+}
+
 int lgd_round_schedule(uint32_t n, uint64_t capacity, uint64_t* count, lgd_bucket_item* items,
                        uint32_t* num_rounds, uint32_t* pairs_per_round) {
   return guarded([&] {
@@ -1468,6 +1545,10 @@ int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device) {
 int lgd_get_stream(lgd_context* ctx, void** cuda_stream) {
   return guarded([&] {
     if (!ctx || !cuda_stream) throw std::invalid_argument("null argument");
+    DeviceGuard g(ctx->device);
+    // work the caller queues on this stream is ordered after pending
+    // asynchronous write-backs, like the library's own table writes
+    ctx->fence_stores();
     *cuda_stream = (void*)ctx->stream;
   });
 }
@@ -1656,23 +1737,42 @@ int lgd_evaluate(lgd_context* ctx, const uint32_t* test_edges, uint64_t count,
       if (s >= ctx->V || d >= ctx->V) throw std::out_of_range("node is not resident");
     }
     DeviceGuard g(ctx->device);
+    if (eval_smem_bytes(ctx->dim) > 227 * 1024) throw std::invalid_argument("dimension too large for evaluate");
+    // candidates in tiles of test edges: scratch <= 256 MB whatever the count
+    const uint64_t tile = std::max<uint64_t>(1, std::min<uint64_t>(count, (64ull << 20) / num_candidates));
     DevBuf<uint32_t> dedges, cand;
-    DevBuf<double> rr, hit, res;
+    DevBuf<double> rr, hit;
     dedges.reserve(count * 3);
-    cand.reserve(count * num_candidates);
+    cand.reserve(tile * num_candidates);
     rr.reserve(count);
     hit.reserve(count);
-    res.reserve(2);
     LGD_CUDA(cudaMemcpyAsync(dedges.get(), test_edges, count * 12, cudaMemcpyHostToDevice,
                              ctx->stream));
     EvalArgs a{ctx->kind, ctx->dim, ctx->theta.get(), ctx->rel_theta.get(), dedges.get(), count,
-               num_candidates, hits_k, ctx->V, seed, cand.get(), rr.get(), hit.get(), res.get()};
-    launch_evaluate(a, ctx->stream);
-    double h[2];
-    LGD_CUDA(cudaMemcpyAsync(h, res.get(), 16, cudaMemcpyDeviceToHost, ctx->stream));
+               num_candidates, hits_k, ctx->V, seed, cand.get(), rr.get(), hit.get()};
+    if (ctx->profiling) LGD_CUDA(cudaEventRecord(ctx->ev_begin, ctx->stream));
+    for (uint64_t t0 = 0; t0 < count; t0 += tile) {
+      launch_evaluate_tile(a, t0, std::min(tile, count - t0), ctx->stream);
+      ctx->launches += 2;
+    }
+    if (ctx->profiling) LGD_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
+    std::vector<double> hr(count), hh(count);
+    LGD_CUDA(cudaMemcpyAsync(hr.data(), rr.get(), count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    LGD_CUDA(cudaMemcpyAsync(hh.data(), hit.get(), count * 8, cudaMemcpyDeviceToHost, ctx->stream));
     LGD_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (mrr) *mrr = h[0];
-    if (hits_at_k) *hits_at_k = h[1];
+    if (ctx->profiling) {
+      float ms = 0;
+      LGD_CUDA(cudaEventElapsedTime(&ms, ctx->ev_begin, ctx->ev_end));
+      ctx->eval_ms = ms;
+    }
+    // result.mrr / hits_at_k accumulate in edge order, then / edges (train.cpp:406-411)
+    double m = 0.0, hk = 0.0;
+    for (uint64_t t = 0; t < count; ++t) {
+      m += hr[t];
+      hk += hh[t];
+    }
+    if (mrr) *mrr = m / (double)count;
+    if (hits_at_k) *hits_at_k = hk / (double)count;
   });
 }
 

@@ -18,12 +18,13 @@ struct EvalArgs {
   uint32_t hits_k;
   uint64_t V;
   uint64_t seed;
-  uint32_t* cand;       // T x ncand scratch
-  double* rr;           // T scratch
-  double* hit;          // T scratch
-  double* out;          // [mrr, hits]
+  uint32_t* cand;       // tile x ncand scratch
+  double* rr;           // T reciprocal ranks
+  double* hit;          // T hits (0 / 1)
 };
 
-void launch_evaluate(const EvalArgs& a, cudaStream_t st);
+// test edges [t0, t0 + T): candidates then scores (rr, hit at index t)
+void launch_evaluate_tile(const EvalArgs& a, uint64_t t0, uint64_t T, cudaStream_t st);
+size_t eval_smem_bytes(uint32_t dim);
 
 }  // namespace lgd

@@ -3,6 +3,7 @@
 // ids, the gather of edges into bucket order, and the synthetic power-law
 // generator used for the benchmark shapes.
 #include "common.cuh"
+#include "detmath.cuh"
 #include "internal.hpp"
 #include "rng.cuh"
 
@@ -40,17 +41,19 @@ __global__ void gather3_kernel(const uint32_t* __restrict__ edges, const uint32_
 // x = (1 + u (V^(1-beta) - 1))^(1/(1-beta))); alpha = 2.3 gives the top node
 // ~0.3% of all endpoints, about Twitter's largest in-degree share.  Ranks are
 // scattered over ids by a multiplicative permutation mod V so hubs land in
-// every partition.  Relations are uniform over [0, R).
+// every partition.  Relations are uniform over [0, R).  pow() is det_pow
+// (detmath.cuh): IEEE-exact operations only, so the host restatement
+// (oracle/legend_oracle.c: lo_powerlaw_edges) reproduces every edge.
 __global__ void powerlaw_kernel(uint64_t V, uint64_t R, uint64_t E, double inv_one_minus_beta,
                                 uint64_t mult, uint64_t seed, uint32_t* __restrict__ edges) {
-  const double span = pow((double)V, 1.0 / inv_one_minus_beta) - 1.0;
+  const double span = det_pow((double)V, 1.0 / inv_one_minus_beta) - 1.0;
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   uint64_t s = seed ^ (e * 0xd1342543de82ef95ull);
   const uint64_t a = splitmix64(s), b = splitmix64(s), c = splitmix64(s);
   auto endpoint = [&](uint64_t r) -> uint32_t {
     const double u = (double)(r >> 11) * 0x1.0p-53;
-    uint64_t rank = (uint64_t)pow(1.0 + u * span, inv_one_minus_beta) - 1;
+    uint64_t rank = (uint64_t)det_pow(1.0 + u * span, inv_one_minus_beta) - 1;
     if (rank >= V) rank = V - 1;
     // (rank * mult) mod V without overflow: 128-bit product
     const uint64_t lo = rank * mult;

@@ -30,6 +30,8 @@
 // FP64 expressions are compiled with -fmad=false so products and sums round
 // exactly like the reference's unfused x86-64 double arithmetic.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "adagrad.cuh"
 #include "common.cuh"
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         const double xr = sr * rr - si * ri, xi = sr * ri + si * rr;
         ir1[j] = xr;
         ir1[j + h] = xi;
-        if (k4_ir1(KIND)) {
+        if (k4_ir1(KIND) && a.ir1) {
           a.ir1[p * d + j] = xr;
           a.ir1[p * d + j + h] = xi;
         }
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         }
         *reinterpret_cast<double2*>(ir1 + i) = make_double2(u0, u1);
         *reinterpret_cast<double2*>(ir1 + i + 2) = make_double2(u2, u3);
-        if (k4_ir1(KIND)) {
+        if (k4_ir1(KIND) && a.ir1) {
           *reinterpret_cast<double2*>(a.ir1 + p * d + i) = make_double2(u0, u1);
           *reinterpret_cast<double2*>(a.ir1 + p * d + i + 2) = make_double2(u2, u3);
         }
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
         ir1[i] = KIND == 0   ? (double)srow[i]
                  : KIND == 3 ? (double)srow[i] + (double)rrow[i]
                              : (double)srow[i] * (double)rrow[i];
-        if (k4_ir1(KIND)) a.ir1[p * d + i] = ir1[i];
+        if (k4_ir1(KIND) && a.ir1) a.ir1[p * d + i] = ir1[i];
       }
       for (uint32_t i = lane; i < d; i += 32) a.snap[p * d + i] = srow[i];
     }
@@ -937,7 +939,7 @@ struct SegCtx {  // hoisted kernel arguments
   const float* gneg;  // shared-negative mode: gradient rows of the shared negatives
 };
 
-template <int KIND, int NV, bool REL, bool SH>
+template <int KIND, int NV, bool REL, bool SH, bool IR1 = k4_ir1(KIND)>
 __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>& L, uint32_t val,
                                           bool pred, ItemRegs<4 * NV>& it) {
   if (REL) {
@@ -962,7 +964,7 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   it.w = (pred && slot - 1u < x.k) ? __ldg(x.w + (uint64_t)p * x.k + (slot - 1))
          : (KIND == 3 && pred && slot == 0) ? __ldg(x.w + x.cpos_off + p) : -1.0;
   const uint64_t row = (uint64_t)p * x.d;
-  if (k4_ir1(KIND) && !SH) {
+  if (IR1 && !SH) {
     // dst / negative: IR1 as K3 formed it; src: mix (both f64 rows)
     L.ldd((is_src ? x.mix : x.ir1) + row, pred, it.mv);
     if (is_src) it.rel = x.rmask ? (val >> x.sbits) & x.rmask : (pred ? __ldg(x.rel_keys + p) : 0);
@@ -974,7 +976,7 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   L.ldd(x.mix + row, pred && is_src, it.mv);
 }
 
-template <int KIND, int NV, bool REL, bool SH>
+template <int KIND, int NV, bool REL, bool SH, bool IR1 = k4_ir1(KIND)>
 __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV>& L,
                                            const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
                                            const float* own) {
@@ -984,7 +986,7 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
     for (int e = 0; e < NE; ++e) acc[e] += (double)it.sv[e];
     return;
   }
-  if (k4_ir1(KIND) && !REL && !SH && it.slot <= k) {  // dst / negative from K3's IR1
+  if (IR1 && !REL && !SH && it.slot <= k) {  // dst / negative from K3's IR1
 #pragma unroll
     for (int e = 0; e < NE; ++e) acc[e] += KIND == 3 ? it.w * (it.mv[e] - (double)own[e]) : it.w * it.mv[e];
     return;
@@ -1261,6 +1263,138 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
   }
 }
 
+// ------------------------------------- K4 v2: segment-list row updates
+// The sorted contributions' segment heads (one per unique node) are listed
+// once per bucket (launch_segment_list: a stable select of the head
+// positions, then each batch's first segment), so the update kernel walks
+// whole segments: a persistent warp claims 32 consecutive segments at a time
+// (one atomic), loads their bounds and keys lane-parallel, and for each
+// segment in order sums ALL its contributions sequentially in FP64 -- the
+// reference's exact std::map accumulation order (train.cpp:290-333), hubs
+// included, so no per-chunk partial sums or second pass -- then runs the
+// Adagrad row update (train.cpp:342-354).  The theta / state rows of the
+// next kSegDepth segments are in flight in the warp's cp.async ring, as in
+// segment_pass1_vec; the contribution payloads of the group come from two
+// 32-item register windows.  No chunk-edge bookkeeping, no atomics on rows.
+template <int KIND, int NV, bool SH, bool IR1>
+__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_rows(
+    BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+    uint64_t n_items, const uint32_t* __restrict__ seg_start,
+    const uint32_t* __restrict__ batch_seg, uint32_t batch, unsigned int* __restrict__ work) {
+  constexpr int NE = 4 * NV;
+  const int lane = threadIdx.x & 31;
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G};
+  float* __restrict__ theta = a.theta;
+  float* __restrict__ state = a.state;
+  const uint64_t d = a.dim;
+  const double lr = a.lr, eps = a.eps;
+  const uint32_t s_begin = batch_seg[batch], s_end = batch_seg[batch + 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(a.counters, (unsigned long long)(s_end - s_begin));
+  extern __shared__ __align__(16) float seg_ring[];
+  const uint32_t rowf = (a.dim + 3) & ~3u;
+  const uint32_t slotf = 2 * rowf;  // slot: theta, state
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
+                        (threadIdx.x >> 5) * kSegDepth * slotf * 4;  // bytes
+  const uint32_t ring_end = ring + kSegDepth * slotf * 4;
+  for (;;) {
+    uint32_t g0 = 0;
+    if (lane == 0) g0 = atomicAdd(work + batch, 32u);
+    g0 = __shfl_sync(0xffffffffu, g0, 0) + s_begin;
+    if (g0 >= s_end) break;
+    const int ns = (int)min(32u, s_end - g0);
+    // lane l: segment g0 + l -- first item, length, table row
+    uint32_t my_st = 0, my_len = 0, my_row = 0;
+    if (lane < ns) {
+      my_st = __ldg(seg_start + g0 + lane);
+      my_len = __ldg(seg_start + g0 + lane + 1) - my_st;
+      my_row = from_pool(a, __ldg(skeys + my_st));
+    }
+    // payload windows: items [i0, i0 + 64) of the group
+    const uint32_t i0 = __shfl_sync(0xffffffffu, my_st, 0);
+    const uint32_t w0 = i0 + lane < n_items ? __ldg(svals + i0 + lane) : 0u;
+    const uint32_t w1 = i0 + 32 + lane < n_items ? __ldg(svals + i0 + 32 + lane) : 0u;
+    auto item = [&](uint32_t q) {
+      const uint32_t o = q - i0;
+      const uint32_t v0 = __shfl_sync(0xffffffffu, w0, o & 31);
+      const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
+      return o < 32 ? v0 : (o < 64 ? v1 : __ldg(svals + q));
+    };
+    auto stage = [&](int j, uint32_t slot) {
+      const uint32_t r = __shfl_sync(0xffffffffu, my_row, j & 31);
+      if (j < ns) {
+        const uint64_t off = (uint64_t)r * d;
+        L.cpa_s(slot, theta + off, true);
+        L.cpa_s(slot + rowf * 4, state + off, true);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int u = 0; u < kSegDepth; ++u) stage(u, ring + u * slotf * 4);
+    uint32_t slot = ring;
+#pragma unroll 1
+    for (int j = 0; j < ns; ++j) {
+      const uint32_t sj = __shfl_sync(0xffffffffu, my_st, j);
+      const uint32_t lj = __shfl_sync(0xffffffffu, my_len, j);
+      const uint32_t row = __shfl_sync(0xffffffffu, my_row, j);
+      ItemRegs<NE> cit;
+      load_item<KIND, NV, false, SH, IR1>(x, L, item(sj), true, cit);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
+      float th[NE], st[NE];
+      L.lds_s(slot, th);
+      L.lds_s(slot + rowf * 4, st);
+      double acc[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+      add_loaded<KIND, NV, false, SH, IR1>(x, L, cit, x.k, acc, th);
+      for (uint32_t q = sj + 1; q < sj + lj; ++q) {
+        ItemRegs<NE> it;
+        load_item<KIND, NV, false, SH, IR1>(x, L, item(q), true, it);
+        add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, th);
+      }
+      adagrad_lanes(L, acc, th, st, lr, eps);
+      L.stf(theta + (uint64_t)row * d, th);
+      L.stf(state + (uint64_t)row * d, st);
+      stage(j + kSegDepth, slot);  // the slot just read is free again
+      slot = slot + slotf * 4 == ring_end ? ring : slot + slotf * 4;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+}
+
+// Segment heads of sorted keys: flag i starts a segment when it is the first
+// item or its key differs from the previous one.
+struct HeadFlag {
+  const uint32_t* keys;
+  __host__ __device__ __forceinline__ bool operator()(const uint32_t& i) const {
+    return i == 0 || keys[i] != keys[i - 1];
+  }
+};
+
+// batch_seg[b] = first segment of batch b (the key's bits above `shift`);
+// batch_seg[nb] = nseg and seg_start[nseg] = n close the last ranges
+__global__ void batch_seg_kernel(const uint32_t* __restrict__ keys, uint64_t n,
+                                 uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ nseg_p,
+                                 int shift, uint32_t nb, uint32_t* __restrict__ batch_seg) {
+  const uint32_t nseg = *nseg_p;
+  auto bat = [&](uint32_t s) -> uint32_t {
+    return shift >= 32 ? 0u : keys[seg_start[s]] >> shift;
+  };
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
+    const uint32_t b = bat(s);
+    const uint32_t pb = s ? bat(s - 1) + 1 : 0u;
+    for (uint32_t bb = pb; bb <= b; ++bb) batch_seg[bb] = s;
+    if (s == nseg - 1) {
+      for (uint32_t bb = b + 1; bb <= nb; ++bb) batch_seg[bb] = nseg;
+      seg_start[nseg] = (uint32_t)n;
+    }
+  }
+}
+
 // ----------------------------------------------------------- dispatchers
 // score_kernel<KIND> is shared by every (dim, k): its dynamic-smem attribute
 // only grows; occupancy is cached per smem size.  (Host-side, per process.)
@@ -1309,9 +1443,66 @@ void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStr
     launch_vec_pass1_<KIND, NV, REL, SH, false>(a, items, grid, st);
 }
 
+template <int KIND, int NV, bool SH, bool IR1>
+void launch_segment_rows_(const BatchArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
+  static size_t attr[kMaxDevices];
+  static int occ[kMaxDevices];
+  static size_t occ_smem[kMaxDevices];
+  const int dev = current_device();
+  if (smem > attr[dev]) {
+    LGD_CUDA(cudaFuncSetAttribute(segment_rows<KIND, NV, SH, IR1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[dev] = smem;
+  }
+  if (occ_smem[dev] != smem) {
+    LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ[dev], segment_rows<KIND, NV, SH, IR1>, kSegThreads, smem));
+    occ_smem[dev] = smem;
+  }
+  const unsigned grid = (unsigned)std::max(1, occ[dev]) * (unsigned)a.sm_count;
+  segment_rows<KIND, NV, SH, IR1><<<grid, kSegThreads, smem, st>>>(
+      a, a.seg_keys, a.seg_vals, a.seg_n, a.seg_start, a.batch_seg, a.seg_batch, a.seg_work);
+  LGD_LAUNCH_CHECK();
+}
+
+// K4 v2 for the node pass when the dimension has vector lanes; the segment
+// list is the bucket's (presorted) or built here for this batch's own sort.
+// ComplEx / TransE read K3's IR1 rows when the context keeps them (a.ir1),
+// else recombine the snapshot with the relation row (same bits).
+template <int KIND, bool SH>
+bool segment_rows_node_pass(BatchArgs& a, uint64_t items, cudaStream_t st) {
+  if (!a.seg_mode) return false;
+  const int nv = vec_width<KIND>(a.dim);
+  if (nv == 0 || (KIND == 3 && SH)) return false;
+  if (a.seg_mode == 2) {  // this batch's sort: a one-batch list
+    a.seg_keys = a.skeys;
+    a.seg_vals = a.svals;
+    a.seg_n = items;
+    a.seg_batch = 0;
+    LGD_CUDA(cudaMemsetAsync(a.seg_work, 0, sizeof(unsigned int), st));
+    launch_segment_list(a.skeys, items, 32, 1, a.seg_start, a.batch_seg, a.seg_nseg, a.seg_temp,
+                        a.seg_temp_bytes, a.sm_count, st);
+  }
+  if constexpr (KIND != 3 || !SH) {
+    constexpr bool kIr1 = k4_ir1(KIND) && !SH;
+    const bool ir1 = kIr1 && a.ir1 != nullptr;
+    if (nv == 1) {
+      if (ir1) launch_segment_rows_<KIND, 1, SH, kIr1>(a, st);
+      else launch_segment_rows_<KIND, 1, SH, false>(a, st);
+    } else {
+      if (ir1) launch_segment_rows_<KIND, 2, SH, kIr1>(a, st);
+      else launch_segment_rows_<KIND, 2, SH, false>(a, st);
+    }
+  }
+  return true;
+}
+
 // shared-negative mode: node items are dst / shared negative / src (slots 0-2)
 template <int KIND>
-void run_segments_shared(const BatchArgs& a, uint64_t items, cudaStream_t st) {
+void run_segments_shared(const BatchArgs& a_in, uint64_t items, cudaStream_t st) {
+  BatchArgs a = a_in;
+  if (segment_rows_node_pass<KIND, true>(a, items, st)) return;
   LGD_CUDA(cudaMemsetAsync(a.span_count, 0, sizeof(unsigned int), st));
   const unsigned grid = ceil_div(ceil_div(items, 32), kSegThreads / 32);
   const int nv = vec_width<KIND>(a.dim);
@@ -1479,7 +1670,8 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   if (a.side) rel_pass_start<KIND, NC>(a, st);
   if (!a.presorted) sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
   rec(2);
-  run_segments<KIND, NC>(a, P * (k + 2), false, st);
+  if (a.grad_nodes || !segment_rows_node_pass<KIND, false>(a, P * (k + 2), st))
+    run_segments<KIND, NC>(a, P * (k + 2), false, st);
   rec(3);
   if (KIND == 0 && a.side) {
     // the next batch's K3 rewrites the per-positive losses
@@ -1626,6 +1818,35 @@ void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* ke
   const uint64_t blocks = ceil_div(n, 256);
   const unsigned grid = (unsigned)(blocks < (uint64_t)a.sm_count * 16 ? blocks : (uint64_t)a.sm_count * 16);
   presort_keys_kernel<<<grid, 256, 0, st>>>(a, m, B, keys, vals);
+  LGD_LAUNCH_CHECK();
+}
+
+int k4_vec_width(int kind, uint32_t dim) {
+  switch (kind) {
+    case 0: return vec_width<0>(dim);
+    case 1: return vec_width<1>(dim);
+    case 2: return vec_width<2>(dim);
+    default: return vec_width<3>(dim);
+  }
+}
+
+size_t segment_list_temp_bytes(uint64_t max_items) {
+  size_t bytes = 0;
+  LGD_CUDA(cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<uint32_t>(0),
+                                 (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                 (int64_t)(max_items ? max_items : 1), HeadFlag{nullptr}));
+  return bytes;
+}
+
+void launch_segment_list(const uint32_t* keys, uint64_t n, int shift, uint32_t nb,
+                         uint32_t* seg_start, uint32_t* batch_seg, uint32_t* nseg, void* temp,
+                         size_t temp_bytes, int sm_count, cudaStream_t st) {
+  if (!n) return;
+  size_t bytes = temp_bytes;
+  LGD_CUDA(cub::DeviceSelect::If(temp, bytes, thrust::counting_iterator<uint32_t>(0), seg_start,
+                                 nseg, (int64_t)n, HeadFlag{keys}, st));
+  batch_seg_kernel<<<(unsigned)sm_count * 4, 256, 0, st>>>(keys, n, seg_start, nseg, shift, nb,
+                                                           batch_seg);
   LGD_LAUNCH_CHECK();
 }
 

@@ -38,7 +38,8 @@ struct BatchArgs {
   // scratch (sized for the largest batch)
   double* w;                  // P x k softmax weights
   double* mix;                // P x d  sum_j w_j neg_j - dst
-  double* ir1;                // P x d  IR1 = combine(src, rel) (typed models; K4's dst / negative items)
+  double* ir1;                // P x d  IR1 = combine(src, rel): written by K3 and read by K4's dst /
+                              // negative items when non-null (k4_ir1 models, vector-lane dims)
   float* snap;                // P x d  pre-update source rows
   double* loss;               // per-positive loss: P values (shared mode), or K3's
                               // parts f_pos | row_max | sum (3 x P, loss_parts)
@@ -97,6 +98,20 @@ struct BatchArgs {
   // only K3's outputs, so its sort and segmented sums overlap the node pass;
   // the relation rows are updated after K4, which reads them pre-update.
   // side == nullptr: sequential relation pass.
+  // K4 v2 (segment_rows): 0 = chunked pass 1 / pass 2; 1 = the bucket's
+  // segment list is ready (seg_keys / seg_vals = the bucket's sorted arrays,
+  // batch seg_batch); 2 = build a one-batch list after this batch's sort
+  int seg_mode;
+  const uint32_t* seg_keys;
+  const uint32_t* seg_vals;
+  uint64_t seg_n;             // items in seg_keys
+  uint32_t* seg_start;        // segment s starts at item seg_start[s]; [nseg] = seg_n
+  uint32_t* batch_seg;        // first segment of each batch, [nb] = nseg
+  uint32_t seg_batch;
+  unsigned int* seg_work;     // per-batch work counters (zeroed)
+  uint32_t* seg_nseg;         // device segment count
+  void* seg_temp;
+  size_t seg_temp_bytes;
   cudaStream_t side;
   cudaEvent_t ev_scored, ev_rel;
   uint64_t num_rels;
@@ -136,6 +151,17 @@ size_t batch_sort_temp_bytes(uint64_t max_items);
 void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* keys,
                         uint32_t* vals, cudaStream_t st);
 size_t bucket_sort_temp_bytes(uint64_t max_items);
+// Segment list of sorted keys (K4 v2): seg_start = item positions where the
+// key changes (n + 1 entries with the closing n), batch_seg[b] = first
+// segment whose key has batch bits (above `shift`; 32 = one batch) b, for
+// b < nb, and batch_seg[nb] = nseg.  nseg: device count.
+size_t segment_list_temp_bytes(uint64_t max_items);
+// 16-byte vectors per lane of K4's vector kernels for (kind, dim); 0 = the
+// 8-lane-group fallback (which never reads K3's IR1 rows)
+int k4_vec_width(int kind, uint32_t dim);
+void launch_segment_list(const uint32_t* keys, uint64_t n, int shift, uint32_t nb,
+                         uint32_t* seg_start, uint32_t* batch_seg, uint32_t* nseg, void* temp,
+                         size_t temp_bytes, int sm_count, cudaStream_t st);
 int sort_bucket(void* temp, size_t temp_bytes, uint32_t* keys[2], uint32_t* vals[2],
                 uint64_t items, int key_bits, cudaStream_t st);
 size_t score_smem_bytes(uint32_t dim, uint32_t k);

@@ -100,6 +100,10 @@ def library():
         "lgd_train_epoch": (i32, [vp, u32, vp]),
         "lgd_train_buckets": (i32, [vp, u32, u64, u64, vp]),
         "lgd_train_buckets_from_host": (i32, [vp, u32, u64, u64, vp, vp]),
+        "lgd_train_bucket_prefix": (i32, [vp, u32, u64, u64, vp, vp, vp]),
+        "lgd_write_graph": (i32, [C.c_char_p, vp, u64, u64, u64]),
+        "lgd_read_graph_meta": (i32, [C.c_char_p, vp, vp, vp]),
+        "lgd_read_graph": (i32, [C.c_char_p, vp, u64]),
         "lgd_round_schedule": (i32, [u32, u64, vp, vp, vp, vp]),
         "lgd_train_items": (i32, [vp, u32, vp, u64, vp]),
         "lgd_set_host_edges": (i32, [vp, vp]),
@@ -309,6 +313,23 @@ def shuffle_permutation(seed, m, device=0):
     return perm[:m], int(used[0])
 
 
+def write_graph(directory, edges, num_nodes, num_relations=0):
+    """write_graph (graph.cpp:152-171): edges.bin + graph_meta.json (host only)."""
+    edges = _u32(edges, 3)
+    _check(library().lgd_write_graph(os.fsencode(directory), _p(edges), len(edges), num_nodes,
+                                     num_relations))
+
+
+def read_graph(directory):
+    """read_graph (graph.cpp:173-192): (edges [E x 3] u32, num_nodes, num_relations)."""
+    E, V, R = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    d = os.fsencode(directory)
+    _check(library().lgd_read_graph_meta(d, C.byref(E), C.byref(V), C.byref(R)))
+    edges = np.zeros((E.value, 3), np.uint32)
+    _check(library().lgd_read_graph(d, _p(edges), E.value))
+    return edges, V.value, R.value
+
+
 class _CudaArray:
     """__cuda_array_interface__ shim: wraps a device pointer of f32 values."""
 
@@ -507,6 +528,21 @@ class Trainer:
         r = _EpochResult()
         _check(library().lgd_train_buckets(self._h, epoch, g_begin, g_end, C.byref(r)))
         return EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
+
+    def train_bucket_prefix(self, epoch, g, max_batches=0):
+        """The bucket at plan position g, cut after max_batches batches (0 =
+        all): returns (EpochResult, per-batch losses, per-batch unique nodes)."""
+        sizes = np.diff(np.asarray(self.bucket_offsets, np.int64))
+        cap = int(-(-sizes.max() // self.options.batch_size)) if len(sizes) else 0
+        if max_batches:
+            cap = min(cap, max_batches)
+        losses = np.zeros(max(cap, 1), np.float64)
+        nodes = np.zeros(max(cap, 1), np.uint64)
+        r = _EpochResult()
+        _check(library().lgd_train_bucket_prefix(self._h, epoch, g, max_batches, _p(losses),
+                                                 _p(nodes), C.byref(r)))
+        res = EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
+        return res, losses[:res.batches], nodes[:res.batches]
 
     def train_buckets_from_host(self, epoch, g_begin, g_end, host_bucketed) -> EpochResult:
         """train_buckets with each bucket's edges copied H2D from host memory."""

@@ -481,3 +481,68 @@ def test_async_store_overlaps_eval_and_orders_before_training(kind):
     t.close()
     for b in bufs:
         b.free()
+
+
+# ------------------------------------------- K4 v2: segment-list row updates
+def _hub_graph(rng, V, R, E):
+    src = rng.integers(0, V, E)
+    dst = rng.integers(0, V, E)
+    dst[rng.random(E) < 0.25] = 11  # a hub: segments of thousands of contributions
+    src[rng.random(E) < 0.10] = 12
+    return np.stack([src, rng.integers(0, max(R, 1), E), dst], 1).astype(np.uint32)
+
+
+@pytest.mark.parametrize("kind", ALL_KINDS)
+def test_k4_segment_rows_sum_hubs_in_reference_order(oracle, kind, monkeypatch):
+    """K4 v2 (segment_rows, the default) sums every segment -- hubs included --
+    sequentially in the reference's std::map order, so its tables match the
+    restatement to the last bit except where K3's exp / log ulps differ; the
+    chunked kernels (LGD_K4=1) add per-chunk partials for hubs.  Both stay
+    within the stated tolerance."""
+    rng = np.random.default_rng(21)
+    V, R, d, Ecnt, n, k, B = 4000, 6, 36 if kind != "complex" else 40, 40000, 4, 8, 3000
+    R = R if kind != "dot" else 0
+    edges = _hub_graph(rng, V, R, Ecnt)
+    if not R:
+        edges[:, 1] = 0xFFFFFFFF
+    plan = lgd.plan_iteration_order(n).as_dict()
+    E0, S0, rE0, rS0 = oracle.store_init(n, V, d, R, 5)
+    want = oracle.run_epoch(edges, V, R, n, plan, kind, E0, S0, rE0, rS0, dim=d, batch_size=B,
+                            k=k, seed=42, dumps=True)
+    same = {}
+    for mode in ("2", "1"):
+        monkeypatch.setenv("LGD_K4", mode)
+        t = make_trainer(kind, d, V, R, edges, n, k=k, batch=B)
+        t.init_store(5)
+        res = t.run_epoch(0)
+        assert res.unique_nodes == int(want["batch_nodes"].sum())
+        assert res.loss_sum == pytest.approx(want["loss_sum"], rel=1e-12)
+        Eg, Sg = t.tables()
+        assert_tables_close(Eg, E0, f"E K4={mode}")
+        assert_tables_close(Sg, S0, f"S K4={mode}")
+        same[mode] = np.mean(Eg == E0)
+        t.close()
+    assert same["2"] >= 0.999, same
+    assert same["2"] >= same["1"], same
+
+
+@pytest.mark.parametrize("kind", ["complex", "transe"])
+def test_k4_ir1_rows_equal_snapshot_recombination(kind, monkeypatch):
+    """ComplEx / TransE: K4 reading K3's FP64 IR1 rows (default) and K4
+    recombining the src snapshot with the relation row (LGD_K4_IR1=0) form
+    the same expression, so losses, counts and tables are bit-identical."""
+    rng = np.random.default_rng(13)
+    V, R, d, Ecnt, n = 2500, 5, 16, 50000, 4
+    edges = _hub_graph(rng, V, R, Ecnt)
+    runs = []
+    for ir1 in ("1", "0"):
+        monkeypatch.setenv("LGD_K4_IR1", ir1)
+        t = make_trainer(kind, d, V, R, edges, n, k=8, batch=700)
+        t.init_store(5)
+        res = t.run_epoch(0)
+        runs.append((res, t.tables(), t.get_relations()))
+        t.close()
+    (ra, (Ea, Sa), rela), (rb, (Eb, Sb), relb) = runs
+    assert ra.loss_sum == rb.loss_sum and ra.unique_nodes == rb.unique_nodes
+    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    assert np.array_equal(rela[0], relb[0]) and np.array_equal(rela[1], relb[1])
