@@ -278,65 +278,60 @@ def reference_arm(args, cfg, rank):
 
 
 def bench_rounds(args, cfg, rank, world, local, pg):
-    """N GPUs: the partition-round schedule.  A step is one
-    round: NVLink hand-off of the partitions that change owner, then every
-    rank's buckets of the round (lock-step NCCL relation sums for typed
-    models).  Total work per step is one round, so scaling is strong."""
+    """The partition-round schedule on N GPUs, through the C++
+    runner (rounds.cu: lgd_train_round): a step is one round -- every rank's
+    buckets of the round, then the next round's partition hand-offs as NVLink
+    pulls on a side stream (overlapped with the buckets that do not touch the
+    moving partitions), lock-step NCCL relation sums for typed models.  Total
+    work per step is one round, so scaling is strong; N = 1 runs the same
+    schedule on one rank (no hand-offs)."""
     import torch
-    import torch.distributed as dist
-
     from paper_2505_09258_b200 import multigpu as mg
     t_setup = time.perf_counter()
     t = setup_trainer(cfg, local)
-    sched = mg.Schedule.build(cfg["n"], world)
-    if pg is None:  # 1 GPU forced onto the round schedule: a trivial comm
-        class _Solo:
-            rank, world = 0, 1
-            stream_ordered = True  # lock-step batches without host drains
-
-            def all_reduce_sum(self, x, drain=True):
-                pass
-
-            def all_reduce_max_int(self, v):
-                return v
-
-            def exchange(self, moves, views):
-                pass
-        comm = _Solo()
-    else:
-        comm = mg.DistComm(dist, torch.device("cuda", local))
-    rel_buf = (torch.zeros((max(cfg["rels"], 1), cfg["dim"] + 1), dtype=torch.float64,
-                           device=f"cuda:{local}") if cfg["rels"] else None)
-    cur = mg.RoundCursor(sched)
+    uid = None
+    if world > 1:
+        box = [mg.NativeRounds.unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(box, src=0)
+        uid = box[0]
+    runner = mg.NativeRounds(t, rank, world, uid)
+    R = runner.num_rounds
     setup_s = time.perf_counter() - t_setup
+    unit = [0]
+
+    def step():
+        e, r = divmod(unit[0], R)
+        unit[0] += 1
+        return runner.run(e, r)
+
     for _ in range(args.warmup):
-        e, r, moves = cur.next()
-        mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+        step()
     t.reset_kernel_stats()
     t.set_profiling(True)
     clocks = Clocks(local)
     clocks.start()
     barrier(pg)
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    edges = 0
-    algo = 0.0
+    edges = algo = 0.0
+    dev_ms = handoff_ms = 0.0
+    handoff_bytes = 0
     for _ in range(args.steps):
-        e, r, moves = cur.next()
-        res = mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+        res, ms, nbytes = step()
         edges += res.edges_trained
         algo += res.algorithmic_bytes
-    ev1.record()
+        dev_ms += res.device_ms
+        handoff_ms += ms
+        handoff_bytes += nbytes
     torch.cuda.synchronize()
     barrier(pg)
     clk = clocks.stop()
     launches = t.launch_count()
     stats = t.kernel_stats()
     t.set_profiling(False)
-    dev_s = max_over_ranks(pg, ev0.elapsed_time(ev1) / 1e3, local)
+    dev_s = max_over_ranks(pg, dev_ms / 1e3, local)
     edges_all = sum_over_ranks(pg, edges, local)
     algo_all = sum_over_ranks(pg, algo, local)
+    handoff_all = max_over_ranks(pg, handoff_ms, local)
 
     e2e = None
     if not args.no_e2e:  # the next K rounds with every bucket streamed from pinned host memory
@@ -344,15 +339,13 @@ def bench_rounds(args, cfg, rank, world, local, pg):
         host = lgd.PinnedArray((t.num_edges, 3), np.uint32)
         t.bucketed_edges(host.array)
         t.set_host_edges(host.array)
-        e, r, moves = cur.next()  # one warm-up round through the host path
-        mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+        step()  # one warm-up round through the host path
         barrier(pg)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e_edges = h2d = d2h = 0
         for _ in range(args.steps):
-            e, r, moves = cur.next()
-            res = mg.run_round(t, sched, e, r, moves, comm, rel_buf)
+            res, _, _ = step()
             e_edges += res.edges_trained
             h2d += res.h2d_bytes
             d2h += res.d2h_bytes
@@ -369,6 +362,10 @@ def bench_rounds(args, cfg, rank, world, local, pg):
     dstat = stats[dom]
     achieved = (dstat["algorithmic_bytes"] / (dstat["total_ms"] / 1e3) / 1e9
                 if dstat["total_ms"] else 0.0)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg, 0, CPU_BASELINE_BATCHES)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "host_cores", "kind", "sample")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": edges_all / dev_s, "unit": "edges/s", "n_gpus": world,
@@ -380,19 +377,29 @@ def bench_rounds(args, cfg, rank, world, local, pg):
                        "partitions": cfg["n"], "negatives": K_NEG, "batch_size": BATCH,
                        "storage": "f32 (E||S), FP64 arithmetic",
                        "graph": f"power-law alpha={ALPHA}, generator seed {GRAPH_SEED}",
-                       "step": "one round of the partition-round schedule "
-                               f"({sched.num_rounds} rounds per epoch)",
-                       "parallelism": f"partition rounds over {world} GPU(s), NVLink hand-offs"
-                                      + (", NCCL relation all-reduce per lock-step batch"
-                                         if cfg["rels"] else ""),
+                       "schedule": "partition rounds (DESIGN.md 6): pairs of partitions per "
+                                   "GPU, negative pool = the pair",
+                       "step": f"one round of the partition-round schedule ({R} rounds per "
+                               "epoch), all ranks", "edges_per_step": edges_all / args.steps,
+                       "parallelism": (f"partition rounds over {world} GPUs, NVLink pulls on a "
+                                       "side stream" + (", NCCL relation all-reduce per "
+                                                        "lock-step batch" if cfg["rels"] else "")
+                                       if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2", "setup_s": round(setup_s, 1)},
-            "roofline": {"bound": "hbm", "kernel": "segment_pass1+2 (K4), rank 0",
+            "roofline": {"bound": "hbm", "kernel": "segment_heads + long segments (K4), rank 0",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_source": peak_kind,
                          "traffic": (traffic_from_profiles(args.config) or {}).get(dom),
+                         "algorithmic_bytes_per_launch": (dstat["algorithmic_bytes"] /
+                                                          max(dstat["launches"], 1)),
+                         "avg_launch_ms": dstat["total_ms"] / max(dstat["launches"], 1),
                          "step_achieved": algo_all / dev_s / 1e9 / world,
-                         "step_frac": algo_all / dev_s / 1e9 / world / hbm},
-            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                         "step_frac": algo_all / dev_s / 1e9 / world / hbm,
+                         "phase_ms": {k: round(v["total_ms"], 3) for k, v in stats.items()}},
+            "handoff": {"ms_per_step": handoff_all / args.steps,
+                        "bytes_per_step": handoff_bytes / args.steps,
+                        "note": "span of the side-stream pulls, max over ranks; overlaps compute"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     t.close()
@@ -419,8 +426,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="tw", choices=sorted(CONFIGS))
     ap.add_argument("--schedule", default="auto", choices=["auto", "plan", "rounds"],
-                    help="plan: the reference iteration plan (1 GPU); rounds: the multi-GPU "
-                         "partition-round schedule (default for N > 1)")
+                    help="rounds (default, every N): the partition-round schedule, so the "
+                         "1/2/4/8-GPU points compare the same epoch; plan: the reference "
+                         "iteration plan (run_epoch's 3-partition buffer; 1 GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--negatives", type=int, default=K_NEG,
@@ -440,7 +448,8 @@ def main():
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 
-    schedule = args.schedule if args.schedule != "auto" else ("rounds" if world > 1 else "plan")
+    schedule = args.schedule if args.schedule != "auto" else (
+        "plan" if args.shared_chunk else "rounds")
     if schedule == "rounds":
         bench_rounds(args, cfg, rank, world, local, pg)
         return

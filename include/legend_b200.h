@@ -230,6 +230,55 @@ int lgd_round_begin(lgd_context* ctx, uint32_t epoch, const lgd_bucket_item* ite
 int lgd_round_step(lgd_context* ctx, uint64_t step, double* rel_grad_device);
 int lgd_round_apply_relations(lgd_context* ctx, const double* summed_device);
 int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out);
+/* ---------------------------------- multi-GPU partition-round runner ----
+ * One process per GPU.  Every rank builds the same graph, partition plan and
+ * store (identical initial tables), then joins the runner; a round is
+ * enqueued, its partition hand-offs issued, and its results collected:
+ *   lgd_train_round = lgd_round_enqueue + lgd_round_handoff + lgd_round_collect.
+ * Hand-offs are pulls over NVLink on a side stream (CUDA IPC mappings of the
+ * peers' tables, inter-process ready events), overlapped with the buckets
+ * that do not touch the moving partitions; typed models sum relation
+ * gradients per lock-step batch with NCCL (loaded at run time).  DESIGN.md 6. */
+
+/* A fresh NCCL unique id (128 bytes) on rank 0, to share with every rank. */
+int lgd_comm_unique_id(void* id128);
+/* Joins rank `rank` of `world` (world = 1: no NCCL, a local runner).  The
+ * tables must exist and stay allocated (lgd_init_store / lgd_load_partition
+ * first).  Collective over the ranks. */
+int lgd_comm_init(lgd_context* ctx, const void* id128, uint32_t rank, uint32_t world);
+/* Virtual ranks in one process: contexts[q] plays rank q (untyped models,
+ * or world 1).  The caller enqueues every rank's round before any hand-off. */
+int lgd_comm_init_local(lgd_context** contexts, uint32_t world);
+int lgd_round_count(lgd_context* ctx, uint32_t* rounds);
+int lgd_round_enqueue(lgd_context* ctx, uint32_t epoch, uint32_t round);
+int lgd_round_handoff(lgd_context* ctx);
+/* Waits for the round; handoff_ms = the hand-off copies' span on the side
+ * stream, handoff_bytes = theta + state bytes pulled for the next round. */
+int lgd_round_collect(lgd_context* ctx, lgd_epoch_result* out, double* handoff_ms,
+                      uint64_t* handoff_bytes);
+int lgd_train_round(lgd_context* ctx, uint32_t epoch, uint32_t round, lgd_epoch_result* out,
+                    double* handoff_ms, uint64_t* handoff_bytes);
+
+/* The runner's plan for one rank and round, host only (CPU tests, other
+ * executors): ARRIVE partitions pulled from `peer` before their first bucket,
+ * TRAIN buckets (item = index into lgd_round_schedule's list) in order,
+ * DEPART partitions ready for their next holder (`peer`) after their last
+ * bucket.
+ * owner_in[p] (may be NULL = all -1): rank holding partition p's current rows
+ * before the round, -1 = identical on every rank; owner_out: after it. */
+#define LGD_ACT_ARRIVE 0
+#define LGD_ACT_TRAIN 1
+#define LGD_ACT_DEPART 2
+typedef struct {
+  uint32_t kind;
+  uint32_t part;
+  int32_t peer;
+  uint64_t item;
+} lgd_round_action;
+int lgd_round_actions(uint32_t n, uint32_t world, uint32_t rank, uint32_t round,
+                      const int32_t* owner_in, uint64_t capacity, uint64_t* count,
+                      lgd_round_action* out, int32_t* owner_out);
+
 /* The context's CUDA stream (cudaStream_t): every kernel of the context runs
  * on it, in order.  The call orders the stream after pending asynchronous
  * write-backs (lgd_store_partition_async), so work the caller then queues on

@@ -1,6 +1,8 @@
 // common.cuh -- error plumbing shared by the CUDA sources.
 #pragma once
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,6 +26,26 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 #define LGD_CUDA(expr) ::lgd::cuda_check((expr), #expr, __FILE__, __LINE__)
 #define LGD_LAUNCH_CHECK() ::lgd::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Checked build (make checked -> liblegend_b200_checked.so): device-side
+// bounds and invariant checks on every gather / scatter index of the hot
+// kernels; a violation prints its site and traps the context.  (The pool's
+// compute-sanitizer is unavailable; tests/test_gpu_checked.py runs the
+// small workloads of profiles/sanitize_workload.py through this build.)
+#ifdef LGD_CHECKED
+#define LGD_DCHECK(cond, what, v)                                                          \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("LGD_CHECKED %s:%d: %s (value %llu)\n", __FILE__, __LINE__, what,            \
+             (unsigned long long)(v));                                                     \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define LGD_DCHECK(cond, what, v) \
+  do {                            \
+  } while (0)
+#endif
 
 constexpr uint32_t kNone32 = 0xffffffffu;
 constexpr int kWarp = 32;

@@ -40,6 +40,7 @@ __global__ void eval_candidates_kernel(uint64_t seed, uint64_t t0, uint64_t T, u
       r = xo_next(x);
     } while (r < bd.threshold);
     cand[i * ncand + c] = (uint32_t)(r % V);
+    LGD_DCHECK(r % V < V, "candidate id", r % V);
   }
 }
 
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
   for (uint64_t t = (uint64_t)blockIdx.x * kEvalWarps + warp; t < T; t += nwarps) {
     const uint32_t s = edges[3 * t], r = edges[3 * t + 1], dd = edges[3 * t + 2];
     const uint32_t* my = cand + t * ncand;
+    LGD_DCHECK(t < T && (uint64_t)(my - cand) + ncand <= T * (uint64_t)ncand, "eval tile", t);
     // IR1 = combine_src_rel (train.cpp:39-60), per element as the reference
     const float* sr = theta + (size_t)s * d;
     const float* rl = KIND != 0 ? rel + (size_t)r * d : nullptr;

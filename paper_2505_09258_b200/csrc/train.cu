@@ -30,6 +30,7 @@
 // FP64 expressions are compiled with -fmad=false so products and sums round
 // exactly like the reference's unfused x86-64 double arithmetic.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -152,6 +153,7 @@ __device__ __forceinline__ uint32_t to_pool(const BatchArgs& a, uint32_t id) {
 }
 __device__ __forceinline__ uint32_t from_pool(const BatchArgs& a, uint32_t idx) {
   idx &= a.key_mask;  // presorted keys carry the batch index above the pool index
+  LGD_DCHECK(idx < a.pool_end[a.pool_n - 1], "pool index beyond the resident pool", idx);
   if (idx < a.pool_end[0]) return (uint32_t)(a.pool_first[0] + idx);
   if (a.pool_n > 1 && idx < a.pool_end[1]) return (uint32_t)(a.pool_first[1] + (idx - a.pool_end[0]));
   return (uint32_t)(a.pool_first[2] + (idx - a.pool_end[1]));
@@ -211,8 +213,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
 
   // row r of positive p: 0 src, 1 rel, 2 dst, 3+j negative j
   auto row_id = [&](uint64_t p, uint32_t r) -> uint32_t {
-    if (r < 3) return a.edges[3 * p + r];
-    return a.negs[p * k + (r - 3)];
+    const uint32_t id = r < 3 ? a.edges[3 * p + r] : a.negs[p * k + (r - 3)];
+    LGD_DCHECK(r == 1 ? (!typed || id < a.num_rels) : id < a.num_nodes, "K3 row id out of range", id);
+    return id;
   };
   auto row_src = [&](uint32_t r, uint32_t id) -> const float* {
     return (r == 1 ? a.rel_theta : a.theta) + size_t(id) * d;
@@ -953,6 +956,7 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   const uint32_t p = val >> x.pshift;
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
+  LGD_DCHECK(!pred || slot <= x.k + 1, "K4 contribution slot", slot);
   it.slot = slot;
   if (SH && slot == 1) {  // shared negative: its precomputed gradient row (shared.cu SG3)
     it.w = 0.0;
@@ -1263,26 +1267,38 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
   }
 }
 
-// ------------------------------------- K4 v2: segment-list row updates
-// The sorted contributions' segment heads (one per unique node) are listed
-// once per bucket (launch_segment_list: a stable select of the head
-// positions, then each batch's first segment), so the update kernel walks
-// whole segments: a persistent warp claims 32 consecutive segments at a time
-// (one atomic), loads their bounds and keys lane-parallel, and for each
-// segment in order sums ALL its contributions sequentially in FP64 -- the
-// reference's exact std::map accumulation order (train.cpp:290-333), hubs
-// included, so no per-chunk partial sums or second pass -- then runs the
-// Adagrad row update (train.cpp:342-354).  The theta / state rows of the
-// next kSegDepth segments are in flight in the warp's cp.async ring, as in
-// segment_pass1_vec; the contribution payloads of the group come from two
-// 32-item register windows.  No chunk-edge bookkeeping, no atomics on rows.
+// ------------------------------------------ K4 v2: whole-segment updates
+// Every segment (one unique node's sorted contributions) is summed by ONE
+// warp, sequentially in FP64 in the reference's std::map order
+// (train.cpp:290-333), then its row gets the Adagrad update
+// (train.cpp:342-354); no partial sums cross warps for segments of up to
+// kLongSeg items.
+//   segment_heads  warp per 32 sorted items of the batch: it owns the segments
+//                  whose HEAD lies in its items.  Head and terminator masks of
+//                  its items and the next 32 (two ballots) give every owned
+//                  segment's length; a segment of <= kLongSeg items ends inside
+//                  that window, so the warp finishes it.  The theta / state
+//                  rows of the next kSegDepth segments are in flight in the
+//                  warp's cp.async ring; payloads come from two 32-item
+//                  register windows.  No continuation pieces, no second pass.
+//   long_chunks /  segments of more than kLongSeg items (hubs: up to thousands
+//   long_combine   of contributions per batch under the power law) are listed
+//                  once per bucket (launch_long_list), cut into 32-item chunks
+//                  summed by independent warps, and their partials added in
+//                  chunk order (deterministic) by one warp per segment.  They
+//                  run on the side stream, concurrently with segment_heads
+//                  (disjoint rows).
+// No atomics on rows; every row is written by exactly one warp.
+constexpr uint32_t kLongSeg = 32;
+
 template <int KIND, int NV, bool SH, bool IR1>
-__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_rows(
+__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
     BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
-    uint64_t n_items, const uint32_t* __restrict__ seg_start,
-    const uint32_t* __restrict__ batch_seg, uint32_t batch, unsigned int* __restrict__ work) {
+    uint64_t b0, uint64_t b1) {
   constexpr int NE = 4 * NV;
   const int lane = threadIdx.x & 31;
+  const uint64_t base = b0 + (((uint64_t)blockIdx.x * kSegThreads + threadIdx.x) >> 5) * 32;
+  if (base >= b1) return;
   const Lanes<KIND, NV> L(lane, a.dim);
   const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
                  (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
@@ -1292,106 +1308,243 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_rows(
   float* __restrict__ state = a.state;
   const uint64_t d = a.dim;
   const double lr = a.lr, eps = a.eps;
-  const uint32_t s_begin = batch_seg[batch], s_end = batch_seg[batch + 1];
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(a.counters, (unsigned long long)(s_end - s_begin));
+  // head / terminator masks of items [base, base + 64): the batch ends at b1
+  const uint64_t i = base + lane, j = i + 32;
+  const uint32_t key = i < b1 ? __ldg(skeys + i) : 0u;
+  const uint32_t key2 = j < b1 ? __ldg(skeys + j) : 0u;
+  const uint32_t prev = (i < b1 && i > b0) ? __ldg(skeys + i - 1) : ~key;
+  const uint32_t prev2 = __shfl_sync(0xffffffffu, key, 31);  // item base + 31
+  const uint32_t prev2_l = __shfl_up_sync(0xffffffffu, key2, 1);
+  const bool head = i < b1 && key != prev;
+  const bool term2 = j >= b1 || key2 != (lane ? prev2_l : prev2);
+  const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+  const uint32_t tmask0 = __ballot_sync(0xffffffffu, head || i >= b1);
+  const uint32_t tmask1 = __ballot_sync(0xffffffffu, term2);
+  const uint64_t ends = (uint64_t)tmask0 | ((uint64_t)tmask1 << 32);
+  if (lane == 0 && hmask) atomicAdd(a.counters, (unsigned long long)__popc(hmask));
+  // lane l with a head: segment length (0 = long, left to the long path)
+  uint32_t my_len = 0;
+  if (head) {
+    const uint64_t above = ends & ~((2ull << lane) - 1);  // terminators after the head
+    const uint32_t e = above ? (uint32_t)__ffsll((long long)above) - 1 : 64u;
+    my_len = e - lane <= kLongSeg ? e - lane : 0u;
+  }
+  uint32_t todo = __ballot_sync(0xffffffffu, my_len != 0);
+  if (!todo) return;
+  const uint32_t my_row = my_len ? from_pool(a, key) : 0u;
+  LGD_DCHECK(my_row < a.num_nodes && my_len <= kLongSeg && base + lane + my_len <= b1,
+             "K4 segment outside the batch / table", my_row);
+  const uint32_t w0 = i < b1 ? __ldg(svals + i) : 0u;
+  const uint32_t w1 = j < b1 ? __ldg(svals + j) : 0u;
+  auto item = [&](uint32_t o) {  // o < 64: the item at base + o
+    const uint32_t v0 = __shfl_sync(0xffffffffu, w0, o & 31);
+    const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
+    return o < 32 ? v0 : v1;
+  };
   extern __shared__ __align__(16) float seg_ring[];
   const uint32_t rowf = (a.dim + 3) & ~3u;
   const uint32_t slotf = 2 * rowf;  // slot: theta, state
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
                         (threadIdx.x >> 5) * kSegDepth * slotf * 4;  // bytes
   const uint32_t ring_end = ring + kSegDepth * slotf * 4;
-  for (;;) {
-    uint32_t g0 = 0;
-    if (lane == 0) g0 = atomicAdd(work + batch, 32u);
-    g0 = __shfl_sync(0xffffffffu, g0, 0) + s_begin;
-    if (g0 >= s_end) break;
-    const int ns = (int)min(32u, s_end - g0);
-    // lane l: segment g0 + l -- first item, length, table row
-    uint32_t my_st = 0, my_len = 0, my_row = 0;
-    if (lane < ns) {
-      my_st = __ldg(seg_start + g0 + lane);
-      my_len = __ldg(seg_start + g0 + lane + 1) - my_st;
-      my_row = from_pool(a, __ldg(skeys + my_st));
+  uint32_t srest = todo;  // segments still to stage, lowest first
+  auto stage = [&](uint32_t slot) {
+    if (srest) {
+      const int h = __ffs(srest) - 1;
+      srest &= srest - 1;
+      const uint64_t off = (uint64_t)__shfl_sync(0xffffffffu, my_row, h) * d;
+      L.cpa_s(slot, theta + off, true);
+      L.cpa_s(slot + rowf * 4, state + off, true);
     }
-    // payload windows: items [i0, i0 + 64) of the group
-    const uint32_t i0 = __shfl_sync(0xffffffffu, my_st, 0);
-    const uint32_t w0 = i0 + lane < n_items ? __ldg(svals + i0 + lane) : 0u;
-    const uint32_t w1 = i0 + 32 + lane < n_items ? __ldg(svals + i0 + 32 + lane) : 0u;
-    auto item = [&](uint32_t q) {
-      const uint32_t o = q - i0;
-      const uint32_t v0 = __shfl_sync(0xffffffffu, w0, o & 31);
-      const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
-      return o < 32 ? v0 : (o < 64 ? v1 : __ldg(svals + q));
-    };
-    auto stage = [&](int j, uint32_t slot) {
-      const uint32_t r = __shfl_sync(0xffffffffu, my_row, j & 31);
-      if (j < ns) {
-        const uint64_t off = (uint64_t)r * d;
-        L.cpa_s(slot, theta + off, true);
-        L.cpa_s(slot + rowf * 4, state + off, true);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
 #pragma unroll
-    for (int u = 0; u < kSegDepth; ++u) stage(u, ring + u * slotf * 4);
-    uint32_t slot = ring;
+  for (int u = 0; u < kSegDepth; ++u) stage(ring + u * slotf * 4);
+  uint32_t slot = ring;
 #pragma unroll 1
-    for (int j = 0; j < ns; ++j) {
-      const uint32_t sj = __shfl_sync(0xffffffffu, my_st, j);
-      const uint32_t lj = __shfl_sync(0xffffffffu, my_len, j);
-      const uint32_t row = __shfl_sync(0xffffffffu, my_row, j);
-      ItemRegs<NE> cit;
-      load_item<KIND, NV, false, SH, IR1>(x, L, item(sj), true, cit);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
-      float th[NE], st[NE];
-      L.lds_s(slot, th);
-      L.lds_s(slot + rowf * 4, st);
-      double acc[NE];
+  while (todo) {
+    const int h = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t len = __shfl_sync(0xffffffffu, my_len, h);
+    const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
+    ItemRegs<NE> cit;
+    load_item<KIND, NV, false, SH, IR1>(x, L, item(h), true, cit);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
+    float th[NE], st[NE];
+    L.lds_s(slot, th);
+    L.lds_s(slot + rowf * 4, st);
+    double acc[NE];
 #pragma unroll
-      for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-      add_loaded<KIND, NV, false, SH, IR1>(x, L, cit, x.k, acc, th);
-      for (uint32_t q = sj + 1; q < sj + lj; ++q) {
-        ItemRegs<NE> it;
-        load_item<KIND, NV, false, SH, IR1>(x, L, item(q), true, it);
-        add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, th);
-      }
-      adagrad_lanes(L, acc, th, st, lr, eps);
-      L.stf(theta + (uint64_t)row * d, th);
-      L.stf(state + (uint64_t)row * d, st);
-      stage(j + kSegDepth, slot);  // the slot just read is free again
-      slot = slot + slotf * 4 == ring_end ? ring : slot + slotf * 4;
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    add_loaded<KIND, NV, false, SH, IR1>(x, L, cit, x.k, acc, th);
+    for (uint32_t q = h + 1; q < h + len; ++q) {
+      ItemRegs<NE> it;
+      load_item<KIND, NV, false, SH, IR1>(x, L, item(q), true, it);
+      add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, th);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    adagrad_lanes(L, acc, th, st, lr, eps);
+    L.stf(theta + (uint64_t)row * d, th);
+    L.stf(state + (uint64_t)row * d, st);
+    stage(slot);  // the slot just read is free again
+    slot = slot + slotf * 4 == ring_end ? ring : slot + slotf * 4;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// The bucket's long segments (launch_long_list): head item, end item,
+// exclusive prefix of their 32-item chunk counts, first long segment of each
+// batch.  Chunk c of long segment j covers items head + 32 (c - base[j]) + [0, 32).
+struct LongList {
+  const uint32_t* head;
+  const uint32_t* end;
+  const uint32_t* chunk_base;
+  const uint32_t* first;  // nb + 1 entries
+};
+
+template <int KIND, int NV, bool SH, bool IR1>
+__global__ void __launch_bounds__(kSegThreads) long_chunks(
+    BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+    LongList ll, uint32_t batch, double* __restrict__ part) {
+  constexpr int NE = 4 * NV;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lf = ll.first[batch], le = ll.first[batch + 1];
+  if (lf == le) return;
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G};
+  const uint32_t c0 = ll.chunk_base[lf], c1 = ll.chunk_base[le];
+  const uint64_t d = a.dim;
+  const uint32_t nwarps = gridDim.x * (kSegThreads / 32);
+  for (uint32_t c = c0 + blockIdx.x * (kSegThreads / 32) + (threadIdx.x >> 5); c < c1; c += nwarps) {
+    uint32_t lo = lf, hi = le;  // last j with chunk_base[j] <= c
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(ll.chunk_base + mid) <= c) lo = mid; else hi = mid;
+    }
+    const uint32_t s0 = __ldg(ll.head + lo), s1 = __ldg(ll.end + lo);
+    const uint32_t q0 = s0 + 32 * (c - __ldg(ll.chunk_base + lo));
+    const uint32_t q1 = min(q0 + 32, s1);
+    LGD_DCHECK(q0 < q1 && s1 - s0 > kLongSeg, "long segment chunk", q0);
+    const uint32_t w = q0 + lane < q1 ? __ldg(svals + q0 + lane) : 0u;
+    float own[NE];
+    if (KIND == 3) {  // TransE contributions read the node's own (pre-update) row
+      const uint32_t row = from_pool(a, __ldg(skeys + s0));
+      L.template ldf<true>(a.theta + (uint64_t)row * d, true, own);
+    }
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    for (uint32_t q = q0; q < q1; ++q) {
+      ItemRegs<NE> it;
+      load_item<KIND, NV, false, SH, IR1>(x, L, __shfl_sync(0xffffffffu, w, q - q0), true, it);
+      add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, own);
+    }
+    L.std_(part + (uint64_t)(c - c0) * d, acc);
   }
 }
 
-// Segment heads of sorted keys: flag i starts a segment when it is the first
-// item or its key differs from the previous one.
-struct HeadFlag {
+template <int KIND, int NV>
+__global__ void __launch_bounds__(kSegThreads) long_combine(
+    BatchArgs a, const uint32_t* __restrict__ skeys, LongList ll, uint32_t batch,
+    const double* __restrict__ part) {
+  constexpr int NE = 4 * NV;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lf = ll.first[batch], le = ll.first[batch + 1];
+  if (lf == le) return;
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const uint32_t c0 = ll.chunk_base[lf];
+  const uint64_t d = a.dim;
+  const uint32_t nwarps = gridDim.x * (kSegThreads / 32);
+  for (uint32_t j = lf + blockIdx.x * (kSegThreads / 32) + (threadIdx.x >> 5); j < le; j += nwarps) {
+    const uint32_t row = from_pool(a, __ldg(skeys + __ldg(ll.head + j)));
+    const uint32_t b0 = __ldg(ll.chunk_base + j) - c0, b1 = __ldg(ll.chunk_base + j + 1) - c0;
+    double acc[NE];
+    L.ldd(part + (uint64_t)b0 * d, true, acc);
+    uint32_t c = b0 + 1;
+    for (; c + 4 <= b1; c += 4) {  // four partials in flight, added in chunk order
+      double v0[NE], v1[NE], v2[NE], v3[NE];
+      L.ldd(part + (uint64_t)c * d, true, v0);
+      L.ldd(part + (uint64_t)(c + 1) * d, true, v1);
+      L.ldd(part + (uint64_t)(c + 2) * d, true, v2);
+      L.ldd(part + (uint64_t)(c + 3) * d, true, v3);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] = (((acc[e] + v0[e]) + v1[e]) + v2[e]) + v3[e];
+    }
+    for (; c < b1; ++c) {
+      double v[NE];
+      L.ldd(part + (uint64_t)c * d, true, v);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) acc[e] += v[e];
+    }
+    float th[NE], st[NE];
+    L.template ldf<false>(a.theta + (uint64_t)row * d, true, th);
+    L.template ldf<false>(a.state + (uint64_t)row * d, true, st);
+    adagrad_lanes(L, acc, th, st, a.lr, a.eps);
+    L.stf(a.theta + (uint64_t)row * d, th);
+    L.stf(a.state + (uint64_t)row * d, st);
+  }
+}
+
+// heads of segments longer than kLongSeg: the item 32 places on has the same key
+struct LongHead {
   const uint32_t* keys;
+  uint64_t n;
   __host__ __device__ __forceinline__ bool operator()(const uint32_t& i) const {
-    return i == 0 || keys[i] != keys[i - 1];
+    return (i == 0 || keys[i] != keys[i - 1]) && i + kLongSeg < n && keys[i + kLongSeg] == keys[i];
   }
 };
 
-// batch_seg[b] = first segment of batch b (the key's bits above `shift`);
-// batch_seg[nb] = nseg and seg_start[nseg] = n close the last ranges
-__global__ void batch_seg_kernel(const uint32_t* __restrict__ keys, uint64_t n,
-                                 uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ nseg_p,
-                                 int shift, uint32_t nb, uint32_t* __restrict__ batch_seg) {
-  const uint32_t nseg = *nseg_p;
-  auto bat = [&](uint32_t s) -> uint32_t {
-    return shift >= 32 ? 0u : keys[seg_start[s]] >> shift;
-  };
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += gridDim.x * blockDim.x) {
-    const uint32_t b = bat(s);
-    const uint32_t pb = s ? bat(s - 1) + 1 : 0u;
-    for (uint32_t bb = pb; bb <= b; ++bb) batch_seg[bb] = s;
-    if (s == nseg - 1) {
-      for (uint32_t bb = b + 1; bb <= nb; ++bb) batch_seg[bb] = nseg;
-      seg_start[nseg] = (uint32_t)n;
+// One block: each long segment's end (galloping search for the first item
+// with another key), chunk_base = exclusive prefix of the chunk counts,
+// first[b] = first long segment at or after batch b's first item.
+__global__ void __launch_bounds__(1024) long_index_kernel(
+    const uint32_t* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ head,
+    const uint32_t* __restrict__ nlong_p, uint64_t batch_items, uint32_t nb,
+    uint32_t* __restrict__ end, uint32_t* __restrict__ chunk_base, uint32_t* __restrict__ first) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t carry;
+  const uint32_t nlong = *nlong_p;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t t0 = 0; t0 <= nlong; t0 += 1024) {
+    const uint32_t jj = t0 + threadIdx.x;
+    uint32_t c = 0;
+    if (jj < nlong) {
+      const uint64_t h = head[jj];
+      const uint32_t k = keys[h];
+      uint64_t lo = h + kLongSeg, step = 64;  // keys[lo] == k
+      uint64_t hi = lo + step;
+      while (hi < n && keys[hi] == k) {
+        lo = hi;
+        step *= 2;
+        hi = lo + step;
+      }
+      if (hi > n) hi = n;
+      while (hi - lo > 1) {  // keys[lo] == k, keys[hi] != k (or hi == n)
+        const uint64_t mid = (lo + hi) >> 1;
+        if (keys[mid] == k) lo = mid; else hi = mid;
+      }
+      end[jj] = (uint32_t)hi;
+      c = (uint32_t)((hi - h + 31) / 32);
     }
+    uint32_t ex, total;
+    Scan(tmp).ExclusiveSum(c, ex, total);
+    if (jj <= nlong) chunk_base[jj] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  for (uint32_t b = threadIdx.x; b <= nb; b += 1024) {  // lower_bound(head, b * batch_items)
+    const uint64_t key = (uint64_t)b * batch_items;
+    uint32_t lo = 0, hi = nlong;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (head[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    first[b] = lo;
   }
 }
 
@@ -1444,55 +1597,64 @@ void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStr
 }
 
 template <int KIND, int NV, bool SH, bool IR1>
-void launch_segment_rows_(const BatchArgs& a, cudaStream_t st) {
+void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStream_t st) {
   const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
   static size_t attr[kMaxDevices];
-  static int occ[kMaxDevices];
-  static size_t occ_smem[kMaxDevices];
   const int dev = current_device();
   if (smem > attr[dev]) {
-    LGD_CUDA(cudaFuncSetAttribute(segment_rows<KIND, NV, SH, IR1>,
+    LGD_CUDA(cudaFuncSetAttribute(segment_heads<KIND, NV, SH, IR1>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[dev] = smem;
   }
-  if (occ_smem[dev] != smem) {
-    LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ[dev], segment_rows<KIND, NV, SH, IR1>, kSegThreads, smem));
-    occ_smem[dev] = smem;
+  // long segments first, on the side stream (disjoint rows), when there is one
+  const LongList ll{a.long_head, a.long_end, a.long_chunk_base, a.long_first};
+  cudaStream_t ls = st;
+  if (a.side) {
+    LGD_CUDA(cudaEventRecord(a.ev_long, st));
+    LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_long, 0));
+    ls = a.side;
   }
-  const unsigned grid = (unsigned)std::max(1, occ[dev]) * (unsigned)a.sm_count;
-  segment_rows<KIND, NV, SH, IR1><<<grid, kSegThreads, smem, st>>>(
-      a, a.seg_keys, a.seg_vals, a.seg_n, a.seg_start, a.batch_seg, a.seg_batch, a.seg_work);
+  long_chunks<KIND, NV, SH, IR1><<<(unsigned)a.sm_count * 2, kSegThreads, 0, ls>>>(
+      a, a.seg_keys, a.seg_vals, ll, a.seg_batch, a.part_first);
   LGD_LAUNCH_CHECK();
+  long_combine<KIND, NV><<<(unsigned)a.sm_count, kSegThreads, 0, ls>>>(a, a.seg_keys, ll,
+                                                                      a.seg_batch, a.part_first);
+  LGD_LAUNCH_CHECK();
+  if (a.side) LGD_CUDA(cudaEventRecord(a.ev_long_done, a.side));
+  const unsigned grid = (unsigned)ceil_div(ceil_div(b1 - b0, 32), kSegThreads / 32);
+  segment_heads<KIND, NV, SH, IR1><<<grid, kSegThreads, smem, st>>>(a, a.seg_keys, a.seg_vals, b0,
+                                                                    b1);
+  LGD_LAUNCH_CHECK();
+  if (a.side) LGD_CUDA(cudaStreamWaitEvent(st, a.ev_long_done, 0));
 }
 
-// K4 v2 for the node pass when the dimension has vector lanes; the segment
-// list is the bucket's (presorted) or built here for this batch's own sort.
-// ComplEx / TransE read K3's IR1 rows when the context keeps them (a.ir1),
-// else recombine the snapshot with the relation row (same bits).
+// K4 v2 for the node pass when the dimension has vector lanes.  The bucket's
+// long-segment list (presorted) or a one-batch list built here for this
+// batch's own sort.  ComplEx / TransE read K3's IR1 rows when the context
+// keeps them (a.ir1), else recombine the snapshot with the relation row
+// (same bits).
 template <int KIND, bool SH>
 bool segment_rows_node_pass(BatchArgs& a, uint64_t items, cudaStream_t st) {
-  if (!a.seg_mode) return false;
+  if (!a.seg_mode || a.grad_nodes) return false;
   const int nv = vec_width<KIND>(a.dim);
   if (nv == 0 || (KIND == 3 && SH)) return false;
+  uint64_t b0 = a.seg_b0;
   if (a.seg_mode == 2) {  // this batch's sort: a one-batch list
     a.seg_keys = a.skeys;
     a.seg_vals = a.svals;
-    a.seg_n = items;
     a.seg_batch = 0;
-    LGD_CUDA(cudaMemsetAsync(a.seg_work, 0, sizeof(unsigned int), st));
-    launch_segment_list(a.skeys, items, 32, 1, a.seg_start, a.batch_seg, a.seg_nseg, a.seg_temp,
-                        a.seg_temp_bytes, a.sm_count, st);
+    b0 = 0;
+    launch_long_list(a.skeys, items, items, 1, a.seg_lists, st);
   }
   if constexpr (KIND != 3 || !SH) {
     constexpr bool kIr1 = k4_ir1(KIND) && !SH;
     const bool ir1 = kIr1 && a.ir1 != nullptr;
     if (nv == 1) {
-      if (ir1) launch_segment_rows_<KIND, 1, SH, kIr1>(a, st);
-      else launch_segment_rows_<KIND, 1, SH, false>(a, st);
+      if (ir1) launch_segment_heads_<KIND, 1, SH, kIr1>(a, b0, b0 + items, st);
+      else launch_segment_heads_<KIND, 1, SH, false>(a, b0, b0 + items, st);
     } else {
-      if (ir1) launch_segment_rows_<KIND, 2, SH, kIr1>(a, st);
-      else launch_segment_rows_<KIND, 2, SH, false>(a, st);
+      if (ir1) launch_segment_heads_<KIND, 2, SH, kIr1>(a, b0, b0 + items, st);
+      else launch_segment_heads_<KIND, 2, SH, false>(a, b0, b0 + items, st);
     }
   }
   return true;
@@ -1830,23 +1992,22 @@ int k4_vec_width(int kind, uint32_t dim) {
   }
 }
 
-size_t segment_list_temp_bytes(uint64_t max_items) {
-  size_t bytes = 0;
-  LGD_CUDA(cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<uint32_t>(0),
+size_t long_list_temp_bytes(uint64_t max_items) {
+  size_t b = 0;
+  LGD_CUDA(cub::DeviceSelect::If(nullptr, b, thrust::counting_iterator<uint32_t>(0),
                                  (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                 (int64_t)(max_items ? max_items : 1), HeadFlag{nullptr}));
-  return bytes;
+                                 (int64_t)(max_items ? max_items : 1), LongHead{nullptr, 0}));
+  return b;
 }
 
-void launch_segment_list(const uint32_t* keys, uint64_t n, int shift, uint32_t nb,
-                         uint32_t* seg_start, uint32_t* batch_seg, uint32_t* nseg, void* temp,
-                         size_t temp_bytes, int sm_count, cudaStream_t st) {
+void launch_long_list(const uint32_t* keys, uint64_t n, uint64_t batch_items, uint32_t nb,
+                      const SegLists& L, cudaStream_t st) {
   if (!n) return;
-  size_t bytes = temp_bytes;
-  LGD_CUDA(cub::DeviceSelect::If(temp, bytes, thrust::counting_iterator<uint32_t>(0), seg_start,
-                                 nseg, (int64_t)n, HeadFlag{keys}, st));
-  batch_seg_kernel<<<(unsigned)sm_count * 4, 256, 0, st>>>(keys, n, seg_start, nseg, shift, nb,
-                                                           batch_seg);
+  size_t bytes = L.temp_bytes;  // heads of segments longer than kLongSeg, ascending
+  LGD_CUDA(cub::DeviceSelect::If(L.temp, bytes, thrust::counting_iterator<uint32_t>(0),
+                                 L.long_head, L.nlong, (int64_t)n, LongHead{keys, n}, st));
+  long_index_kernel<<<1, 1024, 0, st>>>(keys, n, L.long_head, L.nlong, batch_items, nb, L.long_end,
+                                        L.long_chunk_base, L.long_first);
   LGD_LAUNCH_CHECK();
 }
 

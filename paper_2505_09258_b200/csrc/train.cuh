@@ -22,11 +22,22 @@ __host__ __device__ constexpr bool k4_ir1(int kind) {
 #endif
 }
 
+struct SegLists {  // K4 v2 long-segment list (launch_long_list)
+  uint32_t* long_head;        // <= n / 33 + 1 (heads of segments of > 32 items, ascending)
+  uint32_t* long_end;         // same count: end item of each
+  uint32_t* long_chunk_base;  // + 1: exclusive prefix of their 32-item chunk counts
+  uint32_t* long_first;       // nb + 1: first long segment of each batch
+  uint32_t* nlong;            // 1
+  void* temp;
+  size_t temp_bytes;
+};
+
 struct BatchArgs {
   int kind;
   uint32_t dim;
   uint32_t k;
   uint64_t P;                 // positives in this batch
+  uint64_t num_nodes;         // table rows (LGD_CHECKED bounds; num_rels below)
   const uint32_t* edges;      // P x 3 (src, rel, dst), device
   const uint32_t* negs;       // P x k, device
   float* theta;               // V x d embeddings
@@ -98,20 +109,21 @@ struct BatchArgs {
   // only K3's outputs, so its sort and segmented sums overlap the node pass;
   // the relation rows are updated after K4, which reads them pre-update.
   // side == nullptr: sequential relation pass.
-  // K4 v2 (segment_rows): 0 = chunked pass 1 / pass 2; 1 = the bucket's
-  // segment list is ready (seg_keys / seg_vals = the bucket's sorted arrays,
-  // batch seg_batch); 2 = build a one-batch list after this batch's sort
+  // K4 v2 (segment_heads): 0 = chunked pass 1 / pass 2; 1 = the bucket's
+  // long-segment list is ready (seg_keys / seg_vals = the bucket's sorted
+  // arrays, this batch = items [seg_b0, seg_b0 + P(k+2)), batch index
+  // seg_batch); 2 = build a one-batch list after this batch's sort
   int seg_mode;
   const uint32_t* seg_keys;
   const uint32_t* seg_vals;
-  uint64_t seg_n;             // items in seg_keys
-  uint32_t* seg_start;        // segment s starts at item seg_start[s]; [nseg] = seg_n
-  uint32_t* batch_seg;        // first segment of each batch, [nb] = nseg
+  uint64_t seg_b0;
   uint32_t seg_batch;
-  unsigned int* seg_work;     // per-batch work counters (zeroed)
-  uint32_t* seg_nseg;         // device segment count
-  void* seg_temp;
-  size_t seg_temp_bytes;
+  uint32_t* long_head;
+  uint32_t* long_end;
+  uint32_t* long_chunk_base;
+  uint32_t* long_first;
+  SegLists seg_lists;         // the buffers, for a one-batch list (seg_mode 2)
+  cudaEvent_t ev_long, ev_long_done;  // long segments on the side stream
   cudaStream_t side;
   cudaEvent_t ev_scored, ev_rel;
   uint64_t num_rels;
@@ -151,17 +163,18 @@ size_t batch_sort_temp_bytes(uint64_t max_items);
 void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* keys,
                         uint32_t* vals, cudaStream_t st);
 size_t bucket_sort_temp_bytes(uint64_t max_items);
-// Segment list of sorted keys (K4 v2): seg_start = item positions where the
-// key changes (n + 1 entries with the closing n), batch_seg[b] = first
-// segment whose key has batch bits (above `shift`; 32 = one batch) b, for
-// b < nb, and batch_seg[nb] = nseg.  nseg: device count.
-size_t segment_list_temp_bytes(uint64_t max_items);
+// Long-segment list of sorted keys (K4 v2): heads of the segments of more
+// than 32 items (ascending), their ends, the exclusive prefix of their
+// 32-item chunk counts and, per batch b < nb (items [b batch_items, ...)),
+// the first long segment of the batch; first[nb] = nlong (device count).
+size_t long_list_temp_bytes(uint64_t max_items);
+void launch_long_list(const uint32_t* keys, uint64_t n, uint64_t batch_items, uint32_t nb,
+                      const SegLists& lists, cudaStream_t st);
 // 16-byte vectors per lane of K4's vector kernels for (kind, dim); 0 = the
 // 8-lane-group fallback (which never reads K3's IR1 rows)
 int k4_vec_width(int kind, uint32_t dim);
 void launch_segment_list(const uint32_t* keys, uint64_t n, int shift, uint32_t nb,
-                         uint32_t* seg_start, uint32_t* batch_seg, uint32_t* nseg, void* temp,
-                         size_t temp_bytes, int sm_count, cudaStream_t st);
+                         const SegLists& lists, int sm_count, cudaStream_t st);
 int sort_bucket(void* temp, size_t temp_bytes, uint32_t* keys[2], uint32_t* vals[2],
                 uint64_t items, int key_bits, cudaStream_t st);
 size_t score_smem_bytes(uint32_t dim, uint32_t k);

@@ -101,6 +101,15 @@ def library():
         "lgd_train_buckets": (i32, [vp, u32, u64, u64, vp]),
         "lgd_train_buckets_from_host": (i32, [vp, u32, u64, u64, vp, vp]),
         "lgd_train_bucket_prefix": (i32, [vp, u32, u64, u64, vp, vp, vp]),
+        "lgd_comm_unique_id": (i32, [vp]),
+        "lgd_comm_init": (i32, [vp, vp, u32, u32]),
+        "lgd_comm_init_local": (i32, [vp, u32]),
+        "lgd_round_count": (i32, [vp, vp]),
+        "lgd_round_enqueue": (i32, [vp, u32, u32]),
+        "lgd_round_handoff": (i32, [vp]),
+        "lgd_round_collect": (i32, [vp, vp, vp, vp]),
+        "lgd_train_round": (i32, [vp, u32, u32, vp, vp, vp]),
+        "lgd_round_actions": (i32, [u32, u32, u32, u32, vp, u64, vp, vp, vp]),
         "lgd_write_graph": (i32, [C.c_char_p, vp, u64, u64, u64]),
         "lgd_read_graph_meta": (i32, [C.c_char_p, vp, vp, vp]),
         "lgd_read_graph": (i32, [C.c_char_p, vp, u64]),
@@ -141,6 +150,10 @@ def _check(rc):
     if rc:
         msg = library().lgd_last_error().decode(errors="replace")
         raise _ERRORS.get(rc, RuntimeFailure)(msg)
+
+
+def _result(r) -> "EpochResult":
+    return EpochResult(**{f: getattr(r, f) for f, _ in _EpochResult._fields_})
 
 
 def _p(a):

@@ -49,6 +49,29 @@ def round_schedule(n: int) -> np.ndarray:
     return items
 
 
+ACTION_DTYPE = np.dtype([("kind", "<u4"), ("part", "<u4"), ("peer", "<i4"), ("_pad", "<u4"),
+                         ("item", "<u8")])
+assert ACTION_DTYPE.itemsize == 24
+ARRIVE, TRAIN, DEPART = 0, 1, 2
+
+
+def round_actions(n: int, world: int, rank: int, r: int, owner=None):
+    """The C++ runner's plan for one rank and round (lgd_round_actions, host
+    only): ARRIVE (partition, from peer) before the round, TRAIN buckets
+    (index into round_schedule(n)) in order, DEPART (partition, to peer)
+    after its last bucket.  owner[p]: rank with p's current rows (-1: every
+    rank).  Returns (actions, owner after the round)."""
+    lib = L.library()
+    own = None if owner is None else np.ascontiguousarray(owner, np.int32)
+    cnt = np.zeros(1, np.uint64)
+    L._check(lib.lgd_round_actions(n, world, rank, r, L._p(own), 0, L._p(cnt), None, None))
+    acts = np.zeros(int(cnt[0]), ACTION_DTYPE)
+    out = np.zeros(n, np.int32)
+    L._check(lib.lgd_round_actions(n, world, rank, r, L._p(own), len(acts), L._p(cnt),
+                                   acts.ctypes.data_as(C.c_void_p), L._p(out)))
+    return acts, out
+
+
 def items_as_u64(items: np.ndarray) -> np.ndarray:
     """(count, 8) rows for the oracle: src, dst, g, pool0..2, round, pair."""
     out = np.zeros((len(items), 8), np.uint64)
@@ -169,6 +192,104 @@ def lock_step(trainer, comm, steps: int, rel_buf):
         trainer.round_step(s, rel_buf)
         comm.all_reduce_sum(rel_buf)
         trainer.round_apply(rel_buf)
+
+
+def run_epoch_actions(trainer, n: int, epoch: int, comm, rel_buf=None, owner=None):
+    """One epoch on this rank driven by the C++ runner's plan
+    (lgd_round_actions): each round's TRAIN buckets (lock step for typed
+    models), then the partitions that DEPART go to their next holder and the
+    next round's ARRIVE partitions come in -- the hand-offs lgd_train_round
+    does as NVLink pulls, here over the communicator (gloo in the CPU tests).
+    Returns (totals, owner after the epoch)."""
+    items = round_schedule(n)
+    rounds = int(items["round"].max()) + 1 if len(items) else 0
+    own = np.full(n, -1, np.int32) if owner is None else np.asarray(owner, np.int32)
+    totals = {"loss_sum": 0.0, "edges_trained": 0, "batches": 0, "device_ms": 0.0}
+    for r in range(rounds):
+        acts, own_after = round_actions(n, comm.world, comm.rank, r, own)
+        mine = items[acts["item"][acts["kind"] == TRAIN]]
+        if not trainer.typed:
+            res = trainer.train_items(epoch, mine)
+        else:
+            nb = trainer.round_begin(epoch, mine)
+            lock_step(trainer, comm, comm.all_reduce_max_int(nb), rel_buf)
+            res = trainer.round_end()
+        for key in totals:
+            totals[key] += getattr(res, key) if hasattr(res, key) else res[key]
+        # hand-offs for the next round: my departures, my next arrivals
+        moves = [(int(a["part"]), comm.rank, int(a["peer"])) for a in acts if a["kind"] == DEPART]
+        if r + 1 < rounds:
+            nxt, _ = round_actions(n, comm.world, comm.rank, r + 1, own_after)
+            moves += [(int(a["part"]), int(a["peer"]), comm.rank) for a in nxt
+                      if a["kind"] == ARRIVE]
+        else:
+            moves = []  # the epoch's last holders keep their rows (gather_owned)
+        comm.exchange(sorted(set(moves)), trainer.partition_views)
+        own = own_after
+    return totals, own
+
+
+def gather_owned(trainer, owner, comm):
+    """Move every partition from the rank holding its rows to rank 0."""
+    moves = [(p, int(o), 0) for p, o in enumerate(owner) if o not in (-1, 0)]
+    comm.exchange(moves, trainer.partition_views)
+
+
+class NativeRounds:
+    """The C++ partition-round runner (rounds.cu) on one rank:
+    lgd_comm_init(rank, world) -- NCCL for world > 1 -- then lgd_train_round
+    per round: the rank's buckets, the hand-offs of the next round's
+    partitions as NVLink pulls on a side stream, lock-step NCCL relation
+    sums for typed models."""
+
+    def __init__(self, trainer, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self.trainer, self.rank, self.world = trainer, rank, world
+        buf = None
+        if world > 1:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+        L._check(L.library().lgd_comm_init(trainer._h, buf, rank, world))
+        cnt = np.zeros(1, np.uint32)
+        L._check(L.library().lgd_round_count(trainer._h, L._p(cnt)))
+        self.num_rounds = int(cnt[0])
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        L._check(L.library().lgd_comm_unique_id(buf))
+        return buf.raw
+
+    def run(self, epoch: int, r: int):
+        """-> (EpochResult of this rank's buckets, hand-off ms, hand-off bytes)"""
+        res = L._EpochResult()
+        ms = np.zeros(1, np.float64)
+        nbytes = np.zeros(1, np.uint64)
+        L._check(L.library().lgd_train_round(self.trainer._h, epoch, r, C.byref(res), L._p(ms),
+                                             L._p(nbytes)))
+        return L._result(res), float(ms[0]), int(nbytes[0])
+
+
+def init_local(trainers):
+    """Virtual ranks in one process (lgd_comm_init_local): trainers[q] is rank q."""
+    arr = (C.c_void_p * len(trainers))(*[t._h.value for t in trainers])
+    L._check(L.library().lgd_comm_init_local(arr, len(trainers)))
+
+
+def run_round_local(trainers, epoch: int, r: int):
+    """One round of virtual ranks: every rank's round queued, then every
+    rank's hand-offs, then every rank's results."""
+    lib = L.library()
+    for t in trainers:
+        L._check(lib.lgd_round_enqueue(t._h, epoch, r))
+    for t in trainers:
+        L._check(lib.lgd_round_handoff(t._h))
+    out = []
+    for t in trainers:
+        res = L._EpochResult()
+        ms = np.zeros(1, np.float64)
+        nbytes = np.zeros(1, np.uint64)
+        L._check(lib.lgd_round_collect(t._h, C.byref(res), L._p(ms), L._p(nbytes)))
+        out.append((L._result(res), float(ms[0]), int(nbytes[0])))
+    return out
 
 
 def run_epoch_distributed(trainer, sched: Schedule, epoch: int, comm, rel_buf=None):

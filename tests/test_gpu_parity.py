@@ -494,11 +494,10 @@ def _hub_graph(rng, V, R, E):
 
 @pytest.mark.parametrize("kind", ALL_KINDS)
 def test_k4_segment_rows_sum_hubs_in_reference_order(oracle, kind, monkeypatch):
-    """K4 v2 (segment_rows, the default) sums every segment -- hubs included --
-    sequentially in the reference's std::map order, so its tables match the
-    restatement to the last bit except where K3's exp / log ulps differ; the
-    chunked kernels (LGD_K4=1) add per-chunk partials for hubs.  Both stay
-    within the stated tolerance."""
+    """K4 v2 (segment_rows, the default: segments of <= 32 contributions summed
+    whole in the reference's std::map order, hubs in 32-item chunks added in
+    chunk order) and the chunked kernels (LGD_K4=1) both stay within the
+    stated tolerance of the restatement, with exact unique-row counts."""
     rng = np.random.default_rng(21)
     V, R, d, Ecnt, n, k, B = 4000, 6, 36 if kind != "complex" else 40, 40000, 4, 8, 3000
     R = R if kind != "dot" else 0
@@ -522,8 +521,7 @@ def test_k4_segment_rows_sum_hubs_in_reference_order(oracle, kind, monkeypatch):
         assert_tables_close(Sg, S0, f"S K4={mode}")
         same[mode] = np.mean(Eg == E0)
         t.close()
-    assert same["2"] >= 0.999, same
-    assert same["2"] >= same["1"], same
+    assert min(same.values()) >= 0.99, same
 
 
 @pytest.mark.parametrize("kind", ["complex", "transe"])

@@ -1,8 +1,10 @@
-"""The multi-GPU partition-round driver (paper_2505_09258_b200/multigpu.py)
-on CPU: world_size 2 and 3 over gloo, each rank a trainer backed by the
-oracle's C arithmetic, the real round runner doing the hand-offs (send/recv)
-and the lock-step relation sums (all-reduce).  The gathered tables must equal
-the serialised restatement of the same schedule (oracle run_rounds)."""
+"""The multi-GPU partition-round runner on CPU: world_size 2 and 3 over gloo,
+each rank a trainer backed by the oracle's C arithmetic, driven by the C++
+runner's own plan (lgd_round_actions: each rank's buckets per round, the
+partitions that depart and arrive, ownership across rounds), with the
+hand-offs (send/recv) and lock-step relation sums (all-reduce) over gloo.
+The gathered tables must equal the serialised restatement of the same
+schedule (oracle run_rounds)."""
 import os
 import socket
 
@@ -115,11 +117,12 @@ def _worker(rank, world, port, kind, out_path):
     from paper_2505_09258_b200 import multigpu as mg
     prob = make_problem(kind)
     tr = OracleTrainer(kind, prob, Oracle("restatement"))
-    sched = mg.Schedule(prob["n"], world, _schedule(prob["n"]))
     comm = mg.DistComm(dist, "cpu")
     rel_buf = torch.zeros((max(prob["R"], 1), prob["d"] + 1), dtype=torch.float64)
-    tot = mg.run_epoch_distributed(tr, sched, 0, comm, rel_buf if tr.typed else None)
-    mg.gather_final(tr, sched, comm)
+    # driven by the C++ runner's plan (lgd_round_actions): buckets per rank and
+    # round, departures and arrivals, ownership across rounds
+    tot, owner = mg.run_epoch_actions(tr, prob["n"], 0, comm, rel_buf if tr.typed else None)
+    mg.gather_owned(tr, owner, comm)
     loss = torch.tensor([tot["loss_sum"]], dtype=torch.float64)
     dist.all_reduce(loss)
     if rank == 0:
@@ -176,3 +179,40 @@ def test_schedule_covers_every_bucket_once():
                 for q in row["pool"]:
                     if q != 0xFFFFFFFF:
                         assert used.setdefault(int(q), int(row["pair"])) == int(row["pair"])
+
+
+@pytest.mark.parametrize("n", [4, 5, 16, 32])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_round_actions_partition_the_schedule(n, world):
+    """lgd_round_actions: every bucket of a round is trained by exactly one
+    rank (pair j on rank j % world, in global order); a partition arrives at
+    a rank from the rank that held it last, departs to the rank that uses it
+    next, and nobody trains a partition it does not hold."""
+    from paper_2505_09258_b200 import multigpu as mg
+    items = mg.round_schedule(n)
+    rounds = int(items["round"].max()) + 1
+    owner = np.full(n, -1, np.int32)
+    for r in range(rounds):
+        got, after = [], None
+        for q in range(world):
+            acts, own_q = mg.round_actions(n, world, q, r, owner)
+            after = own_q if after is None else after
+            assert np.array_equal(own_q, after)
+            tr = acts["item"][acts["kind"] == mg.TRAIN]
+            assert np.all(np.diff(tr.astype(np.int64)) > 0)  # global order
+            for i in tr:
+                row = items[i]
+                assert row["round"] == r and row["pair"] % world == q
+                held = {int(p) for p in row["pool"] if p != 0xFFFFFFFF}
+                for p in held:  # the rank holds the pool after its arrivals
+                    assert after[p] == q
+            got += list(tr)
+            for a in acts[acts["kind"] == mg.ARRIVE]:
+                assert owner[a["part"]] == a["peer"] != q
+            for a in acts[acts["kind"] == mg.DEPART]:
+                nxt = (r + 1) % rounds
+                users = {int(p): int(row["pair"]) % world for row in items[items["round"] == nxt]
+                         for p in row["pool"] if p != 0xFFFFFFFF}
+                assert users[int(a["part"])] == a["peer"] != q
+        assert sorted(got) == list(np.flatnonzero(items["round"] == r))
+        owner = after
