@@ -407,6 +407,43 @@ def bench_rounds(args, cfg, rank, world, local, pg):
         pg.destroy_process_group()
 
 
+def bench_eval(args, cfg, local):
+    """--eval T: K6 evaluate (train.cpp:375-412) at the workload's scale -- T
+    test edges (seeded uniform, synthetic), 999 sampled candidates each,
+    pessimistic ties -- timed on the device; roofline of the candidate-row
+    gathers ((999 + 2 + t) rows of 4d bytes per test edge)."""
+    import paper_2505_09258_b200 as lgd
+    t = setup_trainer(cfg, local)
+    rng = np.random.default_rng(7)
+    T = args.eval
+    test = np.stack([rng.integers(0, cfg["nodes"], T),
+                     rng.integers(0, cfg["rels"], T) if cfg["rels"] else np.full(T, 0xFFFFFFFF),
+                     rng.integers(0, cfg["nodes"], T)], 1).astype(np.uint32)
+    opts = lgd.EvalOptions(hits_k=10, num_candidates=999, seed=SEED)
+    t.evaluate(test[:min(T, 20000)], opts)  # warm-up
+    t.reset_kernel_stats()
+    t.set_profiling(True)
+    wall0 = time.perf_counter()
+    mrr, hits = t.evaluate(test, opts)
+    wall = time.perf_counter() - wall0
+    st = t.kernel_stats()["evaluate"]
+    t.set_profiling(False)
+    hbm, peak_kind = peaks()
+    dev_s = st["total_ms"] / 1e3
+    line = {"metric": "evaluate test edges/s (999 candidates, MRR / Hits@10)", "value": T / dev_s,
+            "unit": "test edges/s", "n_gpus": 1, "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["workload"], "test_edges": T,
+                                             "candidates": 999, "hits_k": 10},
+            "mrr": mrr, "hits_at_10": hits, "device_s": dev_s, "wall_s": wall,
+            "roofline": {"bound": "hbm", "kernel": "eval_candidates + eval_score (K6)",
+                         "achieved": st["algorithmic_bytes"] / dev_s / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": st["algorithmic_bytes"] / dev_s / 1e9 / hbm,
+                         "peak_source": peak_kind,
+                         "algorithmic_bytes": st["algorithmic_bytes"]}}
+    print(json.dumps(line), flush=True)
+    t.close()
+
+
 def traffic_from_profiles(config):
     """ncu DRAM bytes per launch of this config's kernels (profiles/ncu_traffic.json,
     one capture per config), or None when this config was not captured."""
@@ -429,6 +466,8 @@ def main():
                     help="rounds (default, every N): the partition-round schedule, so the "
                          "1/2/4/8-GPU points compare the same epoch; plan: the reference "
                          "iteration plan (run_epoch's 3-partition buffer; 1 GPU)")
+    ap.add_argument("--eval", type=int, default=0,
+                    help="T > 0: time K6 evaluate over T test edges instead of training")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--negatives", type=int, default=K_NEG,
@@ -445,6 +484,9 @@ def main():
         reference_arm(args, cfg, rank)
         return
     rank, world, local, pg = dist_setup(args.gpus)
+    if args.eval:
+        bench_eval(args, cfg, local)
+        return
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 

@@ -91,7 +91,8 @@ typedef struct {
 #define LGD_KSTAT_REL 3     /* relation sort + segmented reduce + Adagrad     */
 #define LGD_KSTAT_SAMPLE 4  /* per-bucket negative draws (K2)                 */
 #define LGD_KSTAT_SHUFFLE 5 /* per-bucket Fisher-Yates permutation + gather (K1) */
-#define LGD_KSTAT_COUNT 6
+#define LGD_KSTAT_EVAL 6    /* lgd_evaluate: candidates + scores (K6)          */
+#define LGD_KSTAT_COUNT 7
 
 const char* lgd_last_error(void);
 

@@ -690,6 +690,65 @@ int lgd_host_free(void* p) {
   });
 }
 
+// batch_gradients (train.cpp:280-340) as a GradientSet.  Exact path with
+// vector-lane dims: compact -- the sorted segment heads give the unique ids,
+// one warp per segment writes its FP64 row (O(unique rows) memory, ids
+// ascending like the reference's std::map).  Shared-negative chunks and the
+// 8-lane-group dims keep the dense scratch route.
+static void compact_gradients(lgd_context* ctx, uint64_t P, double* loss, uint64_t* num_nodes,
+                              uint32_t* node_ids, double* node_grads, uint64_t* num_rels,
+                              uint32_t* rel_ids, double* rel_grads) {
+  const uint64_t d = ctx->dim, n = P * (ctx->k() + 2);
+  DevBuf<uint32_t> seg, rseg, rk, rv, cnt;
+  DevBuf<unsigned char> temp;
+  seg.reserve(n + 1);
+  cnt.reserve(2);
+  const bool typed = ctx->typed() && ctx->R;
+  if (typed) {
+    rseg.reserve(P + 1);
+    rk.reserve(P);
+    rv.reserve(P);
+  }
+  temp.reserve(grads_select_temp_bytes(n));
+  LGD_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, ctx->stream));
+  GradCompact gc{seg.get(), typed ? rseg.get() : nullptr, rk.get(), rv.get(), cnt.get(),
+                 temp.get(), temp.bytes()};
+  BatchArgs a = ctx->batch_args(ctx->op_edges.get(), ctx->op_negs.get(), P, ctx->batch_losses.get());
+  a.side = nullptr;
+  a.gc = &gc;
+  launch_train_batch(a, ctx->stream, nullptr);
+  uint32_t c[2];
+  double l = 0;
+  LGD_CUDA(cudaMemcpyAsync(c, cnt.get(), 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LGD_CUDA(cudaMemcpyAsync(&l, ctx->batch_losses.get(), 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LGD_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint64_t nn = c[0], nr = typed ? c[1] : 0;
+  if (loss) *loss = l;
+  if (num_nodes) *num_nodes = nn;
+  if (num_rels) *num_rels = nr;
+  if (!node_ids && !node_grads && !rel_ids && !rel_grads) return;  // counts only
+  DevBuf<uint32_t> ni, ri;
+  DevBuf<double> ng, rg;
+  ni.reserve(std::max<uint64_t>(nn, 1));
+  ng.reserve(std::max<uint64_t>(nn, 1) * d);
+  ri.reserve(std::max<uint64_t>(nr, 1));
+  rg.reserve(std::max<uint64_t>(nr, 1) * d);
+  launch_grads_phase2(a, nn, nr, ni.get(), ng.get(), ri.get(), rg.get(), ctx->stream);
+  if (node_ids && nn)
+    LGD_CUDA(cudaMemcpyAsync(node_ids, ni.get(), nn * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (node_grads && nn)
+    LGD_CUDA(cudaMemcpyAsync(node_grads, ng.get(), nn * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rel_ids && nr)
+    LGD_CUDA(cudaMemcpyAsync(rel_ids, ri.get(), nr * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rel_grads && nr)
+    LGD_CUDA(cudaMemcpyAsync(rel_grads, rg.get(), nr * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LGD_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static bool compact_ok(const lgd_context* ctx) {
+  return !ctx->chunk() && k4_vec_width(ctx->kind, ctx->dim) != 0;
+}
+
 int lgd_train_batch(lgd_context* ctx, const uint32_t* edges, uint64_t num_positives,
                     const uint32_t* negatives, int apply, double* loss, uint64_t* unique_nodes,
                     uint64_t* unique_rels) {
@@ -702,6 +761,11 @@ int lgd_train_batch(lgd_context* ctx, const uint32_t* edges, uint64_t num_positi
     LGD_CUDA(cudaMemsetAsync(ctx->batch_losses.get(), 0, 8, ctx->stream));
     DevBuf<double> gn, gr;
     DevBuf<uint8_t> fn, fr;
+    if (!apply && compact_ok(ctx)) {  // loss + unique counts: the segment heads, no scratch rows
+      compact_gradients(ctx, num_positives, loss, unique_nodes, nullptr, nullptr, unique_rels,
+                        nullptr, nullptr);
+      return;
+    }
     if (!apply) {  // loss + unique counts only: route gradients to scratch
       gn.reserve(ctx->V * ctx->dim);
       fn.reserve(ctx->V);
@@ -738,6 +802,11 @@ int lgd_batch_gradients(lgd_context* ctx, const uint32_t* edges, uint64_t num_po
     if (!ctx) throw std::invalid_argument("null context");
     DeviceGuard g(ctx->device);
     ctx->upload_batch(edges, num_positives, negatives);
+    if (compact_ok(ctx)) {
+      compact_gradients(ctx, num_positives, loss, num_nodes, node_ids, node_grads, num_rels,
+                        rel_ids, rel_grads);
+      return;
+    }
     const uint64_t V = ctx->V, R = std::max<uint64_t>(ctx->R, 1), d = ctx->dim;
     DevBuf<double> gn, gr;
     DevBuf<uint8_t> fn, fr;
@@ -826,10 +895,14 @@ int lgd_evaluate(lgd_context* ctx, const uint32_t* test_edges, uint64_t count,
     LGD_CUDA(cudaMemcpyAsync(hr.data(), rr.get(), count * 8, cudaMemcpyDeviceToHost, ctx->stream));
     LGD_CUDA(cudaMemcpyAsync(hh.data(), hit.get(), count * 8, cudaMemcpyDeviceToHost, ctx->stream));
     LGD_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (ctx->profiling) {
+    if (ctx->profiling) {  // K6: (candidates + 1 + typed) rows and the edge record per test edge
       float ms = 0;
       LGD_CUDA(cudaEventElapsedTime(&ms, ctx->ev_begin, ctx->ev_end));
-      ctx->eval_ms = ms;
+      auto& ks = ctx->kstats[LGD_KSTAT_EVAL];
+      ks.launches += 1;
+      ks.total_ms += ms;
+      ks.algorithmic_bytes += double(count) * (12.0 + 4.0 * ctx->dim *
+                                               (num_candidates + 2.0 + (ctx->typed() ? 1 : 0)));
     }
     // result.mrr / hits_at_k accumulate in edge order, then / edges (train.cpp:406-411)
     double m = 0.0, hk = 0.0;

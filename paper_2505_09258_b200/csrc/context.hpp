@@ -100,6 +100,8 @@ struct lgd_context {
   // chunked pass 1 / pass 2 kernels instead (A/B)
   bool seg_rows = true;
   DevBuf<uint32_t> long_head, long_end, long_chunk_base, long_first, nlong;
+  DevBuf<double> rel64;  // FP64 relation rows for K4 (K3 writes them; R <= kRel64Max)
+  static constexpr uint64_t kRel64Max = 256;
   DevBuf<unsigned char> seg_temp;
   bool bucket_segs = false;  // the current bucket's long-segment list is built
   cudaEvent_t ev_long = nullptr, ev_long_done = nullptr;
@@ -143,7 +145,6 @@ struct lgd_context {
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<uint32_t> staging[2];
   uint64_t launches = 0;
-  double eval_ms = 0.0;  // device time of the last lgd_evaluate (profiling mode)
   size_t l2_persist = 0, l2_window_max = 0;  // L2 set-aside for the snapshot rows
   // optional host copy of the bucket-ordered edges (lgd_set_host_edges): the
   // bucket lists and rounds then stream every bucket H2D instead of reading
@@ -346,6 +347,11 @@ struct lgd_context {
     a.theta = theta.get();
     a.state = state.get();
     a.rel_theta = rel_theta.get();
+    a.rel64 = nullptr;
+    if (seg_rows && typed() && R && R <= kRel64Max && !chunk()) {
+      const_cast<DevBuf<double>&>(rel64).reserve(R * dim);
+      a.rel64 = rel64.get();
+    }
     a.rel_state = rel_state.get();
     a.lr = opt.learning_rate;
     a.eps = opt.adagrad_epsilon;
@@ -395,6 +401,7 @@ struct lgd_context {
     }
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
+    a.gc = nullptr;
     a.seg_mode = seg_rows ? 2 : 0;  // run_batch switches to the bucket's list
     a.long_head = long_head.get();
     a.long_end = long_end.get();

@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
   double* ebuf = reinterpret_cast<double*>(wbase + L.e_off);
   const size_t buf_floats = size_t(nrows) * dpad;
   const bool tma = use_tma && nrows <= 32;
+  if (KIND != 0 && a.rel64 && blockIdx.x == 0)  // K4's FP64 relation rows (exact conversion)
+    for (uint64_t i = threadIdx.x; i < a.num_rels * d; i += blockDim.x) a.rel64[i] = a.rel_theta[i];
 
   if (tma) {
     if (lane == 0) {
@@ -814,6 +816,35 @@ struct Lanes {
       }
     }
   }
+  // f64 rows (mix, IR1) in the lane's layout of ldd: double2 at off and at
+  // off + (ComplEx: h, else 2), staged by cp.async into the same positions
+  __device__ __forceinline__ void cpd_s(uint32_t s, const double* g) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!ok[v]) continue;
+      const uint32_t o2 = off[v] + (KIND == 2 ? h : 2);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 8 * off[v]),
+                   "l"(g + off[v])
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 8 * o2), "l"(g + o2)
+                   : "memory");
+    }
+  }
+  __device__ __forceinline__ void ldd_s(uint32_t s, double* x) const {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (ok[v]) {
+        const uint32_t o2 = off[v] + (KIND == 2 ? h : 2);
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0), "=d"(a1) : "r"(s + 8 * off[v]));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a2), "=d"(a3) : "r"(s + 8 * o2));
+      }
+      x[4 * v] = a0;
+      x[4 * v + 1] = a1;
+      x[4 * v + 2] = a2;
+      x[4 * v + 3] = a3;
+    }
+  }
   __device__ __forceinline__ void lds_s(uint32_t s, float* x) const {
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -940,6 +971,7 @@ struct SegCtx {  // hoisted kernel arguments
   uint32_t pshift, rmask;  // positive = val >> pshift; relation = (val >> sbits) & rmask (0: look up)
   uint64_t cpos_off;  // TransE: offset of the dst coefficients in w (P k)
   const float* gneg;  // shared-negative mode: gradient rows of the shared negatives
+  const double* rel64;  // the relation rows in FP64 (K3 writes them for small R), or null
 };
 
 template <int KIND, int NV, bool REL, bool SH, bool IR1 = k4_ir1(KIND)>
@@ -980,7 +1012,63 @@ __device__ __forceinline__ void load_item(const SegCtx& x, const Lanes<KIND, NV>
   L.ldd(x.mix + row, pred && is_src, it.mv);
 }
 
-template <int KIND, int NV, bool REL, bool SH, bool IR1 = k4_ir1(KIND)>
+// The first contribution of a K4 v2 segment, staged by cp.async with the
+// segment's rows (stage_item): its operand row (snapshot / IR1 / mix /
+// shared-negative gradient) at op_s, its weight at w_s.
+template <int KIND, int NV, bool SH, bool IR1>
+__device__ __forceinline__ void stage_item(const SegCtx& x, const Lanes<KIND, NV>& L, uint32_t val,
+                                           uint32_t op_s, uint32_t w_s, int lane) {
+  const uint32_t p = val >> x.pshift;
+  const uint32_t slot = val & x.smask;
+  const uint64_t row = (uint64_t)p * x.d;
+  if (SH && slot == 1) {
+    L.cpa_s(op_s, x.gneg + row, true);
+    return;
+  }
+  if (lane == 0 && (slot - 1u < x.k || (KIND == 3 && slot == 0))) {
+    const double* w = slot == 0 ? x.w + x.cpos_off + p : x.w + (uint64_t)p * x.k + (slot - 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(w_s), "l"(w) : "memory");
+  }
+  if (slot > x.k)
+    L.cpd_s(op_s, x.mix + row);
+  else if (IR1 && !SH)
+    L.cpd_s(op_s, x.ir1 + row);
+  else
+    L.cpa_s(op_s, x.snap + row, true);
+}
+template <int KIND, int NV, bool SH, bool IR1>
+__device__ __forceinline__ void load_item_staged(const SegCtx& x, const Lanes<KIND, NV>& L,
+                                                 uint32_t val, uint32_t op_s, uint32_t w_s,
+                                                 ItemRegs<4 * NV>& it) {
+  constexpr int NE = 4 * NV;
+  const uint32_t p = val >> x.pshift;
+  const uint32_t slot = val & x.smask;
+  const bool is_src = slot > x.k;
+  LGD_DCHECK(slot <= x.k + 1, "K4 contribution slot", slot);
+  it.slot = slot;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    it.sv[e] = 0.f;
+    it.mv[e] = 0.0;
+  }
+  if (SH && slot == 1) {
+    it.w = 0.0;
+    L.lds_s(op_s, it.sv);
+    return;
+  }
+  double wv = -1.0;
+  if (slot - 1u < x.k || (KIND == 3 && slot == 0))
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(w_s));
+  it.w = wv;
+  if (KIND != 0 && (is_src || !IR1 || SH))
+    it.rel = x.rmask ? (val >> x.sbits) & x.rmask : __ldg(x.rel_keys + p);
+  if (is_src || (IR1 && !SH))
+    L.ldd_s(op_s, it.mv);
+  else
+    L.lds_s(op_s, it.sv);
+}
+
+template <int KIND, int NV, bool REL, bool SH, bool IR1 = k4_ir1(KIND), bool R64 = false>
 __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV>& L,
                                            const ItemRegs<4 * NV>& it, uint32_t k, double* acc,
                                            const float* own) {
@@ -995,10 +1083,23 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
     for (int e = 0; e < NE; ++e) acc[e] += KIND == 3 ? it.w * (it.mv[e] - (double)own[e]) : it.w * it.mv[e];
     return;
   }
-  float rv[NE];
-  if (KIND != 0 && !REL) L.template ldf<true>(x.rel_theta + (uint64_t)it.rel * x.d, true, rv);
+  // the relation row in FP64: K3's copy (R64) or converted here -- the same
+  // values (f32 -> f64 is exact)
+  double rv[NE];
+  if (KIND != 0 && !REL) {
+    if (R64) {
+      L.ldd(x.rel64 + (uint64_t)it.rel * x.d, true, rv);
+    } else {
+      float rf[NE];
+      L.template ldf<true>(x.rel_theta + (uint64_t)it.rel * x.d, true, rf);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) rv[e] = rf[e];
+    }
+  }
   if (REL || it.slot > k) {  // adj_other(mix): other = src snapshot (REL) or relation row
-    const float* o = REL ? it.sv : rv;
+    double o[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) o[e] = REL ? (double)it.sv[e] : rv[e];
     if (KIND == 2) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
@@ -1012,14 +1113,14 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
     } else {
 #pragma unroll
       for (int e = 0; e < NE; ++e)
-        acc[e] += (KIND == 0 || KIND == 3) ? it.mv[e] : (double)o[e] * it.mv[e];
+        acc[e] += (KIND == 0 || KIND == 3) ? it.mv[e] : o[e] * it.mv[e];
     }
     return;
   }
   if (KIND == 3) {  // TransE: g += c (u - own row), u = s + r
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const double u = (double)it.sv[e] + (double)rv[e];
+      const double u = (double)it.sv[e] + rv[e];
       acc[e] += it.w * (u - (double)own[e]);
     }
     return;
@@ -1039,7 +1140,7 @@ __device__ __forceinline__ void add_loaded(const SegCtx& x, const Lanes<KIND, NV
   } else {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      const double u = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * (double)rv[e];
+      const double u = KIND == 0 ? (double)it.sv[e] : (double)it.sv[e] * rv[e];
       acc[e] += it.w * u;
     }
   }
@@ -1058,7 +1159,7 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_pass1_vec(
   const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
                  (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
                  (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
-                 a.P * a.k, a.sh_G};
+                 a.P * a.k, a.sh_G, nullptr};
   constexpr bool kOwn = KIND == 3 && !REL;  // TransE contributions read the node's own row
   float* __restrict__ theta = REL ? a.rel_theta : a.theta;
   float* __restrict__ state = REL ? a.rel_state : a.state;
@@ -1291,7 +1392,11 @@ __global__ void __launch_bounds__(kPass2Threads) segment_pass2(BatchArgs a, uint
 // No atomics on rows; every row is written by exactly one warp.
 constexpr uint32_t kLongSeg = 32;
 
-template <int KIND, int NV, bool SH, bool IR1>
+// ring slot of a segment (bytes): theta row, state row, the first
+// contribution's operand row (f64 width), its weight
+__host__ __device__ constexpr uint32_t seg_slot_bytes(uint32_t rowf) { return 16 * rowf + 16; }
+
+template <int KIND, int NV, bool SH, bool IR1, bool R64>
 __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
     BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     uint64_t b0, uint64_t b1) {
@@ -1303,7 +1408,7 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
   const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
                  (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
                  (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
-                 a.P * a.k, a.sh_G};
+                 a.P * a.k, a.sh_G, a.rel64};
   float* __restrict__ theta = a.theta;
   float* __restrict__ state = a.state;
   const uint64_t d = a.dim;
@@ -1332,7 +1437,7 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
   uint32_t todo = __ballot_sync(0xffffffffu, my_len != 0);
   if (!todo) return;
   const uint32_t my_row = my_len ? from_pool(a, key) : 0u;
-  LGD_DCHECK(my_row < a.num_nodes && my_len <= kLongSeg && base + lane + my_len <= b1,
+  LGD_DCHECK(!my_len || (my_row < a.num_nodes && my_len <= kLongSeg && base + lane + my_len <= b1),
              "K4 segment outside the batch / table", my_row);
   const uint32_t w0 = i < b1 ? __ldg(svals + i) : 0u;
   const uint32_t w1 = j < b1 ? __ldg(svals + j) : 0u;
@@ -1341,12 +1446,16 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
     const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
     return o < 32 ? v0 : v1;
   };
+  // ring of kSegDepth slots per warp: the theta / state rows AND the first
+  // contribution's operand row and weight of the next segments are in flight
+  // (cp.async, one commit group per segment), so a segment starts without a
+  // dependent global load
   extern __shared__ __align__(16) float seg_ring[];
   const uint32_t rowf = (a.dim + 3) & ~3u;
-  const uint32_t slotf = 2 * rowf;  // slot: theta, state
+  const uint32_t sb = seg_slot_bytes(rowf);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
-                        (threadIdx.x >> 5) * kSegDepth * slotf * 4;  // bytes
-  const uint32_t ring_end = ring + kSegDepth * slotf * 4;
+                        (threadIdx.x >> 5) * kSegDepth * sb;  // bytes
+  const uint32_t ring_end = ring + kSegDepth * sb;
   uint32_t srest = todo;  // segments still to stage, lowest first
   auto stage = [&](uint32_t slot) {
     if (srest) {
@@ -1355,11 +1464,12 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
       const uint64_t off = (uint64_t)__shfl_sync(0xffffffffu, my_row, h) * d;
       L.cpa_s(slot, theta + off, true);
       L.cpa_s(slot + rowf * 4, state + off, true);
+      stage_item<KIND, NV, SH, IR1>(x, L, item(h), slot + 8 * rowf, slot + 16 * rowf, lane);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int u = 0; u < kSegDepth; ++u) stage(ring + u * slotf * 4);
+  for (int u = 0; u < kSegDepth; ++u) stage(ring + u * sb);
   uint32_t slot = ring;
 #pragma unroll 1
   while (todo) {
@@ -1367,26 +1477,29 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
     todo &= todo - 1;
     const uint32_t len = __shfl_sync(0xffffffffu, my_len, h);
     const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
-    ItemRegs<NE> cit;
-    load_item<KIND, NV, false, SH, IR1>(x, L, item(h), true, cit);
+    const uint32_t v0 = item(h);
     asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
+    __syncwarp();  // lane 0 staged the weight every lane reads
     float th[NE], st[NE];
     L.lds_s(slot, th);
     L.lds_s(slot + rowf * 4, st);
+    ItemRegs<NE> cit;
+    load_item_staged<KIND, NV, SH, IR1>(x, L, v0, slot + 8 * rowf, slot + 16 * rowf, cit);
     double acc[NE];
 #pragma unroll
     for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-    add_loaded<KIND, NV, false, SH, IR1>(x, L, cit, x.k, acc, th);
+    add_loaded<KIND, NV, false, SH, IR1, R64>(x, L, cit, x.k, acc, th);
     for (uint32_t q = h + 1; q < h + len; ++q) {
       ItemRegs<NE> it;
       load_item<KIND, NV, false, SH, IR1>(x, L, item(q), true, it);
-      add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, th);
+      add_loaded<KIND, NV, false, SH, IR1, R64>(x, L, it, x.k, acc, th);
     }
     adagrad_lanes(L, acc, th, st, lr, eps);
     L.stf(theta + (uint64_t)row * d, th);
     L.stf(state + (uint64_t)row * d, st);
+    __syncwarp();  // every lane read the weight before the slot is restaged
     stage(slot);  // the slot just read is free again
-    slot = slot + slotf * 4 == ring_end ? ring : slot + slotf * 4;
+    slot = slot + sb == ring_end ? ring : slot + sb;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -1401,7 +1514,7 @@ struct LongList {
   const uint32_t* first;  // nb + 1 entries
 };
 
-template <int KIND, int NV, bool SH, bool IR1>
+template <int KIND, int NV, bool SH, bool IR1, bool R64>
 __global__ void __launch_bounds__(kSegThreads) long_chunks(
     BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     LongList ll, uint32_t batch, double* __restrict__ part) {
@@ -1413,7 +1526,7 @@ __global__ void __launch_bounds__(kSegThreads) long_chunks(
   const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
                  (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
                  (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
-                 a.P * a.k, a.sh_G};
+                 a.P * a.k, a.sh_G, a.rel64};
   const uint32_t c0 = ll.chunk_base[lf], c1 = ll.chunk_base[le];
   const uint64_t d = a.dim;
   const uint32_t nwarps = gridDim.x * (kSegThreads / 32);
@@ -1439,7 +1552,7 @@ __global__ void __launch_bounds__(kSegThreads) long_chunks(
     for (uint32_t q = q0; q < q1; ++q) {
       ItemRegs<NE> it;
       load_item<KIND, NV, false, SH, IR1>(x, L, __shfl_sync(0xffffffffu, w, q - q0), true, it);
-      add_loaded<KIND, NV, false, SH, IR1>(x, L, it, x.k, acc, own);
+      add_loaded<KIND, NV, false, SH, IR1, R64>(x, L, it, x.k, acc, own);
     }
     L.std_(part + (uint64_t)(c - c0) * d, acc);
   }
@@ -1556,10 +1669,10 @@ size_t g_score_occ_smem[kMaxDevices][4];
 int g_score_occ[kMaxDevices][4];
 
 void sort_items(const BatchArgs& a, uint64_t items, const uint32_t* keys, const uint32_t* vals,
-                int key_bits, cudaStream_t st) {
+                int key_bits, cudaStream_t st, uint32_t* okeys = nullptr, uint32_t* ovals = nullptr) {
   size_t bytes = a.sort_temp_bytes;
-  LGD_CUDA(cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, keys, a.skeys, vals, a.svals,
-                                           (int64_t)items, 0, key_bits, st));
+  LGD_CUDA(cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, keys, okeys ? okeys : a.skeys, vals,
+                                           ovals ? ovals : a.svals, (int64_t)items, 0, key_bits, st));
 }
 
 // vector-lane pass 1 when the dimension fits one (NV = 1) or two (NV = 2)
@@ -1596,13 +1709,13 @@ void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStr
     launch_vec_pass1_<KIND, NV, REL, SH, false>(a, items, grid, st);
 }
 
-template <int KIND, int NV, bool SH, bool IR1>
+template <int KIND, int NV, bool SH, bool IR1, bool R64>
 void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStream_t st) {
-  const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * 2 * ((a.dim + 3) & ~3u) * 4;
+  const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * seg_slot_bytes((a.dim + 3) & ~3u);
   static size_t attr[kMaxDevices];
   const int dev = current_device();
   if (smem > attr[dev]) {
-    LGD_CUDA(cudaFuncSetAttribute(segment_heads<KIND, NV, SH, IR1>,
+    LGD_CUDA(cudaFuncSetAttribute(segment_heads<KIND, NV, SH, IR1, R64>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[dev] = smem;
   }
@@ -1614,7 +1727,7 @@ void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStr
     LGD_CUDA(cudaStreamWaitEvent(a.side, a.ev_long, 0));
     ls = a.side;
   }
-  long_chunks<KIND, NV, SH, IR1><<<(unsigned)a.sm_count * 2, kSegThreads, 0, ls>>>(
+  long_chunks<KIND, NV, SH, IR1, R64><<<(unsigned)a.sm_count * 2, kSegThreads, 0, ls>>>(
       a, a.seg_keys, a.seg_vals, ll, a.seg_batch, a.part_first);
   LGD_LAUNCH_CHECK();
   long_combine<KIND, NV><<<(unsigned)a.sm_count, kSegThreads, 0, ls>>>(a, a.seg_keys, ll,
@@ -1622,8 +1735,8 @@ void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStr
   LGD_LAUNCH_CHECK();
   if (a.side) LGD_CUDA(cudaEventRecord(a.ev_long_done, a.side));
   const unsigned grid = (unsigned)ceil_div(ceil_div(b1 - b0, 32), kSegThreads / 32);
-  segment_heads<KIND, NV, SH, IR1><<<grid, kSegThreads, smem, st>>>(a, a.seg_keys, a.seg_vals, b0,
-                                                                    b1);
+  segment_heads<KIND, NV, SH, IR1, R64><<<grid, kSegThreads, smem, st>>>(a, a.seg_keys, a.seg_vals,
+                                                                         b0, b1);
   LGD_LAUNCH_CHECK();
   if (a.side) LGD_CUDA(cudaStreamWaitEvent(st, a.ev_long_done, 0));
 }
@@ -1648,14 +1761,30 @@ bool segment_rows_node_pass(BatchArgs& a, uint64_t items, cudaStream_t st) {
   }
   if constexpr (KIND != 3 || !SH) {
     constexpr bool kIr1 = k4_ir1(KIND) && !SH;
+    constexpr bool kR64 = KIND != 0;
     const bool ir1 = kIr1 && a.ir1 != nullptr;
+    const bool r64 = kR64 && a.rel64 != nullptr;
+    auto go = [&](auto nvc, auto ir1c, auto r64c) {
+      launch_segment_heads_<KIND, decltype(nvc)::value, SH, decltype(ir1c)::value,
+                            decltype(r64c)::value>(a, b0, b0 + items, st);
+    };
+    using T = std::true_type;
+    using F = std::false_type;
+    using N1 = std::integral_constant<int, 1>;
+    using N2 = std::integral_constant<int, 2>;
     if (nv == 1) {
-      if (ir1) launch_segment_heads_<KIND, 1, SH, kIr1>(a, b0, b0 + items, st);
-      else launch_segment_heads_<KIND, 1, SH, false>(a, b0, b0 + items, st);
+      if (ir1) {
+        if (r64) go(N1{}, std::integral_constant<bool, kIr1>{}, std::integral_constant<bool, kR64>{});
+        else go(N1{}, std::integral_constant<bool, kIr1>{}, F{});
+      } else {
+        if (r64) go(N1{}, F{}, std::integral_constant<bool, kR64>{});
+        else go(N1{}, F{}, F{});
+      }
     } else {
-      if (ir1) launch_segment_heads_<KIND, 2, SH, kIr1>(a, b0, b0 + items, st);
-      else launch_segment_heads_<KIND, 2, SH, false>(a, b0, b0 + items, st);
+      if (ir1) go(N2{}, std::integral_constant<bool, kIr1>{}, F{});
+      else go(N2{}, F{}, F{});
     }
+    (void)sizeof(T);
   }
   return true;
 }
@@ -1780,6 +1909,88 @@ void rel_pass_finish(const BatchArgs& a, cudaStream_t st) {
   LGD_LAUNCH_CHECK();
 }
 
+// ------------------------------------- compact batch_gradients (operator)
+// batch_gradients (train.cpp:280-340) as a GradientSet: the sorted unique
+// node / relation ids and one FP64 gradient row each, O(unique rows) memory.
+// Phase 1: the sorted contributions' segment heads (nodes and relations);
+// phase 2: one warp per segment sums its contributions sequentially in the
+// reference's order and writes row s of the output.
+// segment heads of sorted keys: the first item, or a key change
+struct HeadFlag {
+  const uint32_t* keys;
+  __host__ __device__ __forceinline__ bool operator()(const uint32_t& i) const {
+    return i == 0 || keys[i] != keys[i - 1];
+  }
+};
+
+void grads_phase1(const BatchArgs& a, uint64_t n, cudaStream_t st) {
+  size_t bytes = a.gc->temp_bytes;
+  LGD_CUDA(cub::DeviceSelect::If(a.gc->temp, bytes, thrust::counting_iterator<uint32_t>(0),
+                                 a.gc->node_seg, a.gc->counts, (int64_t)n, HeadFlag{a.skeys}, st));
+  if (a.gc->rel_seg) {
+    sort_items(a, a.P, a.rel_keys, a.iota, a.rel_key_bits, st, a.gc->rel_skeys, a.gc->rel_svals);
+    bytes = a.gc->temp_bytes;
+    LGD_CUDA(cub::DeviceSelect::If(a.gc->temp, bytes, thrust::counting_iterator<uint32_t>(0),
+                                   a.gc->rel_seg, a.gc->counts + 1, (int64_t)a.P,
+                                   HeadFlag{a.gc->rel_skeys}, st));
+  }
+}
+
+template <int KIND, int NV, bool REL>
+__global__ void __launch_bounds__(kSegThreads) grad_segments(BatchArgs a, const uint32_t* __restrict__ skeys,
+                                                             const uint32_t* __restrict__ svals, uint64_t n,
+                                                             const uint32_t* __restrict__ seg, uint64_t nseg,
+                                                             uint32_t* __restrict__ ids, double* __restrict__ out) {
+  constexpr int NE = 4 * NV;
+  const int lane = threadIdx.x & 31;
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G, nullptr};
+  const uint64_t d = a.dim;
+  const uint64_t nw = (uint64_t)gridDim.x * (kSegThreads / 32);
+  for (uint64_t s = ((uint64_t)blockIdx.x * kSegThreads + threadIdx.x) >> 5; s < nseg; s += nw) {
+    const uint32_t q0 = seg[s], q1 = s + 1 < nseg ? seg[s + 1] : (uint32_t)n;
+    const uint32_t key = skeys[q0];
+    const uint32_t row = REL ? key : from_pool(a, key);
+    float own[NE];
+    if (KIND == 3 && !REL) L.template ldf<true>(a.theta + (uint64_t)row * d, true, own);
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    for (uint32_t q = q0; q < q1; ++q) {  // every contribution, in order
+      ItemRegs<NE> it;
+      load_item<KIND, NV, REL, false>(x, L, __ldg(svals + q), true, it);
+      add_loaded<KIND, NV, REL, false>(x, L, it, x.k, acc, own);
+    }
+    L.std_(out + s * d, acc);
+    if (lane == 0) ids[s] = row;
+  }
+}
+
+template <int KIND>
+void grads_phase2_kind(const BatchArgs& a, uint64_t nn, uint64_t nr, uint32_t* node_ids,
+                       double* node_grads, uint32_t* rel_ids, double* rel_grads, cudaStream_t st) {
+  const int nv = vec_width<KIND>(a.dim);
+  const unsigned grid = (unsigned)a.sm_count * 8;
+  const uint64_t n = a.P * (a.k + 2);
+  if (nn) {
+    if (nv == 1)
+      grad_segments<KIND, 1, false><<<grid, kSegThreads, 0, st>>>(a, a.skeys, a.svals, n, a.gc->node_seg, nn, node_ids, node_grads);
+    else
+      grad_segments<KIND, 2, false><<<grid, kSegThreads, 0, st>>>(a, a.skeys, a.svals, n, a.gc->node_seg, nn, node_ids, node_grads);
+    LGD_LAUNCH_CHECK();
+  }
+  if (KIND != 0 && nr) {
+    if (nv == 1)
+      grad_segments<KIND, 1, true><<<grid, kSegThreads, 0, st>>>(a, a.gc->rel_skeys, a.gc->rel_svals, a.P, a.gc->rel_seg, nr, rel_ids, rel_grads);
+    else
+      grad_segments<KIND, 2, true><<<grid, kSegThreads, 0, st>>>(a, a.gc->rel_skeys, a.gc->rel_svals, a.P, a.gc->rel_seg, nr, rel_ids, rel_grads);
+    LGD_LAUNCH_CHECK();
+  }
+}
+
 template <int KIND, int NC>
 void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   BatchArgs a = a_in;
@@ -1831,6 +2042,10 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   rec(1);
   if (a.side) rel_pass_start<KIND, NC>(a, st);
   if (!a.presorted) sort_items(a, P * (k + 2), a.node_keys, a.node_vals, a.node_key_bits, st);
+  if (a.gc) {  // compact gradients (batch_gradients): sorted runs + segment heads, no update
+    grads_phase1(a, P * (k + 2), st);
+    return;
+  }
   rec(2);
   if (a.grad_nodes || !segment_rows_node_pass<KIND, false>(a, P * (k + 2), st))
     run_segments<KIND, NC>(a, P * (k + 2), false, st);
@@ -1981,6 +2196,24 @@ void launch_bucket_keys(const BatchArgs& a, uint64_t m, uint64_t B, uint32_t* ke
   const unsigned grid = (unsigned)(blocks < (uint64_t)a.sm_count * 16 ? blocks : (uint64_t)a.sm_count * 16);
   presort_keys_kernel<<<grid, 256, 0, st>>>(a, m, B, keys, vals);
   LGD_LAUNCH_CHECK();
+}
+
+void launch_grads_phase2(const BatchArgs& a, uint64_t nn, uint64_t nr, uint32_t* node_ids,
+                         double* node_grads, uint32_t* rel_ids, double* rel_grads, cudaStream_t st) {
+  switch (a.kind) {
+    case 0: return grads_phase2_kind<0>(a, nn, nr, node_ids, node_grads, rel_ids, rel_grads, st);
+    case 1: return grads_phase2_kind<1>(a, nn, nr, node_ids, node_grads, rel_ids, rel_grads, st);
+    case 2: return grads_phase2_kind<2>(a, nn, nr, node_ids, node_grads, rel_ids, rel_grads, st);
+    default: return grads_phase2_kind<3>(a, nn, nr, node_ids, node_grads, rel_ids, rel_grads, st);
+  }
+}
+
+size_t grads_select_temp_bytes(uint64_t max_items) {
+  size_t b = 0;
+  LGD_CUDA(cub::DeviceSelect::If(nullptr, b, thrust::counting_iterator<uint32_t>(0),
+                                 (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                 (int64_t)(max_items ? max_items : 1), HeadFlag{nullptr}));
+  return b;
 }
 
 int k4_vec_width(int kind, uint32_t dim) {

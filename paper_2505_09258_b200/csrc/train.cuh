@@ -32,6 +32,16 @@ struct SegLists {  // K4 v2 long-segment list (launch_long_list)
   size_t temp_bytes;
 };
 
+struct GradCompact {  // compact batch_gradients (launch_train_batch phase 1, then phase 2)
+  uint32_t* node_seg;         // segment heads of the sorted node contributions (P (k+2))
+  uint32_t* rel_seg;          // of the sorted relation ids (P), or null (untyped)
+  uint32_t* rel_skeys;        // the relation sort's output (P)
+  uint32_t* rel_svals;
+  uint32_t* counts;           // [unique nodes, unique relations] (device)
+  void* temp;
+  size_t temp_bytes;
+};
+
 struct BatchArgs {
   int kind;
   uint32_t dim;
@@ -43,6 +53,7 @@ struct BatchArgs {
   float* theta;               // V x d embeddings
   float* state;               // V x d Adagrad accumulators
   float* rel_theta;           // R x d
+  double* rel64;              // R x d FP64 copy K3 writes for K4 (small R), or null
   float* rel_state;           // R x d
   double lr;
   double eps;
@@ -124,6 +135,7 @@ struct BatchArgs {
   uint32_t* long_first;
   SegLists seg_lists;         // the buffers, for a one-batch list (seg_mode 2)
   cudaEvent_t ev_long, ev_long_done;  // long segments on the side stream
+  const GradCompact* gc;      // non-null: stop after the sorts (compact gradients, phase 1)
   cudaStream_t side;
   cudaEvent_t ev_scored, ev_rel;
   uint64_t num_rels;
@@ -170,6 +182,13 @@ size_t bucket_sort_temp_bytes(uint64_t max_items);
 size_t long_list_temp_bytes(uint64_t max_items);
 void launch_long_list(const uint32_t* keys, uint64_t n, uint64_t batch_items, uint32_t nb,
                       const SegLists& lists, cudaStream_t st);
+// Compact gradients, phase 2 (after launch_train_batch with a.gc set and the
+// counts read back): row s of node_grads / rel_grads = the FP64 gradient of
+// unique id s, ids ascending.
+void launch_grads_phase2(const BatchArgs& a, uint64_t num_nodes, uint64_t num_rels,
+                         uint32_t* node_ids, double* node_grads, uint32_t* rel_ids,
+                         double* rel_grads, cudaStream_t st);
+size_t grads_select_temp_bytes(uint64_t max_items);
 // 16-byte vectors per lane of K4's vector kernels for (kind, dim); 0 = the
 // 8-lane-group fallback (which never reads K3's IR1 rows)
 int k4_vec_width(int kind, uint32_t dim);

@@ -22,8 +22,8 @@ LIB_PATH = os.environ.get("LGD_LIBRARY") or os.path.join(_HERE, "liblegend_b200.
 MODELS = {"dot": 0, "distmult": 1, "complex": 2, "transe": 3}
 NO_RELATION = 0xFFFFFFFF
 
-KSTAT_SCORE, KSTAT_SORT, KSTAT_UPDATE, KSTAT_REL, KSTAT_SAMPLE, KSTAT_SHUFFLE = range(6)
-KSTAT_NAMES = ["score", "sort", "update", "relations", "sample", "shuffle"]
+KSTAT_SCORE, KSTAT_SORT, KSTAT_UPDATE, KSTAT_REL, KSTAT_SAMPLE, KSTAT_SHUFFLE, KSTAT_EVAL = range(7)
+KSTAT_NAMES = ["score", "sort", "update", "relations", "sample", "shuffle", "evaluate"]
 
 
 class InvalidArgument(ValueError):
