@@ -1504,6 +1504,194 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// --------------------------- K4 v3: warp-specialised whole-segment updates
+// The same segments as segment_heads (<= kLongSeg contributions, summed whole
+// in the reference order), split between producer and consumer warps so
+// neither carries the other's registers or bookkeeping:
+//   producer warps  decode 32 sorted items at a time lane-parallel (heads,
+//                   lengths, rows, first payloads) and stage each segment into
+//                   a consumer's ring slot with cp.async: its theta / state
+//                   rows, its first contribution's operand row and weight, and
+//                   its metadata; completion is tracked by the slot's mbarrier
+//                   (cp.async.mbarrier.arrive.noinc), so the producer never
+//                   waits for its copies;
+//   consumer warps  wait on the slot, sum the contributions (the first from
+//                   shared memory, any others from global), run the Adagrad
+//                   row update, store the row and release the slot.
+// Block: kWsProducers producers, kWsConsumers consumers (each producer feeds
+// its own kWsConsumers / kWsProducers), kWsDepth slots per consumer.
+#ifndef WS_PRODUCERS
+#define WS_PRODUCERS 4
+#endif
+constexpr int kWsProducers = WS_PRODUCERS;
+constexpr int kWsConsumers = 8;
+constexpr int kWsDepth = 3;
+constexpr int kWsThreads = (kWsProducers + kWsConsumers) * 32;
+constexpr int kWsPer = kWsConsumers / kWsProducers;
+constexpr uint32_t kWsChunks = 64;  // 32-item chunks per block
+// slot (bytes): theta 4 rowf | state 4 rowf | operand 8 rowf | weight 8 | meta 16
+__host__ __device__ constexpr uint32_t ws_slot_bytes(uint32_t rowf) { return 16 * rowf + 32; }
+__host__ __device__ constexpr uint32_t ws_bar_bytes() { return 2 * kWsConsumers * kWsDepth * 8; }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cpasync(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+// waits with a back-off so a waiting warp does not take issue slots from the
+// warps doing work
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  if (mbar_try_wait(bar, phase)) return;
+  uint32_t ns = 32;
+  while (!mbar_try_wait(bar, phase)) {
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : ns;
+  }
+}
+
+template <int KIND, int NV, bool SH, bool IR1, bool R64>
+__global__ void __launch_bounds__(kWsThreads, 2) segment_ws(
+    BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+    uint64_t b0, uint64_t b1) {
+  constexpr int NE = 4 * NV;
+  extern __shared__ __align__(16) unsigned char ws_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ws_smem);  // [consumer][slot]
+  uint64_t* empty = full + kWsConsumers * kWsDepth;
+  const uint32_t rowf = (a.dim + 3) & ~3u;
+  const uint32_t sb = ws_slot_bytes(rowf);
+  const uint32_t slots = (uint32_t)__cvta_generic_to_shared(ws_smem) + ws_bar_bytes();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsConsumers * kWsDepth; ++i) {
+      mbar_init(full + i, 33);  // 32 producer lanes' copies + the metadata arrive
+      mbar_init(empty + i, 1);  // the consumer's release
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < kWsConsumers * kWsDepth; ++i) mbar_arrive(empty + i);  // slots start free
+  }
+  __syncthreads();
+  const Lanes<KIND, NV> L(lane, a.dim);
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G, a.rel64};
+  const uint64_t d = a.dim;
+  auto slot_addr = [&](int c, int s) { return slots + (uint32_t)(c * kWsDepth + s) * sb; };
+  if (warp < kWsProducers) {
+    // ----------------------------------------------------------- producer
+    const uint64_t cb0 = b0 + (uint64_t)blockIdx.x * kWsChunks * 32;
+    const uint64_t cb1 = min(b1, cb0 + (uint64_t)kWsChunks * 32);
+    uint32_t state = 0;  // per own consumer: use count mod 2 kWsDepth, 3 bits each
+    int rr = 0;          // next own consumer
+    auto claim = [&](int& c, uint32_t& sa, uint32_t& par) {
+      const uint32_t st = (state >> (3 * rr)) & 7u;
+      c = warp * kWsPer + rr;
+      const int s = (int)(st % kWsDepth);
+      par = st / kWsDepth;
+      state = (state & ~(7u << (3 * rr))) | (((st + 1) % (2 * kWsDepth)) << (3 * rr));
+      rr = (rr + 1) % kWsPer;
+      mbar_wait(empty + c * kWsDepth + s, par);
+      sa = slot_addr(c, s);
+      return s;
+    };
+    for (uint64_t base = cb0 + (uint64_t)warp * 32; base < cb1; base += kWsProducers * 32) {
+      const uint64_t i = base + lane, j = i + 32;
+      const uint32_t key = i < b1 ? __ldg(skeys + i) : 0u;
+      const uint32_t key2 = j < b1 ? __ldg(skeys + j) : 0u;
+      const uint32_t prev = (i < b1 && i > b0) ? __ldg(skeys + i - 1) : ~key;
+      const uint32_t prev2 = __shfl_sync(0xffffffffu, key, 31);
+      const uint32_t prev2_l = __shfl_up_sync(0xffffffffu, key2, 1);
+      const bool head = i < b1 && key != prev;
+      const bool term2 = j >= b1 || key2 != (lane ? prev2_l : prev2);
+      const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+      const uint32_t tmask0 = __ballot_sync(0xffffffffu, head || i >= b1);
+      const uint32_t tmask1 = __ballot_sync(0xffffffffu, term2);
+      const uint64_t ends = (uint64_t)tmask0 | ((uint64_t)tmask1 << 32);
+      if (lane == 0 && hmask) atomicAdd(a.counters, (unsigned long long)__popc(hmask));
+      uint32_t my_len = 0;
+      if (head) {
+        const uint64_t above = ends & ~((2ull << lane) - 1);
+        const uint32_t e = above ? (uint32_t)__ffsll((long long)above) - 1 : 64u;
+        my_len = e - lane <= kLongSeg ? e - lane : 0u;
+      }
+      uint32_t todo = __ballot_sync(0xffffffffu, my_len != 0);
+      const uint32_t my_row = my_len ? from_pool(a, key) : 0u;
+      const uint32_t my_val = i < b1 ? __ldg(svals + i) : 0u;  // a head's own first item
+      LGD_DCHECK(!my_len || (my_row < a.num_nodes && base + lane + my_len <= b1),
+                 "K4 segment outside the batch / table", my_row);
+      while (todo) {
+        const int h = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
+        const uint32_t val = __shfl_sync(0xffffffffu, my_val, h);
+        const uint32_t len = __shfl_sync(0xffffffffu, my_len, h);
+        int c;
+        uint32_t sa, par;
+        const int s = claim(c, sa, par);
+        const uint64_t off = (uint64_t)row * d;
+        L.cpa_s(sa, a.theta + off, true);
+        L.cpa_s(sa + 4 * rowf, a.state + off, true);
+        stage_item<KIND, NV, SH, IR1>(x, L, val, sa + 8 * rowf, sa + 16 * rowf, lane);
+        if (lane == 0) {
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16 * rowf + 16),
+                       "r"(row), "r"(len), "r"((uint32_t)(base + h)), "r"(val)
+                       : "memory");
+          mbar_arrive(full + c * kWsDepth + s);
+        }
+        mbar_arrive_cpasync(full + c * kWsDepth + s);
+      }
+    }
+    for (int t = 0; t < kWsPer; ++t) {  // end of work: a zero-length slot per consumer
+      int c;
+      uint32_t sa, par;
+      const int s = claim(c, sa, par);
+      if (lane == 0) {
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16 * rowf + 16),
+                     "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+                     : "memory");
+        mbar_arrive(full + c * kWsDepth + s);
+      }
+      mbar_arrive_cpasync(full + c * kWsDepth + s);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  // ------------------------------------------------------------- consumer
+  const int c = warp - kWsProducers;
+  const double lr = a.lr, eps = a.eps;
+  for (uint32_t k = 0;; ++k) {
+    const int s = (int)(k % kWsDepth);
+    mbar_wait(full + c * kWsDepth + s, (k / kWsDepth) & 1u);
+    const uint32_t sa = slot_addr(c, s);
+    uint32_t row, len, q0, val;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(row), "=r"(len), "=r"(q0), "=r"(val)
+                 : "r"(sa + 16 * rowf + 16));
+    if (len == 0) break;
+    float th[NE], st[NE];
+    L.lds_s(sa, th);
+    L.lds_s(sa + 4 * rowf, st);
+    ItemRegs<NE> cit;
+    load_item_staged<KIND, NV, SH, IR1>(x, L, val, sa + 8 * rowf, sa + 16 * rowf, cit);
+    double acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+    add_loaded<KIND, NV, false, SH, IR1, R64>(x, L, cit, x.k, acc, th);
+    for (uint32_t q = q0 + 1; q < q0 + len; ++q) {
+      ItemRegs<NE> it;
+      load_item<KIND, NV, false, SH, IR1>(x, L, __ldg(svals + q), true, it);
+      add_loaded<KIND, NV, false, SH, IR1, R64>(x, L, it, x.k, acc, th);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + c * kWsDepth + s);  // slot read: release it
+    adagrad_lanes(L, acc, th, st, lr, eps);
+    L.stf(a.theta + (uint64_t)row * d, th);
+    L.stf(a.state + (uint64_t)row * d, st);
+  }
+}
+
 // The bucket's long segments (launch_long_list): head item, end item,
 // exclusive prefix of their 32-item chunk counts, first long segment of each
 // batch.  Chunk c of long segment j covers items head + 32 (c - base[j]) + [0, 32).
@@ -1734,9 +1922,22 @@ void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStr
                                                                       a.seg_batch, a.part_first);
   LGD_LAUNCH_CHECK();
   if (a.side) LGD_CUDA(cudaEventRecord(a.ev_long_done, a.side));
-  const unsigned grid = (unsigned)ceil_div(ceil_div(b1 - b0, 32), kSegThreads / 32);
-  segment_heads<KIND, NV, SH, IR1, R64><<<grid, kSegThreads, smem, st>>>(a, a.seg_keys, a.seg_vals,
-                                                                         b0, b1);
+  if (a.k4_ws) {
+    const size_t wsm = ws_bar_bytes() + (size_t)kWsConsumers * kWsDepth * ws_slot_bytes((a.dim + 3) & ~3u);
+    static size_t wattr[kMaxDevices];
+    if (wsm > wattr[dev]) {
+      LGD_CUDA(cudaFuncSetAttribute(segment_ws<KIND, NV, SH, IR1, R64>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+      wattr[dev] = wsm;
+    }
+    const unsigned wgrid = (unsigned)ceil_div(b1 - b0, (uint64_t)kWsChunks * 32);
+    segment_ws<KIND, NV, SH, IR1, R64><<<wgrid, kWsThreads, wsm, st>>>(a, a.seg_keys, a.seg_vals,
+                                                                       b0, b1);
+  } else {
+    const unsigned grid = (unsigned)ceil_div(ceil_div(b1 - b0, 32), kSegThreads / 32);
+    segment_heads<KIND, NV, SH, IR1, R64><<<grid, kSegThreads, smem, st>>>(a, a.seg_keys,
+                                                                           a.seg_vals, b0, b1);
+  }
   LGD_LAUNCH_CHECK();
   if (a.side) LGD_CUDA(cudaStreamWaitEvent(st, a.ev_long_done, 0));
 }

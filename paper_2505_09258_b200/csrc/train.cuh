@@ -125,6 +125,7 @@ struct BatchArgs {
   // arrays, this batch = items [seg_b0, seg_b0 + P(k+2)), batch index
   // seg_batch); 2 = build a one-batch list after this batch's sort
   int seg_mode;
+  int k4_ws;                  // K4 v3: warp-specialised producer / consumer kernel
   const uint32_t* seg_keys;
   const uint32_t* seg_vals;
   uint64_t seg_b0;
