@@ -125,6 +125,15 @@ int lgd_write_graph(const char* dir, const uint32_t* edges, uint64_t num_edges, 
 int lgd_read_graph_meta(const char* dir, uint64_t* num_edges, uint64_t* num_nodes,
                         uint64_t* num_relations);
 int lgd_read_graph(const char* dir, uint32_t* edges_out, uint64_t num_edges);
+/* ingest (graph.cpp:39-118), host only: a TSV edge list of 3 (triples != 0)
+ * or 2 decimal columns per line, '#' lines and blank lines skipped, parsed by
+ * `threads` host threads (0 = all).  remap_ids: dense ids in first-appearance
+ * order.  *edges_out: num_edges records allocated by the library, released
+ * with lgd_free_edges.  Malformed input is LGD_RUNTIME_ERROR carrying the
+ * reference's ParseError text with the line number. */
+int lgd_ingest_tsv(const char* path, int triples, int remap_ids, int threads, uint32_t** edges_out,
+                   uint64_t* num_edges, uint64_t* num_nodes, uint64_t* num_relations);
+void lgd_free_edges(uint32_t* edges);
 
 /* make_partition_plan (graph.cpp:120-150), computed on the device.  Outputs
  * may be NULL; bucket_offsets has n*n+1 entries, edge_order num_edges. */

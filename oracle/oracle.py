@@ -104,6 +104,7 @@ class Oracle:
                                               i32, u32, vp, vp, u64, vp, vp, u64, f64, f64, vp,
                                               vp, vp, u64])
             bind("write_graph", i32, [C.c_char_p, vp, u64, u64, u64])
+            bind("ingest", i32, [C.c_char_p, i32, i32, vp, u64, vp, vp, vp])
             bind("read_graph", i32, [C.c_char_p, vp, u64, vp, vp, vp])
 
     def _check(self, rc):
@@ -342,6 +343,17 @@ class Oracle:
         edges = np.ascontiguousarray(edges, np.uint32).reshape(-1, 3)
         self._check(self._fn["write_graph"](os.fsencode(directory), _ptr(edges), len(edges),
                                             num_nodes, num_relations))
+
+    def ingest(self, path, triples=True, remap_ids=False):
+        """ingest (graph.cpp:39-118) of the reference itself."""
+        cnt, V, R = (np.zeros(1, np.uint64) for _ in range(3))
+        p = os.fsencode(path)
+        self._check(self._fn["ingest"](p, int(triples), int(remap_ids), None, 0, _ptr(cnt),
+                                       _ptr(V), _ptr(R)))
+        out = np.zeros((max(int(cnt[0]), 1), 3), np.uint32)
+        self._check(self._fn["ingest"](p, int(triples), int(remap_ids), _ptr(out), int(cnt[0]),
+                                       _ptr(cnt), _ptr(V), _ptr(R)))
+        return out[:int(cnt[0])], int(V[0]), int(R[0])
 
     def read_graph(self, directory):
         """read_graph (graph.cpp:173-192) of the reference itself."""

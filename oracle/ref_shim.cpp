@@ -528,6 +528,26 @@ int ref_bucket_sample_timed(const std::uint32_t* bucket_edges, std::uint64_t m,
   });
 }
 
+// ingest (graph.cpp:39-118) through the reference itself; edges_out holds up
+// to cap records
+int ref_ingest(const char* path, int triples, int remap, std::uint32_t* edges_out,
+               std::uint64_t cap, std::uint64_t* num_edges, std::uint64_t* num_nodes,
+               std::uint64_t* num_relations) {
+  return guarded([&] {
+    IngestOptions o;
+    o.remap_ids = remap != 0;
+    const Graph g = ingest(path, triples ? EdgeFileFormat::kTriples : EdgeFileFormat::kPairs, o);
+    *num_edges = g.edges.size();
+    *num_nodes = g.num_nodes;
+    *num_relations = g.num_relations;
+    for (std::uint64_t i = 0; i < g.edges.size() && i < cap; ++i) {
+      edges_out[3 * i] = g.edges[i].src;
+      edges_out[3 * i + 1] = g.edges[i].rel;
+      edges_out[3 * i + 2] = g.edges[i].dst;
+    }
+  });
+}
+
 // write_graph / read_graph (graph.cpp:152-192) through the reference itself
 int ref_write_graph(const char* dir, const std::uint32_t* edges, std::uint64_t num_edges,
                     std::uint64_t num_nodes, std::uint64_t num_relations) {

@@ -5,10 +5,10 @@ include/legend_b200.h; this package is the thin Python face of that ABI.
 """
 from .legend import (EpochResult, EvalOptions, InvalidArgument, IterationPlan, LogicError,
                      OutOfRange, PinnedArray, RuntimeFailure, ScoreModel, Trainer, TrainOptions, library,
-                     plan_iteration_order, plan_to_json, read_graph, rng_below, sample_negatives,
+                     ingest_tsv, plan_iteration_order, plan_to_json, read_graph, rng_below, sample_negatives,
                      shuffle_permutation, single_state_plan, write_graph)
 
 __all__ = ["EpochResult", "EvalOptions", "InvalidArgument", "IterationPlan", "LogicError",
            "OutOfRange", "PinnedArray", "RuntimeFailure", "ScoreModel", "Trainer", "TrainOptions", "library",
-           "plan_iteration_order", "plan_to_json", "read_graph", "rng_below", "sample_negatives",
+           "ingest_tsv", "plan_iteration_order", "plan_to_json", "read_graph", "rng_below", "sample_negatives",
            "shuffle_permutation", "single_state_plan", "write_graph"]

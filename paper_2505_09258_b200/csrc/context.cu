@@ -98,7 +98,7 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       if (const char* env = std::getenv("LGD_K4")) {
         const long v = std::strtol(env, nullptr, 10);
         c->seg_rows = v != 1;
-        c->k4_ws = v == 3;
+        c->k4_variant = v == 3 ? 1 : (v == 4 ? 2 : 0);
       }
       if (const char* env = std::getenv("LGD_K4_IR1")) c->ir1_rows = std::strtol(env, nullptr, 10) != 0;
       LGD_CUDA(cudaEventCreate(&c->ev_begin));

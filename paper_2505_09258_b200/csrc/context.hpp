@@ -99,7 +99,8 @@ struct lgd_context {
   // K4 v2 (train.cu: segment_rows) over a segment list; LGD_K4=1 selects the
   // chunked pass 1 / pass 2 kernels instead (A/B)
   bool seg_rows = true;
-  bool k4_ws = false;  // LGD_K4=3: the warp-specialised producer / consumer kernel
+  // K4 v2 kernel: 0 segment_heads, 1 warp-specialised (LGD_K4=3), 2 flattened (LGD_K4=4)
+  int k4_variant = 0;
   DevBuf<uint32_t> long_head, long_end, long_chunk_base, long_first, nlong;
   DevBuf<double> rel64;  // FP64 relation rows for K4 (K3 writes them; R <= kRel64Max)
   static constexpr uint64_t kRel64Max = 256;
@@ -403,7 +404,7 @@ struct lgd_context {
     a.rel_key_bits = bits_for(R ? R - 1 : 0);
     a.sm_count = sm_count;
     a.gc = nullptr;
-    a.k4_ws = k4_ws ? 1 : 0;
+    a.k4_ws = k4_variant;
     a.seg_mode = seg_rows ? 2 : 0;  // run_batch switches to the bucket's list
     a.long_head = long_head.get();
     a.long_end = long_end.get();

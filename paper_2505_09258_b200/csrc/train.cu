@@ -1504,6 +1504,111 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ------------------------------- K4 v4: flattened whole-segment updates
+// The warp owns the segments whose heads lie in its 32 sorted items (as
+// segment_heads) but walks them as ONE flat sequence of 16-byte row vectors:
+// at each step lane l takes vector f = 32 s + l of the concatenated rows of
+// the warp's segments (d = 100: 25 vectors per row), so every lane works --
+// no idle lanes at row ends -- and the per-segment bookkeeping is paid once
+// per 32 vectors, not once per row.  A lane sums its vector's contributions
+// sequentially in the reference order (all lanes step through the longest
+// segment of the step, predicated), runs the Adagrad update on its four
+// elements and stores them.  theta / state and the operands are plain
+// coalesced 16-byte loads: consecutive lanes read consecutive vectors of the
+// same row.
+template <int KIND, bool SH, bool IR1, bool R64>
+__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
+    BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+    uint64_t b0, uint64_t b1) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t base = b0 + (((uint64_t)blockIdx.x * kSegThreads + threadIdx.x) >> 5) * 32;
+  if (base >= b1) return;
+  const SegCtx x{a.snap, a.mix, a.ir1, a.w, a.rel_theta, a.rel_keys, a.dim, a.k,
+                 (uint32_t)a.slot_bits, (1u << a.slot_bits) - 1u,
+                 (uint32_t)(a.slot_bits + a.rel_bits), a.rel_bits ? (1u << a.rel_bits) - 1u : 0u,
+                 a.P * a.k, a.sh_G, a.rel64};
+  const uint64_t d = a.dim;
+  const double lr = a.lr, eps = a.eps;
+  const uint64_t i = base + lane, j = i + 32;
+  const uint32_t key = i < b1 ? __ldg(skeys + i) : 0u;
+  const uint32_t key2 = j < b1 ? __ldg(skeys + j) : 0u;
+  const uint32_t prev = (i < b1 && i > b0) ? __ldg(skeys + i - 1) : ~key;
+  const uint32_t prev2 = __shfl_sync(0xffffffffu, key, 31);
+  const uint32_t prev2_l = __shfl_up_sync(0xffffffffu, key2, 1);
+  const bool head = i < b1 && key != prev;
+  const bool term2 = j >= b1 || key2 != (lane ? prev2_l : prev2);
+  const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+  const uint32_t tmask0 = __ballot_sync(0xffffffffu, head || i >= b1);
+  const uint32_t tmask1 = __ballot_sync(0xffffffffu, term2);
+  const uint64_t ends = (uint64_t)tmask0 | ((uint64_t)tmask1 << 32);
+  if (lane == 0 && hmask) atomicAdd(a.counters, (unsigned long long)__popc(hmask));
+  uint32_t my_len = 0;
+  if (head) {
+    const uint64_t above = ends & ~((2ull << lane) - 1);
+    const uint32_t e = above ? (uint32_t)__ffsll((long long)above) - 1 : 64u;
+    my_len = e - lane <= kLongSeg ? e - lane : 0u;
+  }
+  const uint32_t todo = __ballot_sync(0xffffffffu, my_len != 0);
+  if (!todo) return;
+  const int ns = __popc(todo);
+  const uint32_t my_row = my_len ? from_pool(a, key) : 0u;
+  LGD_DCHECK(!my_len || (my_row < a.num_nodes && base + lane + my_len <= b1),
+             "K4 segment outside the batch / table", my_row);
+  // compact: lane c holds the c-th short segment (head position, length, row)
+  const uint32_t src = __fns(todo, 0, lane + 1);
+  const int sl = (int)(src & 31);
+  const uint32_t c_pos = __shfl_sync(0xffffffffu, (uint32_t)lane, sl);
+  const uint32_t c_len = __shfl_sync(0xffffffffu, my_len, sl);
+  const uint32_t c_row = __shfl_sync(0xffffffffu, my_row, sl);
+  const uint32_t w0 = i < b1 ? __ldg(svals + i) : 0u;
+  const uint32_t w1 = j < b1 ? __ldg(svals + j) : 0u;
+  const uint32_t nvec = KIND == 2 ? (uint32_t)(d / 4) : (uint32_t)(d / 4);  // 16-byte vectors per row
+  const uint32_t total = (uint32_t)ns * nvec;
+  // this lane's (segment, vector) at flat index lane, advanced by 32 per step
+  uint32_t seg = 0, q = lane;
+  while (q >= nvec) {
+    q -= nvec;
+    ++seg;
+  }
+#pragma unroll 1
+  for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+    const bool act = f0 + lane < total;
+    const int sg = act ? (int)seg : 0;
+    const uint32_t pos = __shfl_sync(0xffffffffu, c_pos, sg);
+    const uint32_t len = act ? __shfl_sync(0xffffffffu, c_len, sg) : 0u;
+    const uint32_t row = __shfl_sync(0xffffffffu, c_row, sg);
+    const Lanes<KIND, 1> L(act ? (int)q : 0, a.dim);
+    const uint64_t off = (uint64_t)row * d;
+    float th[4], st[4];
+    L.template ldf<false>(a.theta + off, act, th);
+    L.template ldf<false>(a.state + off, act, st);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    uint32_t maxlen = len;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    for (uint32_t t = 0; t < maxlen; ++t) {  // contributions in order; lanes past their end idle
+      const uint32_t o = pos + (t < len ? t : 0u);
+      const uint32_t v0 = __shfl_sync(0xffffffffu, w0, o & 31);
+      const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
+      if (t < len) {
+        ItemRegs<4> it;
+        load_item<KIND, 1, false, SH, IR1>(x, L, o < 32 ? v0 : v1, true, it);
+        add_loaded<KIND, 1, false, SH, IR1, R64>(x, L, it, x.k, acc, th);
+      }
+    }
+    if (act) {
+      adagrad_lanes(L, acc, th, st, lr, eps);
+      L.stf(a.theta + off, th);
+      L.stf(a.state + off, st);
+    }
+    q += 32;
+    while (q >= nvec) {
+      q -= nvec;
+      ++seg;
+    }
+  }
+}
+
 // --------------------------- K4 v3: warp-specialised whole-segment updates
 // The same segments as segment_heads (<= kLongSeg contributions, summed whole
 // in the reference order), split between producer and consumer warps so
@@ -1922,7 +2027,11 @@ void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStr
                                                                       a.seg_batch, a.part_first);
   LGD_LAUNCH_CHECK();
   if (a.side) LGD_CUDA(cudaEventRecord(a.ev_long_done, a.side));
-  if (a.k4_ws) {
+  if (a.k4_ws == 2 && NV == 1) {  // K4 v4: flattened vectors
+    const unsigned grid = (unsigned)ceil_div(ceil_div(b1 - b0, 32), kSegThreads / 32);
+    segment_flat<KIND, SH, IR1, R64><<<grid, kSegThreads, 0, st>>>(a, a.seg_keys, a.seg_vals, b0,
+                                                                   b1);
+  } else if (a.k4_ws == 1) {
     const size_t wsm = ws_bar_bytes() + (size_t)kWsConsumers * kWsDepth * ws_slot_bytes((a.dim + 3) & ~3u);
     static size_t wattr[kMaxDevices];
     if (wsm > wattr[dev]) {

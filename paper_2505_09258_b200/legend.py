@@ -113,6 +113,8 @@ def library():
         "lgd_write_graph": (i32, [C.c_char_p, vp, u64, u64, u64]),
         "lgd_read_graph_meta": (i32, [C.c_char_p, vp, vp, vp]),
         "lgd_read_graph": (i32, [C.c_char_p, vp, u64]),
+        "lgd_ingest_tsv": (i32, [C.c_char_p, i32, i32, i32, vp, vp, vp, vp]),
+        "lgd_free_edges": (None, [vp]),
         "lgd_round_schedule": (i32, [u32, u64, vp, vp, vp, vp]),
         "lgd_train_items": (i32, [vp, u32, vp, u64, vp]),
         "lgd_set_host_edges": (i32, [vp, vp]),
@@ -331,6 +333,21 @@ def write_graph(directory, edges, num_nodes, num_relations=0):
     edges = _u32(edges, 3)
     _check(library().lgd_write_graph(os.fsencode(directory), _p(edges), len(edges), num_nodes,
                                      num_relations))
+
+
+def ingest_tsv(path, triples=True, remap_ids=False, threads=0):
+    """ingest (graph.cpp:39-118) on host threads: (edges [E x 3] u32, num_nodes,
+    num_relations); malformed input raises RuntimeFailure with the line."""
+    ptr = C.c_void_p()
+    E, V, R = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _check(library().lgd_ingest_tsv(os.fsencode(path), int(triples), int(remap_ids), threads,
+                                    C.byref(ptr), C.byref(E), C.byref(V), C.byref(R)))
+    try:
+        buf = (C.c_uint32 * (3 * E.value)).from_address(ptr.value)
+        edges = np.frombuffer(buf, np.uint32).reshape(-1, 3).copy()
+    finally:
+        library().lgd_free_edges(ptr)
+    return edges, V.value, R.value
 
 
 def read_graph(directory):

@@ -3,6 +3,9 @@
 * lgd_write_graph / lgd_read_graph against the reference's own write_graph /
   read_graph (graph.cpp:152-192): files written by either side are read by the
   other, and graph_meta.json is byte-identical.
+* lgd_ingest_tsv against the reference's ingest (graph.cpp:39-118): the same
+  edges, counts and remapped ids, and the same ParseError text with the line
+  number, for files parsed by several host threads.
 * The host restatement of the power-law generator (oracle/graphgen.c, the
   workload of bench.py's reference arm): determinism, counter-based chunking,
   bucket extraction, and its degree distribution.  tests/test_gpu_graph.py
@@ -115,3 +118,71 @@ def test_degree_distribution_is_power_law(oracle):
     # the 100 largest hubs land in many of the 16 partitions
     hubs = np.argsort(deg)[::-1][:100]
     assert len(np.unique(hubs // -(-V // 16))) >= 12
+
+
+def _tsv(rng, n, triples, sparse=False, junk=True):
+    lines = ["# a comment line"]
+    hi = 10**12 if sparse else 5000
+    for i in range(n):
+        cols = [rng.integers(0, hi)] + ([rng.integers(0, 40)] if triples else []) + \
+               [rng.integers(0, hi)]
+        sep = "\t" if i % 3 else "  \t "
+        lines.append(sep.join(str(c) for c in cols) + ("\r" if i % 7 == 0 else ""))
+        if junk and i % 50 == 0:
+            lines += ["", "   ", "#x 1 2"]
+    return "\n".join(lines) + ("\n" if n % 2 else "")
+
+
+@pytest.mark.parametrize("triples", [True, False])
+@pytest.mark.parametrize("remap", [False, True])
+@pytest.mark.parametrize("threads", [1, 5])
+def test_ingest_matches_reference(tmp_path, reference, triples, remap, threads):
+    rng = np.random.default_rng(4)
+    path = tmp_path / "edges.tsv"
+    path.write_text(_tsv(rng, 20000, triples, sparse=remap))
+    want = reference.ingest(path, triples, remap)
+    got = lgd.ingest_tsv(path, triples, remap, threads=threads)
+    assert got[1:] == want[1:]
+    assert np.array_equal(got[0], want[0])
+
+
+@pytest.mark.parametrize("text,msg", [
+    ("1 2 3\n4 5\n", "line 2: expected 3 columns, got 2"),
+    ("1 2 3\n# c\n\n7 x 9\n", "line 4: malformed integer field 'x'"),
+    ("1 2 3\n4 -5 6\n", "line 2: malformed integer field '-5'"),
+    ("# only comments\n\n", "edge file has no edges"),
+])
+def test_ingest_errors_match_reference(tmp_path, reference, text, msg):
+    path = tmp_path / "bad.tsv"
+    path.write_text(text)
+    with pytest.raises(lgd.RuntimeFailure, match=msg):
+        lgd.ingest_tsv(path, True, False, threads=3)
+    with pytest.raises(Exception, match=msg):
+        reference.ingest(path, True, False)
+
+
+def test_ingest_large_file_parallel(tmp_path, reference):
+    rng = np.random.default_rng(9)
+    path = tmp_path / "big.tsv"
+    edges = np.stack([rng.integers(0, 10**6, 400000), rng.integers(0, 100, 400000),
+                      rng.integers(0, 10**6, 400000)], 1)
+    np.savetxt(path, edges, fmt="%d", delimiter="\t")
+    got = lgd.ingest_tsv(path, True, False, threads=8)
+    assert np.array_equal(got[0], edges.astype(np.uint32))
+    assert got[1:] == (int(edges[:, [0, 2]].max()) + 1, int(edges[:, 1].max()) + 1)
+    assert np.array_equal(reference.ingest(path)[0], got[0])
+
+
+def test_ingest_error_line_in_a_later_chunk(tmp_path, reference):
+    rng = np.random.default_rng(10)
+    text = _tsv(rng, 30000, True).split("\n")
+    text[25001] = "1 2"  # deep in the file: another thread's chunk
+    path = tmp_path / "late.tsv"
+    path.write_text("\n".join(text))
+    with pytest.raises(Exception) as ref_err:
+        reference.ingest(path)
+    with pytest.raises(lgd.RuntimeFailure) as err:
+        lgd.ingest_tsv(path, True, False, threads=7)
+    assert str(err.value) == str(ref_err.value).split(": ", 1)[1] or \
+        str(err.value) in str(ref_err.value)
+    assert "line 25002: expected 3 columns, got 2" in str(err.value)
