@@ -940,7 +940,11 @@ __device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const do
     if (!L.ok[v]) continue;
 #pragma unroll
     for (int e = 4 * v; e < 4 * v + 4; ++e)
+#ifdef LGD_ADAGRAD1
+      if (!adagrad_try_fast1(acc[e], th[e], st[e], lr, eps)) slow |= 1u << e;
+#else
       if (!adagrad_try_fast(acc[e], th[e], st[e], lr, eps)) slow |= 1u << e;
+#endif
   }
   if (slow) {
 #pragma unroll
@@ -1555,8 +1559,9 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
   LGD_DCHECK(!my_len || (my_row < a.num_nodes && base + lane + my_len <= b1),
              "K4 segment outside the batch / table", my_row);
   // compact: lane c holds the c-th short segment (head position, length, row)
-  const uint32_t src = __fns(todo, 0, lane + 1);
-  const int sl = (int)(src & 31);
+  uint32_t m = todo;  // lane c: the c-th set bit of todo
+  for (int t = 0; t < lane && m; ++t) m &= m - 1;
+  const int sl = m ? __ffs(m) - 1 : 0;
   const uint32_t c_pos = __shfl_sync(0xffffffffu, (uint32_t)lane, sl);
   const uint32_t c_len = __shfl_sync(0xffffffffu, my_len, sl);
   const uint32_t c_row = __shfl_sync(0xffffffffu, my_row, sl);
@@ -1574,9 +1579,11 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
   for (uint32_t f0 = 0; f0 < total; f0 += 32) {
     const bool act = f0 + lane < total;
     const int sg = act ? (int)seg : 0;
+    // (every lane takes part in each shuffle: none sits under a condition)
     const uint32_t pos = __shfl_sync(0xffffffffu, c_pos, sg);
-    const uint32_t len = act ? __shfl_sync(0xffffffffu, c_len, sg) : 0u;
+    const uint32_t len_s = __shfl_sync(0xffffffffu, c_len, sg);
     const uint32_t row = __shfl_sync(0xffffffffu, c_row, sg);
+    const uint32_t len = act ? len_s : 0u;
     const Lanes<KIND, 1> L(act ? (int)q : 0, a.dim);
     const uint64_t off = (uint64_t)row * d;
     float th[4], st[4];

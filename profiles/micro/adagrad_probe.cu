@@ -12,7 +12,7 @@ __device__ uint64_t mix64(uint64_t x) {
 }
 __device__ double u01(uint64_t& s) { s = mix64(s + 0x9e3779b97f4a7c15ull); return (s >> 11) * 0x1p-53; }
 
-__global__ void probe(uint64_t n, unsigned long long* out) {
+__global__ void probe(uint64_t n, unsigned long long* out, int mode) {
   unsigned long long fast = 0, bad = 0, total = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t s = i * 0x2545F4914F6CDD1Dull + 7;
@@ -27,7 +27,8 @@ __global__ void probe(uint64_t n, unsigned long long* out) {
     const double lr = 0.1, eps = 1e-10;
     float th_e = th, st_e = st, th_f = th, st_f = st;
     lgd::adagrad_exact(g, th_e, st_e, lr, eps);
-    const bool ok = lgd::adagrad_try_fast(g, th_f, st_f, lr, eps);
+    const bool ok = mode ? lgd::adagrad_try_fast1(g, th_f, st_f, lr, eps)
+                         : lgd::adagrad_try_fast(g, th_f, st_f, lr, eps);
     ++total;
     if (ok) {
       ++fast;
@@ -40,7 +41,8 @@ __global__ void probe(uint64_t n, unsigned long long* out) {
 int main(int argc, char** argv) {
   const unsigned long long n = argc > 1 ? strtoull(argv[1], nullptr, 0) : (1ull << 32);
   unsigned long long* d; cudaMalloc(&d, 24); cudaMemset(d, 0, 24);
-  probe<<<148 * 8, 256>>>(n, d);
+  const int mode = argc > 2 ? atoi(argv[2]) : 0;  // 1: the single-Newton-step variant
+  probe<<<148 * 8, 256>>>(n, d, mode);
   unsigned long long h[3]; cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
   printf("%s total %llu fast %llu (%.5f%%) mismatches %llu\n", cudaGetErrorString(cudaGetLastError()),
          h[0], h[1], 100.0 * h[1] / h[0], h[2]);
