@@ -940,9 +940,9 @@ __device__ __forceinline__ void adagrad_lanes(const Lanes<KIND, NV>& L, const do
     if (!L.ok[v]) continue;
 #pragma unroll
     for (int e = 4 * v; e < 4 * v + 4; ++e)
-#ifdef LGD_ADAGRAD1
+#ifndef LGD_ADAGRAD2
       if (!adagrad_try_fast1(acc[e], th[e], st[e], lr, eps)) slow |= 1u << e;
-#else
+#else  // the two-Newton-step certificate (round 1)
       if (!adagrad_try_fast(acc[e], th[e], st[e], lr, eps)) slow |= 1u << e;
 #endif
   }

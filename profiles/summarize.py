@@ -1,12 +1,13 @@
 """Summarise an ncu launch list and full capture into committed JSON.
 
-    python profiles/summarize.py gpurun_out/launches.csv gpurun_out/prof_full.ncu-rep profiles/r01
+    python profiles/summarize.py gpurun_out/launches.csv gpurun_out/prof_full.ncu-rep profiles/r02l [config]
 
 Writes <dir>/launch_shares.json (per-kernel share of the device time of the
 steady-state launches: the setup kernels -- graph generator, partition sort,
 store init -- are excluded), <dir>/ncu_full_summary.json (per-kernel DRAM
-bytes, duration, pipe utilisation, stall reasons) and profiles/ncu_traffic.json
-(DRAM bytes per launch for the bench's roofline `traffic` field).
+bytes, duration, pipe utilisation, stall reasons) and the config's entry of
+profiles/ncu_traffic.json (DRAM bytes per launch for the bench's roofline
+`traffic` field; config defaults to tw).
 """
 import csv
 import json
@@ -21,7 +22,9 @@ SETUP = ("powerlaw", "bucket_keys", "gather3", "init_uniform", "DeviceRadixSortH
 
 def short(name):
     n = name.split("(")[0]
-    for tag in ("score_kernel", "segment_pass1_vec", "segment_pass1", "segment_pass2",
+    for tag in ("score_kernel", "segment_heads", "long_chunks", "long_combine", "long_index",
+                "segment_ws", "segment_flat", "presort_keys", "DeviceSelect",
+                "segment_pass1_vec", "segment_pass1", "segment_pass2",
                 "loss_reduce", "draw_const", "shuffle_draw", "keys_kernel", "head_kernel",
                 "chase_kernel", "final_kernel", "gather_edges", "Onesweep", "Histogram",
                 "ExclusiveSum", "zero_kernel", "init_uniform", "powerlaw", "bucket_keys",
@@ -97,13 +100,14 @@ def to_bytes(s):
 
 def main():
     launches, rep, outdir = sys.argv[1], sys.argv[2], sys.argv[3]
+    config = sys.argv[4] if len(sys.argv) > 4 else "tw"
     os.makedirs(outdir, exist_ok=True)
     if os.path.exists(launches):
         with open(os.path.join(outdir, "launch_shares.json"), "w") as f:
             json.dump(launch_shares(launches), f, indent=1)
     if os.path.exists(rep):
         full = full_summary(rep)
-        with open(os.path.join(outdir, "ncu_full_summary.json"), "w") as f:
+        with open(os.path.join(outdir, f"ncu_full_summary_{config}.json"), "w") as f:
             json.dump(full, f, indent=1)
         traffic = {}
         def node_pass(name):  # segment_pass1_vec<KIND, NV, REL, SH>: REL == 0
@@ -112,18 +116,26 @@ def main():
             args = [x.strip() for x in name.split("<", 1)[1].split(">")[0].split(",")]
             return len(args) < 3 or args[2] in ("0", "(bool)0", "false")
 
-        for cls, tag in (("score", "score_kernel"), ("update", "segment_pass1")):
+        for cls, tag in (("score", "score_kernel"), ("update", "segment_heads")):
             hits = [e for e in full if tag in e["kernel"] and node_pass(e["kernel"])]
+            if not hits and cls == "update":  # the chunked kernels (LGD_K4=1)
+                hits = [e for e in full if "segment_pass1" in e["kernel"] and node_pass(e["kernel"])]
             if hits:
                 b = [to_bytes(e["dram__bytes_read.sum"]) + to_bytes(e["dram__bytes_write.sum"])
                      for e in hits]
                 traffic[cls] = sum(b) / len(b)
-        traffic["source"] = os.path.relpath(os.path.join(outdir, "ncu_full_summary.json"),
-                                            os.path.dirname(os.path.dirname(os.path.abspath(
-                                                __file__))))
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json"),
-                  "w") as f:
-            json.dump(traffic, f, indent=1)
+        traffic["source"] = os.path.relpath(
+            os.path.join(outdir, f"ncu_full_summary_{config}.json"),
+            os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json")
+        try:
+            with open(tpath) as f:
+                allt = json.load(f)
+        except Exception:
+            allt = {}
+        allt[config] = traffic
+        with open(tpath, "w") as f:
+            json.dump(allt, f, indent=1)
     print("ok")
 
 
