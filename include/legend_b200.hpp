@@ -154,12 +154,66 @@ class Trainer {
     return r;
   }
 
+  // ---- multi-GPU partition rounds (rounds.cu; one process per GPU) ----
+  // id: 128 bytes from comm_unique_id() on rank 0, shared with every rank
+  void comm_init(const void* nccl_id, std::uint32_t rank, std::uint32_t world) {
+    check(lgd_comm_init(ctx_, nccl_id, rank, world));
+  }
+  std::uint32_t round_count() {
+    std::uint32_t r = 0;
+    check(lgd_round_count(ctx_, &r));
+    return r;
+  }
+  // one round: this rank's buckets, the next round's NVLink pulls, lock-step relations
+  EpochResult train_round(std::uint32_t epoch, std::uint32_t round, double* handoff_ms = nullptr,
+                          std::uint64_t* handoff_bytes = nullptr) {
+    EpochResult r{};
+    check(lgd_train_round(ctx_, epoch, round, &r, handoff_ms, handoff_bytes));
+    return r;
+  }
+
   lgd_context* handle() const { return ctx_; }
 
  private:
   lgd_context* ctx_ = nullptr;
   ScoreModel model_;
 };
+
+inline std::vector<unsigned char> comm_unique_id() {
+  std::vector<unsigned char> id(128);
+  check(lgd_comm_unique_id(id.data()));
+  return id;
+}
+
+// ingest (graph.cpp:39-118): a TSV edge list on host threads.
+struct IngestedGraph {
+  std::vector<std::uint32_t> edges;  // 3 per edge: src, rel, dst
+  std::uint64_t num_nodes = 0, num_relations = 0;
+};
+inline IngestedGraph ingest_tsv(const std::string& path, bool triples, bool remap_ids = false,
+                                int threads = 0) {
+  std::uint32_t* e = nullptr;
+  std::uint64_t n = 0;
+  IngestedGraph g;
+  check(lgd_ingest_tsv(path.c_str(), triples ? 1 : 0, remap_ids ? 1 : 0, threads, &e, &n,
+                       &g.num_nodes, &g.num_relations));
+  g.edges.assign(e, e + 3 * n);
+  lgd_free_edges(e);
+  return g;
+}
+// write_graph / read_graph (graph.cpp:152-192): edges.bin + graph_meta.json.
+inline void write_graph(const std::string& dir, const std::vector<std::uint32_t>& edges,
+                        std::uint64_t num_nodes, std::uint64_t num_relations) {
+  check(lgd_write_graph(dir.c_str(), edges.data(), edges.size() / 3, num_nodes, num_relations));
+}
+inline IngestedGraph read_graph(const std::string& dir) {
+  IngestedGraph g;
+  std::uint64_t n = 0;
+  check(lgd_read_graph_meta(dir.c_str(), &n, &g.num_nodes, &g.num_relations));
+  g.edges.resize(3 * n);
+  check(lgd_read_graph(dir.c_str(), g.edges.data(), n));
+  return g;
+}
 
 // The reference's Algorithms 1-2 (ordering.hpp:49-54) as flat arrays.
 struct Plan {

@@ -1569,11 +1569,21 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
   const uint32_t w1 = j < b1 ? __ldg(svals + j) : 0u;
   const uint32_t nvec = KIND == 2 ? (uint32_t)(d / 4) : (uint32_t)(d / 4);  // 16-byte vectors per row
   const uint32_t total = (uint32_t)ns * nvec;
-  // this lane's (segment, vector) at flat index lane, advanced by 32 per step
+  // this lane's (segment, vector) at flat index lane, advanced by 32 per step;
+  // the next step's theta / state vectors are loaded while this step sums
   uint32_t seg = 0, q = lane;
   while (q >= nvec) {
     q -= nvec;
     ++seg;
+  }
+  auto row_of = [&](uint32_t sgv) { return __shfl_sync(0xffffffffu, c_row, (int)sgv & 31); };
+  float th[4], st[4];
+  {
+    const bool act0 = lane < total;
+    const uint32_t r0 = row_of(act0 ? seg : 0);
+    const Lanes<KIND, 1> L0(act0 ? (int)q : 0, a.dim);
+    L0.template ldf<false>(a.theta + (uint64_t)r0 * d, act0, th);
+    L0.template ldf<false>(a.state + (uint64_t)r0 * d, act0, st);
   }
 #pragma unroll 1
   for (uint32_t f0 = 0; f0 < total; f0 += 32) {
@@ -1586,9 +1596,20 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
     const uint32_t len = act ? len_s : 0u;
     const Lanes<KIND, 1> L(act ? (int)q : 0, a.dim);
     const uint64_t off = (uint64_t)row * d;
-    float th[4], st[4];
-    L.template ldf<false>(a.theta + off, act, th);
-    L.template ldf<false>(a.state + off, act, st);
+    // the next step's position and rows, in flight during this step
+    uint32_t nseg = seg, nq = q + 32;
+    while (nq >= nvec) {
+      nq -= nvec;
+      ++nseg;
+    }
+    const bool nact = f0 + 32 + lane < total;
+    const uint32_t nrow = row_of(nact ? nseg : 0);
+    float nth[4], nst[4];
+    {
+      const Lanes<KIND, 1> Ln(nact ? (int)nq : 0, a.dim);
+      Ln.template ldf<false>(a.theta + (uint64_t)nrow * d, nact, nth);
+      Ln.template ldf<false>(a.state + (uint64_t)nrow * d, nact, nst);
+    }
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     uint32_t maxlen = len;
 #pragma unroll
@@ -1608,11 +1629,13 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
       L.stf(a.theta + off, th);
       L.stf(a.state + off, st);
     }
-    q += 32;
-    while (q >= nvec) {
-      q -= nvec;
-      ++seg;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      th[e] = nth[e];
+      st[e] = nst[e];
     }
+    seg = nseg;
+    q = nq;
   }
 }
 

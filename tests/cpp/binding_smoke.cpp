@@ -11,6 +11,23 @@ int main(int argc, char** argv) {
   const bool expect_gpu = argc > 1 && argv[1][0] == '1';
   const auto plan = legend_b200::plan_iteration_order(6);
   if (plan.state_offsets.size() != 9) return 2;  // n = 6 has 8 buffer states
+  {  // host-only graph I/O: ingest a TSV, write and read back the reference's graph files
+    const char* tsv = "binding_smoke_edges.tsv";
+    if (FILE* f = std::fopen(tsv, "w")) {
+      std::fputs("# src rel dst\n3 1 4\n1 0 5\n9 2 6\n", f);
+      std::fclose(f);
+    }
+    const auto g = legend_b200::ingest_tsv(tsv, true);
+    std::remove(tsv);
+    if (g.edges.size() != 9 || g.num_nodes != 10 || g.num_relations != 3) return 6;
+    legend_b200::write_graph("binding_smoke_graph", g.edges, g.num_nodes, g.num_relations);
+    const auto back = legend_b200::read_graph("binding_smoke_graph");
+    std::remove("binding_smoke_graph/edges.bin");
+    std::remove("binding_smoke_graph/graph_meta.json");
+    std::remove("binding_smoke_graph");
+    if (back.edges != g.edges || back.num_nodes != 10) return 7;
+    std::printf("graph io ok\n");
+  }
   try {
     legend_b200::Trainer t({legend_b200::ScoreKind::kDistMult, 8}, {0.1, 1e-10, 64, 3, true, 7});
     std::vector<std::uint32_t> edges;
