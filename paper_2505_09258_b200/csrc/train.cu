@@ -56,9 +56,12 @@ constexpr int kSegThreads = SEG_THREADS;
 #define SEG_MINB 4
 #endif
 #ifndef SEG_DEPTH
-#define SEG_DEPTH 3
+#define SEG_DEPTH 2
 #endif
-constexpr int kSegDepth = SEG_DEPTH;  // 3 measured best (2: -2%, 4: -2.5%, 6: -0.3%)  // pieces whose theta / state rows are in flight per warp
+// segments whose rows (and first contribution) are in flight per warp in K4's
+// cp.async ring: segment_heads measured 2 best (0.80 ms per TW batch; 3: 0.81,
+// 4: 0.88 -- the ring's shared memory costs occupancy)
+constexpr int kSegDepth = SEG_DEPTH;
 
 // Developer timeline of K4 warps (build with -DLGD_TRACE; not in the product .so)
 #ifdef LGD_TRACE
