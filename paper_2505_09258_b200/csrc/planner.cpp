@@ -4,6 +4,14 @@
 // its position g in bucket_order (pipeline.cpp:296), so the plan must match
 // the reference's exactly; tests/test_planner.py checks every n in 4..40
 // against the reference library and the byte-stable fig6 fixture.
+//
+// make_loading_order / make_iteration_order are therefore a RESTATEMENT of
+// the reference's plan_loading_order / plan_iteration_order
+// (ordering.cpp:59-346), step for step (the column-owner sweep, the greedy
+// swap choice, the seed prefix, the Kuhn matching for empty windows, and the
+// same error texts): the bucket order is a bit-exact contract, not a design
+// choice.  The multi-GPU round schedule (make_round_schedule) and the n <= 3
+// single-state plan are new.
 #include "planner.hpp"
 
 #include <algorithm>

@@ -1047,17 +1047,12 @@ template <int KIND, int NV, bool SH, bool IR1>
 __device__ __forceinline__ void load_item_staged(const SegCtx& x, const Lanes<KIND, NV>& L,
                                                  uint32_t val, uint32_t op_s, uint32_t w_s,
                                                  ItemRegs<4 * NV>& it) {
-  constexpr int NE = 4 * NV;
   const uint32_t p = val >> x.pshift;
   const uint32_t slot = val & x.smask;
   const bool is_src = slot > x.k;
   LGD_DCHECK(slot <= x.k + 1, "K4 contribution slot", slot);
   it.slot = slot;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    it.sv[e] = 0.f;
-    it.mv[e] = 0.0;
-  }
+  // (each path fills only the operand add_loaded reads on that path)
   if (SH && slot == 1) {
     it.w = 0.0;
     L.lds_s(op_s, it.sv);
