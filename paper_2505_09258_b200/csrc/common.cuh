@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace lgd {
 
@@ -89,6 +90,10 @@ struct DevBuf {
   }
   T* get() const { return ptr; }
   size_t bytes() const { return n * sizeof(T); }
+  void swap(DevBuf& o) {
+    std::swap(ptr, o.ptr);
+    std::swap(n, o.n);
+  }
 };
 
 }  // namespace lgd

@@ -115,8 +115,18 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       LGD_CUDA(cudaEventCreateWithFlags(&c->ev_rel, cudaEventDisableTiming));
       LGD_CUDA(cudaEventCreateWithFlags(&c->ev_long, cudaEventDisableTiming));
       LGD_CUDA(cudaEventCreateWithFlags(&c->ev_long_done, cudaEventDisableTiming));
-      for (auto* e : {&c->copy_done[0], &c->copy_done[1], &c->stage_free[0], &c->stage_free[1]})
+      for (auto* e : {&c->copy_done[0], &c->copy_done[1], &c->stage_free[0], &c->stage_free[1],
+                      &c->ev_prepped[0], &c->ev_prepped[1], &c->ev_consumed[0], &c->ev_consumed[1]})
         LGD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      // the next bucket's prep (opt-in): lowest priority, so the batches on
+      // the training stream (the critical path) are scheduled first
+      if (const char* env = std::getenv("LGD_OVERLAP_PREP"))
+        c->overlap_prep = std::strtol(env, nullptr, 10) != 0;
+      if (c->overlap_prep) {
+        int lo = 0, hi = 0;
+        LGD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LGD_CUDA(cudaStreamCreateWithPriority(&c->prep_stream, cudaStreamNonBlocking, lo));
+      }
       c->pos.reserve(1);
       c->reject.reserve(1);
       LGD_CUDA(cudaMemset(c->reject.get(), 0xff, sizeof(unsigned long long)));

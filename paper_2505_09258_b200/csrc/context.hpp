@@ -114,6 +114,61 @@ struct lgd_context {
     int rel_bits = 0;  // payload layout of the whole bucket
     uint64_t items = 0;
   } bk;
+  // Bucket-prep overlap (LGD_OVERLAP_PREP=1, opt-in): the next bucket's
+  // shuffle / sample / presort / segment list run on prep_stream into a
+  // second set of the per-bucket buffers while the batches of the current
+  // bucket run on `stream`.  The members above always hold the set being
+  // enqueued; swap_sets() exchanges them with `alt`.  Only the outputs are
+  // doubled: the prep-only scratch (H, perm, sh_*, pos, reject) is used by
+  // one prep at a time, all on prep_stream.
+  struct BucketSet {
+    DevBuf<uint32_t> shuffled, negs, keys[2], vals[2];
+    DevBuf<uint32_t> long_head, long_end, long_chunk_base, long_first, nlong;
+    DevBuf<unsigned char> bk_temp, seg_temp;
+    Presorted bk;
+    bool segs = false;
+  } alt;
+  // measured on TW: no gain (plan 87.5M vs 87.7M edges/s serial; rounds
+  // 89.9M vs 90.4M: the prep's sorts run in K4's gaps and stretch K4 by the
+  // SMs they hold), so the serial prep stays the default
+  bool overlap_prep = false;
+  int set_id = 0;  // which of the two physical sets the members hold
+  cudaStream_t prep_stream = nullptr;
+  cudaEvent_t ev_prepped[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  void swap_sets() {
+    shuffled.swap(alt.shuffled);
+    negs.swap(alt.negs);
+    for (int i = 0; i < 2; ++i) {
+      bk_keys[i].swap(alt.keys[i]);
+      bk_vals[i].swap(alt.vals[i]);
+    }
+    long_head.swap(alt.long_head);
+    long_end.swap(alt.long_end);
+    long_chunk_base.swap(alt.long_chunk_base);
+    long_first.swap(alt.long_first);
+    nlong.swap(alt.nlong);
+    bk_temp.swap(alt.bk_temp);
+    seg_temp.swap(alt.seg_temp);
+    std::swap(bk, alt.bk);
+    std::swap(bucket_segs, alt.segs);
+    set_id ^= 1;
+  }
+  // the second set sized like the first (after reserve_for)
+  void reserve_alt() {
+    alt.shuffled.reserve(shuffled.n);
+    alt.negs.reserve(negs.n);
+    for (int i = 0; i < 2; ++i) {
+      alt.keys[i].reserve(bk_keys[i].n);
+      alt.vals[i].reserve(bk_vals[i].n);
+    }
+    alt.long_head.reserve(long_head.n);
+    alt.long_end.reserve(long_end.n);
+    alt.long_chunk_base.reserve(long_chunk_base.n);
+    alt.long_first.reserve(long_first.n);
+    alt.nlong.reserve(nlong.n);
+    alt.bk_temp.reserve(bk_temp.n);
+    alt.seg_temp.reserve(seg_temp.n);
+  }
   DevBuf<uint8_t> chunk_flags;
   DevBuf<uint32_t> span_list;
   DevBuf<unsigned int> span_count;
@@ -175,8 +230,10 @@ struct lgd_context {
     if (ev_rel) cudaEventDestroy(ev_rel);
     if (ev_long) cudaEventDestroy(ev_long);
     if (ev_long_done) cudaEventDestroy(ev_long_done);
-    for (auto e : {copy_done[0], copy_done[1], stage_free[0], stage_free[1]})
+    for (auto e : {copy_done[0], copy_done[1], stage_free[0], stage_free[1], ev_prepped[0],
+                   ev_prepped[1], ev_consumed[0], ev_consumed[1]})
       if (e) cudaEventDestroy(e);
+    if (prep_stream) cudaStreamDestroy(prep_stream);
   }
 
   // Orders every later launch on `stream` (the only stream that writes the
@@ -566,7 +623,7 @@ struct lgd_context {
   // large sort runs near HBM speed where ~50 per-batch sorts of 1.8M items
   // are launch- and lookback-bound.  Off (bk.keys = nullptr) for shared
   // negatives and when the keys would not fit 32 bits.
-  void presort_bucket(const Pool& pool, uint64_t m, cudaEvent_t* bev) {
+  void presort_bucket(const Pool& pool, uint64_t m, cudaEvent_t* bev, cudaStream_t st) {
     bk = Presorted{};
     bucket_segs = false;
     if (presort && !chunk() && m) {
@@ -584,11 +641,11 @@ struct lgd_context {
         }
         const size_t tb = bucket_sort_temp_bytes(items);
         if (bk_temp.bytes() < tb) bk_temp.reserve(tb);
-        launch_bucket_keys(a, m, B, bk_keys[0].get(), bk_vals[0].get(), stream);
+        launch_bucket_keys(a, m, B, bk_keys[0].get(), bk_vals[0].get(), st);
         uint32_t* kk[2] = {bk_keys[0].get(), bk_keys[1].get()};
         uint32_t* vv[2] = {bk_vals[0].get(), bk_vals[1].get()};
         const int sel = sort_bucket(bk_temp.get(), bk_temp.bytes(), kk, vv, items,
-                                    a.node_key_bits + bbits, stream);
+                                    a.node_key_bits + bbits, st);
         bk.keys = kk[sel];
         bk.vals = vv[sel];
         bk.mask = a.node_key_bits >= 32 ? 0xffffffffu : (1u << a.node_key_bits) - 1u;
@@ -597,14 +654,13 @@ struct lgd_context {
         launches += 1 + 2 + (a.node_key_bits + bbits + 7) / 8;
         if (seg_rows) {  // K4 v2: every batch's segments, listed once for the bucket
           ensure_segments(items, nb);
-          launch_long_list(bk.keys, items, uint64_t(B) * (k() + 2), (uint32_t)nb, seg_lists(),
-                           stream);
+          launch_long_list(bk.keys, items, uint64_t(B) * (k() + 2), (uint32_t)nb, seg_lists(), st);
           bucket_segs = true;
           launches += 2;
         }
       }
     }
-    if (bev) LGD_CUDA(cudaEventRecord(bev[3], stream));
+    if (bev) LGD_CUDA(cudaEventRecord(bev[3], st));
   }
 
   // algorithmic bytes of the score phase: the edge record and
@@ -695,31 +751,32 @@ struct lgd_context {
   // Shuffle draws + permutation + gather, then the bucket's m*k negative
   // draws, all from the bucket's stream (pipeline.cpp:296-308).
   void prepare_bucket(const WorkItem& it, uint32_t epoch, const uint32_t* bucket_edges, uint64_t m,
-                      cudaEvent_t* bev) {
+                      cudaEvent_t* bev, cudaStream_t st) {
     StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, it.g)), pos.get(),
                     reject.get()};
-    if (bev) LGD_CUDA(cudaEventRecord(bev[0], stream));
-    LGD_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(uint64_t), stream));
+    if (bev) LGD_CUDA(cudaEventRecord(bev[0], st));
+    LGD_CUDA(cudaMemsetAsync(pos.get(), 0, sizeof(uint64_t), st));
     if (opt.shuffle) {
-      launch_shuffle_draws(slot, m, H.get(), stream);
+      launch_shuffle_draws(slot, m, H.get(), st);
       ShuffleScratch s{sh_keys_in.get(), sh_vals_in.get(), sh_keys_out.get(), sh_vals_out.get(),
                        sh_ptr.get(),     sh_G.get(),       sh_temp.get(),     sh_temp.bytes()};
-      launch_shuffle_permutation(H.get(), m, s, perm.get(), stream);
-      launch_gather_edges(bucket_edges, perm.get(), m, shuffled.get(), stream);
+      launch_shuffle_permutation(H.get(), m, s, perm.get(), st);
+      launch_gather_edges(bucket_edges, perm.get(), m, shuffled.get(), st);
       launches += 2 + 5 + 2 + (bits_for(m) + 7) / 8 + 1;
     } else {
-      launch_gather_edges(bucket_edges, nullptr, m, shuffled.get(), stream);
+      launch_gather_edges(bucket_edges, nullptr, m, shuffled.get(), st);
       launches += 1;
     }
   }
-  void sample_bucket(const WorkItem& it, uint32_t epoch, uint64_t m, cudaEvent_t* bev) {
+  void sample_bucket(const WorkItem& it, uint32_t epoch, uint64_t m, cudaEvent_t* bev,
+                     cudaStream_t st) {
     (void)epoch;
     StreamSlot slot{xo_seed(derive_seed(opt.seed, kTagBucket, epoch, it.g)), pos.get(),
                     reject.get()};
-    if (bev) LGD_CUDA(cudaEventRecord(bev[1], stream));
-    launch_sample_nodes(slot, bucket_negs(m), it.pool, negs.get(), stream);
+    if (bev) LGD_CUDA(cudaEventRecord(bev[1], st));
+    launch_sample_nodes(slot, bucket_negs(m), it.pool, negs.get(), st);
     launches += 2;
-    if (bev) LGD_CUDA(cudaEventRecord(bev[2], stream));
+    if (bev) LGD_CUDA(cudaEventRecord(bev[2], st));
   }
 
   // the largest bucket of the partition plan: scratch is sized for it once,
@@ -838,31 +895,52 @@ struct lgd_context {
       if (i0 < items.size()) issue_copy(i0, 0);
     }
     uint64_t nb = 0, edges_trained = 0, buckets = 0;
-    const uint32_t kk = k();
-    for (size_t idx = 0; idx < items.size(); ++idx) {
-      const WorkItem& it = items[idx];
+    // bucket i's shuffle / sample / presort into the members' buffer set,
+    // on `ps`: prep_stream (overlapped with the previous bucket's batches)
+    // or the training stream itself
+    const bool ovl = overlap_prep && prep_stream;
+    cudaStream_t ps = ovl ? prep_stream : stream;
+    if (ovl) {
+      reserve_alt();
+      // neither set is rewritten before the stream's earlier readers finish
+      LGD_CUDA(cudaEventRecord(ev_consumed[0], stream));
+      LGD_CUDA(cudaEventRecord(ev_consumed[1], stream));
+    }
+    auto prep = [&](size_t i) {
+      const WorkItem& it = items[i];
       uint64_t off;
       const uint64_t m = bucket_size(it, &off);
+      cudaEvent_t* bev = profiling ? prof_ev(prof_slot(2)) : nullptr;
+      const uint32_t* bucket_edges = edges_bucketed.get() + 3 * off;
+      if (ovl) LGD_CUDA(cudaStreamWaitEvent(ps, ev_consumed[set_id], 0));
+      if (host_bucketed) {
+        LGD_CUDA(cudaStreamWaitEvent(ps, copy_done[stage], 0));
+        bucket_edges = staging[stage].get();
+        const size_t in = next_nonempty(i + 1);
+        if (in < items.size()) issue_copy(in, stage ^ 1);
+      }
+      prepare_bucket(it, epoch, bucket_edges, m, bev, ps);
+      if (host_bucketed) {
+        LGD_CUDA(cudaEventRecord(stage_free[stage], ps));
+        stage ^= 1;
+      }
+      sample_bucket(it, epoch, m, bev, ps);
+      presort_bucket(it.pool, m, bev, ps);
+      if (ovl) LGD_CUDA(cudaEventRecord(ev_prepped[set_id], ps));
+    };
+    if (ovl && next_nonempty(0) < items.size()) prep(next_nonempty(0));
+    for (size_t idx = 0; idx < items.size(); ++idx) {
+      const WorkItem& it = items[idx];
+      const uint64_t m = bucket_size(it);
       if (hook) (*hook)(idx, true);
       if (m == 0) {  // pipeline.cpp:291, before the RNG is created
         if (hook) (*hook)(idx, false);
         continue;
       }
-      cudaEvent_t* bev = profiling ? prof_ev(prof_slot(2)) : nullptr;
-      const uint32_t* bucket_edges = edges_bucketed.get() + 3 * off;
-      if (host_bucketed) {
-        LGD_CUDA(cudaStreamWaitEvent(stream, copy_done[stage], 0));
-        bucket_edges = staging[stage].get();
-        const size_t in = next_nonempty(idx + 1);
-        if (in < items.size()) issue_copy(in, stage ^ 1);
-      }
-      prepare_bucket(it, epoch, bucket_edges, m, bev);
-      if (host_bucketed) {
-        LGD_CUDA(cudaEventRecord(stage_free[stage], stream));
-        stage ^= 1;
-      }
-      sample_bucket(it, epoch, m, bev);
-      presort_bucket(it.pool, m, bev);
+      if (ovl)
+        LGD_CUDA(cudaStreamWaitEvent(stream, ev_prepped[set_id], 0));
+      else
+        prep(idx);
       uint64_t done = 0;
       for (uint64_t o = 0, b = 0; o < m && b < batch_limit; o += opt.batch_size, ++b) {
         const uint64_t P = std::min<uint64_t>(opt.batch_size, m - o);
@@ -873,6 +951,14 @@ struct lgd_context {
                                    cudaMemcpyDeviceToDevice, stream));
         ++nb;
         done += P;
+      }
+      if (ovl) {  // the next bucket's prep overlaps these batches
+        LGD_CUDA(cudaEventRecord(ev_consumed[set_id], stream));
+        const size_t in = next_nonempty(idx + 1);
+        if (in < items.size()) {
+          swap_sets();
+          prep(in);
+        }
       }
       edges_trained += done;
       ++buckets;
@@ -952,9 +1038,9 @@ struct lgd_context {
           src = staging[0].get();
           round_h2d += m * 12;
         }
-        prepare_bucket(it, round_epoch, src, m, nullptr);
-        sample_bucket(it, round_epoch, m, nullptr);
-        presort_bucket(it.pool, m, nullptr);
+        prepare_bucket(it, round_epoch, src, m, nullptr, stream);
+        sample_bucket(it, round_epoch, m, nullptr, stream);
+        presort_bucket(it.pool, m, nullptr, stream);
         round_prepared = i;
         round_edges += m;
         ++round_buckets;

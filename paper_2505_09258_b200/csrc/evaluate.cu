@@ -7,9 +7,8 @@
 //   scores      one warp per test edge.  IR1 = combine_src_rel(src, rel) in
 //               FP64 in shared memory; the true destination and the candidate
 //               rows are staged 32 at a time into a per-warp shared-memory
-//               double buffer by cp.async (lane l copies row l in 16-byte
-//               pieces; the next 32 rows in flight while the current ones are
-//               scored), and lane
+//               double buffer by cp.async (coalesced 16-byte copies, the next
+//               32 rows in flight while the current ones are scored), and lane
 //               l scores row l SEQUENTIALLY over the dimension -- the
 //               reference's own FP64 summation order (train.cpp:392-396), so a
 //               near-tie lands on the same side of the pessimistic ">=" rule.
@@ -105,18 +104,6 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
       float* buf = rows + (c & 1) * 32 * rs;
       const uint32_t q0 = 32 * c;
       const uint32_t my_id = q0 + lane < nrows ? row_id(q0 + lane) : 0;
-      if (vec) {  // lane l copies row l: one 16-byte cp.async per vector, no shuffles
-        if (q0 + lane < nrows) {
-          const float* src = theta + (size_t)my_id * d;
-          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + lane * rs);
-          for (uint32_t v = 0; v < nv; ++v)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * v),
-                         "l"(src + 4 * v)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        return;
-      }
       for (int q = 0; q < 32; ++q) {
         const uint32_t id = __shfl_sync(0xffffffffu, my_id, q);
         if (q0 + q >= nrows) break;

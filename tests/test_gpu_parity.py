@@ -544,3 +544,46 @@ def test_k4_ir1_rows_equal_snapshot_recombination(kind, monkeypatch):
     assert ra.loss_sum == rb.loss_sum and ra.unique_nodes == rb.unique_nodes
     assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
     assert np.array_equal(rela[0], relb[0]) and np.array_equal(rela[1], relb[1])
+
+
+# ------------------------------------ next-bucket prep on its own stream
+@pytest.mark.parametrize("kind,host,shared", [("distmult", False, 0), ("complex", True, 0),
+                                               ("dot", False, 0), ("transe", True, 0),
+                                               ("distmult", False, 50)])
+def test_overlapped_bucket_prep_matches_serial(kind, host, shared, monkeypatch):
+    """LGD_OVERLAP_PREP=1 (opt-in): the next bucket's shuffle, sample,
+    presort and segment list run on a low-priority stream into the second
+    buffer set while the current bucket's batches train.  Two epochs, device
+    or host-streamed edges, exact or shared negatives: losses, counts and
+    tables equal the serial path (LGD_OVERLAP_PREP=0) bit for bit."""
+    rng = np.random.default_rng(17)
+    V, R, d, Ecnt, n = 3000, 5, 16, 60000, 4
+    edges = _hub_graph(rng, V, R, Ecnt)
+    R = R if kind != "dot" else 0
+    if not R:
+        edges[:, 1] = 0xFFFFFFFF
+    runs = []
+    for ovl in ("1", "0"):
+        monkeypatch.setenv("LGD_OVERLAP_PREP", ovl)
+        opts = lgd.TrainOptions(batch_size=900, negatives=8, seed=3, shared_chunk=shared)
+        t = lgd.Trainer(lgd.ScoreModel(kind, d), opts)
+        t.set_graph(edges, V, R)
+        t.make_partition_plan(n)
+        t.init_store(5)
+        pinned = None
+        if host:
+            pinned = lgd.PinnedArray((t.num_edges, 3), np.uint32)
+            t.bucketed_edges(pinned.array)
+            t.set_host_edges(pinned.array)
+        res = [t.run_epoch(e) for e in range(2)]
+        if host:
+            t.set_host_edges(None)
+            pinned.free()
+        runs.append(([(r.loss_sum, r.batches, r.unique_nodes, r.unique_rels) for r in res],
+                     t.tables(), t.get_relations() if R else None))
+        t.close()
+    (la, (Ea, Sa), rela), (lb, (Eb, Sb), relb) = runs
+    assert la == lb
+    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    if R:
+        assert np.array_equal(rela[0], relb[0]) and np.array_equal(rela[1], relb[1])
