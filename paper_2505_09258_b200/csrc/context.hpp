@@ -88,7 +88,7 @@ struct lgd_context {
   DevBuf<double> w, mix, ir1, loss, part_first, part_last;
   DevBuf<float> snap;
   // shared-negative chunks (shared.cu)
-  DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowmax, sn_rowinv, sn_G;
+  DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowc, sn_G;
   DevBuf<double> sn_pos;
   DevBuf<uint32_t> node_keys, node_vals, rel_keys, iota, skeys, svals;
   // bucket-level presort (presort_bucket): keys / payloads and their
@@ -300,8 +300,7 @@ struct lgd_context {
       sn_AT.reserve(rows * sh.dpad);
       sn_B.reserve(sh.nch * sh.kpad * sh.dpad);
       sn_BT.reserve(sh.nch * sh.kpad * sh.dpad);
-      sn_rowmax.reserve(rows);
-      sn_rowinv.reserve(rows);
+      sn_rowc.reserve(rows);
       sn_G.reserve(sh.nch * sh.kpad * dim);
       sn_pos.reserve(P);
     } else {
@@ -502,8 +501,7 @@ struct lgd_context {
       a.sh_B = sn_B.get();
       a.sh_AT = sn_AT.get();
       a.sh_BT = sn_BT.get();
-      a.sh_rowmax = sn_rowmax.get();
-      a.sh_rowinv = sn_rowinv.get();
+      a.sh_rowc = sn_rowc.get();
       a.sh_pos = sn_pos.get();
       a.sh_G = sn_G.get();
     }

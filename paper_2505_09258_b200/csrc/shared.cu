@@ -365,16 +365,17 @@ constexpr int kThreadsSG = (kWarps + 1) * 32;  // + the control warp
 
 // Developer timeline of one CTA (build with -DLGD_TRACE; not in the product .so)
 #ifdef LGD_TRACE
-__device__ unsigned long long g_trace[2][4096];
-#define SG_TRACE(slot)                                                                 \
+// [kernel: SG1, SG2, SG3][control warp, epilogue warp 1][slot]
+__device__ unsigned long long g_trace[3][2][4096];
+#define SG_TRACE(kid, slot)                                                            \
   do {                                                                                 \
     if (blockIdx.x == 64 && (threadIdx.x == kWarps * 32 || threadIdx.x == 32) &&       \
         (slot) < 4096)                                                                 \
-      g_trace[threadIdx.x == 32 ? 1 : 0][(slot)] = clock64();                          \
+      g_trace[kid][threadIdx.x == 32 ? 1 : 0][(slot)] = clock64();                     \
   } while (0)
 #else
-#define SG_TRACE(slot) \
-  do {                 \
+#define SG_TRACE(kid, slot) \
+  do {                      \
   } while (0)
 #endif
 
@@ -450,14 +451,19 @@ __device__ __forceinline__ float tf32_pos(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 constexpr float kLog2e = 1.4426950408889634f;
-// softmax weights of 32 scores, branch-free: w = 2^(s log2e - m log2e) / Z,
-// zero where !keep (bit c of keep)
-__device__ __forceinline__ void weights32(const float* v, float ml2, float zinv, uint32_t keep,
-                                          float* w) {
+// softmax weights of 32 scores, branch-free: w = 2^(s log2e - c) with the
+// row's c = M log2e + log2 Z (= 2^(s log2e - M log2e) / Z, one MUFU op and no
+// multiply), zero where !keep (bit c of keep)
+__device__ __forceinline__ void weights32(const float* v, float rc, uint32_t keep, float* w) {
+  if (keep == 0xffffffffu) {
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const float e = ex2(__fmaf_rn(v[c], kLog2e, -ml2)) * zinv;
-    w[c] = (keep >> c) & 1u ? tf32_pos(e) : 0.f;
+    for (int c = 0; c < 32; ++c) w[c] = tf32_pos(ex2(__fmaf_rn(v[c], kLog2e, -rc)));
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const float e = ex2(__fmaf_rn(v[c], kLog2e, -rc));
+      w[c] = (keep >> c) & 1u ? tf32_pos(e) : 0.f;
+    }
   }
 }
 __device__ __forceinline__ uint32_t keep_mask(uint32_t j0, uint32_t limit) {
@@ -499,8 +505,9 @@ __device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint
   tc_fence_after();
 }
 
-// SG1: per tile, S = IR1 N^T in 64-negative blocks; online max / sum of exp
-// per row -> M_p, 1/Z_p and loss_p = -(pos_p - (M_p + log Z_p)) (train.cpp:274).
+// SG1: per tile, S = IR1 N^T in 128-negative blocks; online max / sum of exp
+// per row -> c_p = M_p log2e + log2 Z_p (the weights' offset) and
+// loss_p = -(pos_p - (M_p + log Z_p)) (train.cpp:274).
 __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t dp = a.dpad, k = a.k, kp = a.kpad;
@@ -515,6 +522,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
   sg_setup(&tbase_s, 512, bars, 7, counts);  // S buffers [0, 256), IR1 tile [256, 256 + dpad)
+  SG_TRACE(0, 4090);
   const uint32_t tbase = tbase_s;
   const uint32_t nblk = kp / kStatBlk;
   const int q = warp & 3, hf = warp >> 2;
@@ -541,21 +549,29 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
       bar_expect(ld_a, tile_bytes);
       bulk_load(sA, gA, tile_bytes, ld_a);
       for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_n(b);
+      SG_TRACE(0, 4000);
       bar_wait(ld_a, 0);
+      SG_TRACE(0, 4001);
       tc_fence_after();
       tile_to_tmem(tbase + 256, saddr(sA), dp);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
+        SG_TRACE(0, b * 8 + 0);
         if (b + 1 < nblk) issue_s(b + 1);
+        SG_TRACE(0, b * 8 + 1);
         bar_wait(mma_s + (b & 1), (b >> 1) & 1);
+        SG_TRACE(0, b * 8 + 2);
         if (b + 2 < nblk) load_n(b + 2);
       }
     }
   } else {  // epilogue
     // each warp half covers 64 of a block's 128 columns
     const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + hf * (kStatBlk / 2);
+    SG_TRACE(0, 4000);
     for (uint32_t nb = 0; nb < nblk; ++nb) {
+      SG_TRACE(0, nb * 8 + 0);
       bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
+      SG_TRACE(0, nb * 8 + 1);
       tc_fence_after();
       float v[64];
       tmem_ld32(lane_addr + (nb & 1) * kStatBlk, v);
@@ -565,22 +581,43 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
       if (lane == 0) bar_arrive(epi + (nb & 1));
       const uint32_t j0 = nb * kStatBlk + hf * (kStatBlk / 2);
       const uint32_t keep0 = keep_mask(j0, k), keep1 = keep_mask(j0 + 32, k);
-      float bm = -INFINITY;
+      float zs = 0.f, mn;
+      if ((keep0 & keep1) == 0xffffffffu) {  // every column a negative: no masks
+        float b0 = v[0], b1 = v[1];
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
-        bm = fmaxf(bm, kc ? v[c] : -INFINITY);
-      }
-      const float mn = fmaxf(m, bm);
-      const float ml2 = mn * kLog2e;
-      float zs = 0.f;
+        for (int c = 2; c < 64; c += 2) {
+          b0 = fmaxf(b0, v[c]);
+          b1 = fmaxf(b1, v[c + 1]);
+        }
+        mn = fmaxf(m, fmaxf(b0, b1));
+        const float ml2 = mn * kLog2e;
+        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;  // four chains: MUFU latency overlaps
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
-        zs += kc ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+        for (int c = 0; c < 64; c += 4) {
+          z0 += ex2(__fmaf_rn(v[c], kLog2e, -ml2));
+          z1 += ex2(__fmaf_rn(v[c + 1], kLog2e, -ml2));
+          z2 += ex2(__fmaf_rn(v[c + 2], kLog2e, -ml2));
+          z3 += ex2(__fmaf_rn(v[c + 3], kLog2e, -ml2));
+        }
+        zs = (z0 + z1) + (z2 + z3);
+      } else {
+        float bm = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
+          bm = fmaxf(bm, kc ? v[c] : -INFINITY);
+        }
+        mn = fmaxf(m, bm);
+        const float ml2 = mn * kLog2e;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
+          zs += kc ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+        }
       }
       z = (m == -INFINITY ? 0.f : z * ex2((m - mn) * kLog2e)) + zs;
       m = mn;
+      SG_TRACE(0, nb * 8 + 2);
     }
     if (hf == 1) {
       red_m[row] = m;
@@ -594,13 +631,14 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
     const float Z = (m == -INFINITY ? 0.f : z * ex2((m - M) * kLog2e)) +
                     (m1 == -INFINITY ? 0.f : z1 * ex2((m1 - M) * kLog2e));
     const uint64_t tr = g.row0 + row;
-    a.sh_rowmax[tr] = M;
-    a.sh_rowinv[tr] = 1.f / Z;
+    a.sh_rowc[tr] = (float)((double)M * (double)kLog2e + log2((double)Z));
     const uint64_t p = g.c * a.chunk + (tr - g.c * (uint64_t)a.tpc * 128);
     a.loss[p] = -(a.sh_pos[p] - ((double)M + log((double)Z)));
   }
+  SG_TRACE(0, 4010);
   tc_fence_before();
   __syncthreads();
+  SG_TRACE(0, 4091);
   if (warp == 0) tmem_free(tbase, 512);
 }
 
@@ -628,11 +666,18 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const TileGeom g = tile_geom(a, blockIdx.x);
   sg_setup(&tbase_s, tcols, bars, 10, counts);
+  SG_TRACE(1, 4090);
   const uint32_t tbase = tbase_s;
   const uint32_t nblk = kp / kMixBlk;
   const int q = warp & 3, hf = warp >> 2;
   const uint32_t row = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
+  // first positive of the tile; lane i < 16 of epilogue warp w: the dst id of
+  // tile row w + 8 i (the mix tail's rows), fetched now, used at the end
+  const uint64_t tile_p0 = g.c * a.chunk + (g.row0 - g.c * (uint64_t)a.tpc * 128);
+  uint32_t dst_id = 0;
+  if (warp < kWarps && lane < 128 / kWarps && warp + kWarps * lane < g.valid)
+    dst_id = a.edges[3 * (tile_p0 + warp + kWarps * lane) + 2];
   if (warp == kWarps) {  // control
     if (lane == 0) {
       const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
@@ -664,14 +709,14 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       bar_wait(ld_a, 0);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
-        SG_TRACE(b * 8 + 0);
+        SG_TRACE(1, b * 8 + 0);
         if (nbuf == 2 && b + 1 < nblk) issue_s(b + 1);
-        SG_TRACE(b * 8 + 1);
+        SG_TRACE(1, b * 8 + 1);
         bar_wait(mma_s + (b & 1), (b >> 1) & 1);
         if (b + nbuf < nblk) load_n(b + nbuf);  // S(b) is done with its buffer
         if (nbuf == 1 && b + 1 < nblk) issue_s(b + 1);
         bar_wait(wrdy, b & 1);  // the epilogue wrote W(b)
-        SG_TRACE(b * 8 + 2);
+        SG_TRACE(1, b * 8 + 2);
         bar_wait(ld_t, b & 1);
         tc_fence_after();
         // mix += W . N^T over the block's 128 negatives (two N^T sub-tiles)
@@ -681,50 +726,87 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
                       smem_desc(saddr(sT) + (ks >> 3) * sub_bytes + (ks & 7) * 256, 128, 16 * 128),
                       id, (b | ks) != 0);
         mma_commit(mma_w);
-        SG_TRACE(b * 8 + 3);
+        SG_TRACE(1, b * 8 + 3);
         bar_wait(mma_w, b & 1);
-        SG_TRACE(b * 8 + 4);
+        SG_TRACE(1, b * 8 + 4);
         if (b + 1 < nblk) load_t(b + 1);
       }
     }
   } else {  // epilogue: warp half hf covers 64 of a block's 128 columns
     const bool valid = row < g.valid;
-    const float rm2 = valid ? a.sh_rowmax[g.row0 + row] * kLog2e : 0.f;
-    const float ri = valid ? a.sh_rowinv[g.row0 + row] : 0.f;
+    const float rc = valid ? a.sh_rowc[g.row0 + row] : 0.f;
     for (uint32_t nb = 0; nb < nblk; ++nb) {
-      SG_TRACE(nb * 8 + 0);
+      SG_TRACE(1, nb * 8 + 0);
       bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
       tc_fence_after();
-      SG_TRACE(nb * 8 + 1);
+      SG_TRACE(1, nb * 8 + 1);
       const uint32_t scol0 = 128 + (nb & 1) * kMixBlk + hf * 64;
       float v[32], w0[32], w1[32];
       const uint32_t j0 = nb * kMixBlk + hf * 64;
       tmem_ld32(lane_addr + scol0, v);
-      weights32(v, rm2, ri, valid ? keep_mask(j0, k) : 0u, w0);
+      weights32(v, rc, valid ? keep_mask(j0, k) : 0u, w0);
       tmem_ld32(lane_addr + scol0 + 32, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(epi + (nb & 1));
-      weights32(v, rm2, ri, valid ? keep_mask(j0 + 32, k) : 0u, w1);
-      SG_TRACE(nb * 8 + 2);
+      weights32(v, rc, valid ? keep_mask(j0 + 32, k) : 0u, w1);
+      SG_TRACE(1, nb * 8 + 2);
       if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W free again
       tc_fence_after();
-      SG_TRACE(nb * 8 + 3);
+      SG_TRACE(1, nb * 8 + 3);
       tmem_st32(lane_addr + 384 + hf * 64, w0);
       tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(wrdy);
-      SG_TRACE(nb * 8 + 4);
+      SG_TRACE(1, nb * 8 + 4);
     }
   }
+  // the tile's dst rows (mix = sum_j w_j n_j - dst, train.cpp:306-323) go to
+  // shared memory by cp.async while the last mix MMA drains: the N blocks are
+  // free once the last S MMA is done (every epilogue warp has seen it).  Warp
+  // w owns rows w, w + 8, ... (ids fetched at the kernel's start).  (Loads
+  // into registers here were consumed -- converted -- one by one, each
+  // waiting its full latency: half of SG2's time.)
+  constexpr int kRowsPerWarp = 128 / kWarps;
+  const uint32_t dst_s = saddr(sN) + 512;  // past the tail tile's overhang into sN
+  auto stage_dst = [&]() {
+    if (warp >= kWarps) return;
+#pragma unroll 4
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const uint32_t r = warp + kWarps * i;
+      const uint32_t id = __shfl_sync(0xffffffffu, dst_id, i);
+      if (r >= g.valid) continue;
+      const float* src = a.theta + (size_t)id * d;
+      if ((d & 3) == 0) {
+        for (uint32_t c = lane; c < d / 4; c += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_s + (r * d + 4 * c) * 4),
+                       "l"(src + 4 * c)
+                       : "memory");
+      } else {
+        for (uint32_t e = lane; e < d; e += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_s + (r * d + e) * 4),
+                       "l"(src + e)
+                       : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // with one N buffer the rows reach into the N^T block the last mix MMA reads
+  if (nbuf == 2) stage_dst();
+  SG_TRACE(1, 4001);
   __syncthreads();
+  SG_TRACE(1, 4002);
   bar_wait(mma_w, (nblk - 1) & 1);
+  SG_TRACE(1, 4003);
+  if (nbuf != 2) stage_dst();
   tc_fence_after();
-  float* out = reinterpret_cast<float*>(sA);  // the IR1 tile is free now
-  const uint32_t ts = dp + 4;
-  if (warp < kWarps) {  // TMEM -> shared tile
+  // mix accumulator -> shared tile (the IR1 tile, overhanging into the free N
+  // blocks by dpad floats); odd row stride: lanes (rows) hit distinct banks
+  float* out = reinterpret_cast<float*>(sA);
+  const uint32_t ts = dp + 1;
+  if (warp < kWarps) {
     const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
     for (uint32_t cc = c0; cc < c1; cc += 16) {
       float v[16];
@@ -733,41 +815,23 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       for (int e = 0; e < 16; ++e) out[row * ts + cc + e] = v[e];
     }
   }
+  SG_TRACE(1, 4004);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   tc_fence_before();
   __syncthreads();
-  if (warp < kWarps) {
-    // mix = sum_j w_j n_j - dst (train.cpp:306-323), coalesced; warp w writes
-    // rows w, w + 8, ...: dst ids lane-parallel, four rows' dst in flight
-    const uint64_t pbase = g.c * a.chunk + (g.row0 - g.c * (uint64_t)a.tpc * 128);
-    uint32_t myid = 0;
-    if (lane < 128 / kWarps && warp + kWarps * lane < g.valid)
-      myid = a.edges[3 * (pbase + warp + kWarps * lane) + 2];
-    for (uint32_t rb = 0; rb < 128 / kWarps; rb += 4) {
-      float dv[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t r = warp + kWarps * (rb + i);
-        const uint32_t id = __shfl_sync(0xffffffffu, myid, rb + i);
-#pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-          const uint32_t e = lane + 32 * e4;
-          dv[i][e4] = (r < g.valid && e < d) ? __ldg(a.theta + (size_t)id * d + e) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t r = warp + kWarps * (rb + i);
-        if (r >= g.valid) continue;
-        double* mx = a.mix + (pbase + r) * d;
-#pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-          const uint32_t e = lane + 32 * e4;
-          if (e < d) mx[e] = (double)out[r * ts + e] - (double)dv[i][e4];
-        }
-      }
+  SG_TRACE(1, 4005);
+  if (warp < kWarps) {  // coalesced FP64 rows
+    const float* dsts = reinterpret_cast<const float*>(sN + 512);
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const uint32_t r = warp + kWarps * i;
+      if (r >= g.valid) break;
+      double* mx = a.mix + (tile_p0 + r) * d;
+      for (uint32_t e = lane; e < d; e += 32)
+        mx[e] = (double)out[r * ts + e] - (double)dsts[r * d + e];
     }
   }
   __syncthreads();
+  SG_TRACE(1, 4091);
   if (warp == 0) tmem_free(tbase, tcols);
 }
 
@@ -803,6 +867,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   const uint32_t nsl = (uint32_t)((chunk_rows + kGradSlice - 1) / kGradSlice);
   const uint64_t crow0 = c * (uint64_t)a.tpc * 128;
   sg_setup(&tbase_s, tcols, bars, 10, counts);
+  SG_TRACE(2, 4090);
   const uint32_t tbase = tbase_s;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
   if (warp == kWarps) {  // control
@@ -835,13 +900,19 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       bar_wait(ld_n, 0);
       issue_s(0);
       const uint32_t id = instr_desc(128, dp, false, false);
+      SG_TRACE(2, 4000);
       for (uint32_t s = 0; s < nsl; ++s) {
+        SG_TRACE(2, s * 8 + 0);
         if (nbuf == 2 && s + 1 < nsl) issue_s(s + 1);
+        SG_TRACE(2, s * 8 + 1);
         bar_wait(mma_s + (s & 1), (s >> 1) & 1);
+        SG_TRACE(2, s * 8 + 2);
         if (s + nbuf < nsl) load_a(s + nbuf);
         if (nbuf == 1 && s + 1 < nsl) issue_s(s + 1);
         bar_wait(wrdy, s & 1);
+        SG_TRACE(2, s * 8 + 3);
         bar_wait(ld_t, s & 1);
+        SG_TRACE(2, s * 8 + 4);
         tc_fence_after();
         // G += W^T . IR1 over the slice's 128 positives (two IR1^T sub-tiles)
         for (uint32_t ks = 0; ks < kGradSlice / 8; ++ks)
@@ -850,31 +921,40 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
                       id, (s | ks) != 0);
         mma_commit(mma_w);
         bar_wait(mma_w, s & 1);
+        SG_TRACE(2, s * 8 + 5);
         if (s + 1 < nsl) load_t(s + 1);
       }
     }
   } else {  // epilogue: row = negative, warp half hf covers 64 of the slice's positives
     const bool nvalid = n0 + row < k;
+    // the offsets c of this half's 64 positives of slice s: lane i holds
+    // positives i and 32 + i; loaded one slice ahead (their latency overlaps
+    // the wait for the slice's MMA)
+    auto load_c = [&](uint32_t s, float& c0, float& c1) {
+      const uint64_t pq0 = (uint64_t)s * kGradSlice + hf * 64 + lane, pq1 = pq0 + 32;
+      c0 = pq0 < chunk_rows ? a.sh_rowc[crow0 + pq0] : 0.f;
+      c1 = pq1 < chunk_rows ? a.sh_rowc[crow0 + pq1] : 0.f;
+    };
+    float cn0, cn1;
+    load_c(0, cn0, cn1);
     for (uint32_t s = 0; s < nsl; ++s) {
-      // statistics of this half's 64 positives: lane i holds positives i and 32 + i
       const uint64_t pq0 = (uint64_t)s * kGradSlice + hf * 64 + lane, pq1 = pq0 + 32;
       const bool pv0 = pq0 < chunk_rows, pv1 = pq1 < chunk_rows;
-      const float m0 = pv0 ? a.sh_rowmax[crow0 + pq0] * kLog2e : 0.f;
-      const float i0 = pv0 ? a.sh_rowinv[crow0 + pq0] : 0.f;
-      const float m1 = pv1 ? a.sh_rowmax[crow0 + pq1] * kLog2e : 0.f;
-      const float i1 = pv1 ? a.sh_rowinv[crow0 + pq1] : 0.f;
+      const float c0 = cn0, c1 = cn1;
+      if (s + 1 < nsl) load_c(s + 1, cn0, cn1);
       const uint32_t pm0 = __ballot_sync(0xffffffffu, pv0);  // every lane: no divergent vote
       const uint32_t pm1 = __ballot_sync(0xffffffffu, pv1);
       const uint32_t keep0 = nvalid ? pm0 : 0u, keep1 = nvalid ? pm1 : 0u;
+      SG_TRACE(2, s * 8 + 0);
       bar_wait(mma_s + (s & 1), (s >> 1) & 1);
+      SG_TRACE(2, s * 8 + 1);
       tc_fence_after();
       const uint32_t scol0 = 128 + (s & 1) * kGradSlice + hf * 64;
       float v[32], w0[32], w1[32];
       tmem_ld32(lane_addr + scol0, v);
 #pragma unroll
       for (int cc = 0; cc < 32; ++cc) {
-        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, m0, cc))) *
-                        __shfl_sync(0xffffffffu, i0, cc);
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, c0, cc)));
         w0[cc] = (keep0 >> cc) & 1u ? tf32_pos(e) : 0.f;
       }
       tmem_ld32(lane_addr + scol0 + 32, v);
@@ -883,11 +963,12 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       if (lane == 0) bar_arrive(epi + (s & 1));
 #pragma unroll
       for (int cc = 0; cc < 32; ++cc) {
-        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, m1, cc))) *
-                        __shfl_sync(0xffffffffu, i1, cc);
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, c1, cc)));
         w1[cc] = (keep1 >> cc) & 1u ? tf32_pos(e) : 0.f;
       }
+      SG_TRACE(2, s * 8 + 2);
       if (s >= 1) bar_wait(mma_w, (s - 1) & 1);  // W^T free again
+      SG_TRACE(2, s * 8 + 3);
       tc_fence_after();
       tmem_st32(lane_addr + 384 + hf * 64, w0);
       tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
@@ -895,13 +976,16 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(wrdy);
+      SG_TRACE(2, s * 8 + 4);
     }
   }
   __syncthreads();
   bar_wait(mma_w, (nsl - 1) & 1);
   tc_fence_after();
-  float* out = reinterpret_cast<float*>(sN);  // the negative block is free now
-  const uint32_t ts = dp + 4;
+  // the negative block (and the IR1 tiles after it) is free now; odd row
+  // stride: lanes (rows) hit distinct banks
+  float* out = reinterpret_cast<float*>(sN);
+  const uint32_t ts = dp + 1;
   if (warp < kWarps) {
     const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
     for (uint32_t cc = c0; cc < c1; cc += 16) {
@@ -921,6 +1005,7 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
     }
   }
   __syncthreads();
+  SG_TRACE(2, 4091);
   if (warp == 0) tmem_free(tbase, tcols);
 }
 

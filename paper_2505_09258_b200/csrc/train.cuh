@@ -112,8 +112,8 @@ struct BatchArgs {
   float* sh_AT;               // IR1^T per 64-positive slice (dpad x 64), core-matrix layout
   float* sh_B;                // negative rows, core-matrix layout (nch x kpad x dpad)
   float* sh_BT;               // N^T per 64-negative block (dpad x 64)
-  float* sh_rowmax;           // per padded tile row: max score, 1 / sum exp
-  float* sh_rowinv;
+  float* sh_rowc;             // per padded tile row: log2 of the softmax denominator,
+                              // M log2e + log2 Z (weight = 2^(s log2e - c))
   double* sh_pos;             // P positive scores (FP64)
   float* sh_G;                // nch x kpad x dim: gradient of every shared negative
   // relation pass on a side stream (typed models, updating batches): it needs
