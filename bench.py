@@ -575,7 +575,7 @@ def main():
         sc = stats["score"]
         bf16, _ = peaks_tensor()
         flops = 6.0 * res.edges_trained * args.negatives * cfg["dim"]  # 6 P k d
-        tensor = {"bound": "tensor", "kernel": "score phase: prep + gather + SG1/SG2/SG3 "
+        tensor = {"bound": "tensor", "kernel": "score phase: prep + gather + SG2/SG3 "
                   "(tcgen05.mma kind::tf32)", "achieved": flops / (sc["total_ms"] / 1e3) / 1e12,
                   "peak": bf16 / 2, "unit": "TFLOP/s",
                   "frac": flops / (sc["total_ms"] / 1e3) / 1e12 / (bf16 / 2),

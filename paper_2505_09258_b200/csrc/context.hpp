@@ -88,7 +88,7 @@ struct lgd_context {
   DevBuf<double> w, mix, ir1, loss, part_first, part_last;
   DevBuf<float> snap;
   // shared-negative chunks (shared.cu)
-  DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_rowc, sn_G;
+  DevBuf<float> sn_A, sn_AT, sn_B, sn_BT, sn_D, sn_rowc, sn_G;
   DevBuf<double> sn_pos;
   DevBuf<uint32_t> node_keys, node_vals, rel_keys, iota, skeys, svals;
   // bucket-level presort (presort_bucket): keys / payloads and their
@@ -298,6 +298,7 @@ struct lgd_context {
       const uint64_t rows = sh.nch * sh.tpc * 128;
       sn_A.reserve(rows * sh.dpad);
       sn_AT.reserve(rows * sh.dpad);
+      sn_D.reserve(rows * dim + 4);  // + slack: SG2 copies whole 16-byte pieces
       sn_B.reserve(sh.nch * sh.kpad * sh.dpad);
       sn_BT.reserve(sh.nch * sh.kpad * sh.dpad);
       sn_rowc.reserve(rows);
@@ -502,6 +503,7 @@ struct lgd_context {
       a.sh_AT = sn_AT.get();
       a.sh_BT = sn_BT.get();
       a.sh_rowc = sn_rowc.get();
+      a.sh_D = sn_D.get();
       a.sh_pos = sn_pos.get();
       a.sh_G = sn_G.get();
     }

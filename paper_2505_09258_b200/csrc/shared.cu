@@ -6,14 +6,16 @@
 // (ceil(P / C) k draws per batch).  The reference math on the expanded
 // negative list is the oracle; scores are a dense chunk x negatives x dim
 // contraction, computed here with tcgen05.mma kind::tf32 (FP32 accumulate in
-// TMEM), in three kernels that never materialise the P x k weight matrix:
+// TMEM), in two kernels that never materialise the P x k weight matrix:
 //
-//   SG1 stats   per 128-positive tile: S = IR1 N^T block by block (64
-//               negatives), online row max / sum of exp  ->  M_p, 1/Z_p, loss_p
-//   SG2 mix     per tile: recompute S, W = exp(S - M) / Z into shared memory,
-//               mix += W N on the tensor core
+//   SG2 mix     per 128-positive tile: S = IR1 N^T block by block with an
+//               online softmax; the unnormalised weights into TMEM, acc += W N
+//               on the tensor core  ->  mix = acc / Z - dst, the row's weight
+//               offset c_p = M_p log2e + log2 Z_p and loss_p
 //   SG3 grad    per (chunk, 128 negatives): S^T = N IR1^T recomputed per
-//               64-positive slice, W^T into shared memory, G += W^T IR1
+//               128-positive slice, W^T = 2^(S^T log2e - c) into TMEM,
+//               G += W^T IR1
+// (round 2: a separate statistics pass, SG1, was folded into SG2)
 //
 // Operands live in global memory in the tcgen05 K-major "core matrix" layout
 // without swizzle (8 rows x 16 bytes per 128-byte core matrix, the K-adjacent
@@ -38,7 +40,6 @@ namespace lgd {
 
 namespace {
 
-constexpr int kStatBlk = 128;  // negatives per S block (SG1: one N = 128 MMA chain per block)
 constexpr int kMixBlk = 128;   // negatives per S / mix block (SG2)
 constexpr int kGradSlice = 128;  // positives per S^T / G slice (SG3)
 
@@ -191,7 +192,8 @@ __device__ __forceinline__ void write_core_layouts(const float* tile, uint32_t t
 }
 
 // IR1 (TF32) of 64 padded tile rows, the positive score in FP64, snap = the
-// src row, the dst / src contribution items and the relation key.  Warp w
+// src row, the dst row (tile-major, for SG2's tail), the dst / src
+// contribution items and the relation key.  Warp w
 // fills rows 8w .. 8w + 7: their edges are fetched lane-parallel, then every
 // row is read with 16-byte (ComplEx: 8-byte re / im pair) loads.
 template <int KIND>
@@ -249,6 +251,8 @@ __global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
         pos = xr0 * dr.x + xr1 * dr.y + xi0 * di.x + xi1 * di.y;
         *reinterpret_cast<float2*>(a.snap + p * d + j) = sr;
         *reinterpret_cast<float2*>(a.snap + p * d + j + h) = si;
+        *reinterpret_cast<float2*>(a.sh_D + (row0 + rr) * d + j) = dr;
+        *reinterpret_cast<float2*>(a.sh_D + (row0 + rr) * d + j + h) = di;
         trow[j] = to_tf32((float)xr0);
         trow[j + 1] = to_tf32((float)xr1);
         trow[j + h] = to_tf32((float)xi0);
@@ -266,6 +270,7 @@ __global__ void __launch_bounds__(256) shared_prep_kernel(BatchArgs a) {
       const double x3 = KIND == 0 ? (double)sv.w : (double)sv.w * qv.w;
       pos = x0 * dv.x + x1 * dv.y + x2 * dv.z + x3 * dv.w;
       *reinterpret_cast<float4*>(a.snap + p * d + e) = sv;
+      *reinterpret_cast<float4*>(a.sh_D + (row0 + rr) * d + e) = dv;
       *reinterpret_cast<float4*>(trow + e) =
           make_float4(to_tf32((float)x0), to_tf32((float)x1), to_tf32((float)x2),
                       to_tf32((float)x3));
@@ -350,27 +355,31 @@ __device__ __forceinline__ TileGeom tile_geom(const BatchArgs& a, uint64_t t) {
   return g;
 }
 
-// Pipelining (all three kernels): warp specialised.  Warp 8 (lane 0) issues
-// every bulk copy and MMA; warps 0-7 are the epilogue: warp w reads TMEM lane
-// quarter w % 4 (its 32 tile rows) and column half w / 4 of each 64-column
-// block.  S lives in two TMEM buffers, so the MMA of block b + 1 runs while
-// the epilogue drains block b.  mbarriers:
+// Pipelining (both kernels): warp specialised.  Warp 8 (lane 0) issues the
+// S MMAs and their operands' bulk copies, warp 9 (lane 0) the W-operand MMAs
+// (acc / G) and theirs -- two issuing threads, so the two MMA chains
+// interleave on the tensor pipe instead of one queueing behind the other;
+// warps 0-7 are the epilogue: warp w reads TMEM lane quarter w % 4 (its 32
+// tile rows) and column half w / 4 of each 128-column block.  S lives in two
+// TMEM buffers, so the MMA of block b + 1 runs while the epilogue drains
+// block b.  mbarriers:
 //   ld_*   bulk copy landed (complete_tx)       mma_s[2]  S MMA done (commit)
 //   epi[2] the 8 epilogue warps read S buffer    wrdy      W written (8 warps)
 //   mma_w  the W-operand MMA done (commit): W and that block's operand free
 // Phase parity of a barrier used once per block b with buffer b % 2 is
 // (b / 2) & 1; of one used once per block, b & 1.
 constexpr int kWarps = 8;                      // epilogue warps
-constexpr int kThreadsSG = (kWarps + 1) * 32;  // + the control warp
+constexpr int kThreadsSG = (kWarps + 2) * 32;  // + the two issuing warps
 
 // Developer timeline of one CTA (build with -DLGD_TRACE; not in the product .so)
 #ifdef LGD_TRACE
-// [kernel: SG1, SG2, SG3][control warp, epilogue warp 1][slot]
+// [kernel: SG1 (retired), SG2, SG3][control warp, epilogue warp 1][slot]
 __device__ unsigned long long g_trace[3][2][4096];
 #define SG_TRACE(kid, slot)                                                            \
   do {                                                                                 \
-    if (blockIdx.x == 64 && (threadIdx.x == kWarps * 32 || threadIdx.x == 32) &&       \
-        (slot) < 4096)                                                                 \
+    if (blockIdx.x == 64 &&                                                            \
+        (threadIdx.x == kWarps * 32 || threadIdx.x == (kWarps + 1) * 32 ||              \
+         threadIdx.x == 32) && (slot) < 4096)                                          \
       g_trace[kid][threadIdx.x == 32 ? 1 : 0][(slot)] = clock64();                     \
   } while (0)
 #else
@@ -417,6 +426,19 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
       "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
       "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+// 16 consecutive 32-bit TMEM columns of this thread's lane <- v
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
       : "memory");
 }
 // D[tmem] (+)= A[tmem] . B[smem]^T ("TS": A is read from TMEM, lane = row)
@@ -505,148 +527,15 @@ __device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint
   tc_fence_after();
 }
 
-// SG1: per tile, S = IR1 N^T in 128-negative blocks; online max / sum of exp
-// per row -> c_p = M_p log2e + log2 Z_p (the weights' offset) and
-// loss_p = -(pos_p - (M_p + log Z_p)) (train.cpp:274).
-__global__ void __launch_bounds__(kThreadsSG, 1) sg1_stats_kernel(BatchArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const uint32_t dp = a.dpad, k = a.k, kp = a.kpad;
-  const uint32_t tile_bytes = 128 * dp * 4, blk_bytes = kStatBlk * dp * 4;
-  unsigned char* sA = smem;
-  unsigned char* sN = smem + tile_bytes;  // two blocks
-  __shared__ uint64_t bars[7];            // 0 ld_a, 1-2 ld_n, 3-4 mma_s, 5-6 epi
-  __shared__ uint32_t tbase_s;
-  __shared__ float red_m[128], red_z[128];
-  uint64_t *ld_a = bars, *ld_n = bars + 1, *mma_s = bars + 3, *epi = bars + 5;
-  const uint32_t counts[7] = {1, 1, 1, 1, 1, kWarps, kWarps};
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const TileGeom g = tile_geom(a, blockIdx.x);
-  sg_setup(&tbase_s, 512, bars, 7, counts);  // S buffers [0, 256), IR1 tile [256, 256 + dpad)
-  SG_TRACE(0, 4090);
-  const uint32_t tbase = tbase_s;
-  const uint32_t nblk = kp / kStatBlk;
-  const int q = warp & 3, hf = warp >> 2;
-  const uint32_t row = q * 32 + lane;
-  float m = -INFINITY, z = 0.f;  // running max and sum of 2^((s - m) log2e)
-  if (warp == kWarps) {          // control
-    if (lane == 0) {
-      const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
-      const unsigned char* gN =
-          reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
-      auto load_n = [&](uint32_t b) {
-        bar_expect(ld_n + (b & 1), blk_bytes);
-        bulk_load(sN + (b & 1) * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes,
-                  ld_n + (b & 1));
-      };
-      auto issue_s = [&](uint32_t b) {
-        bar_wait(ld_n + (b & 1), (b >> 1) & 1);
-        if (b >= 2) bar_wait(epi + (b & 1), ((b - 2) >> 1) & 1);
-        tc_fence_after();
-        mma_scores(tbase + (b & 1) * kStatBlk, tbase + 256, saddr(sN + (b & 1) * blk_bytes), dp,
-                   kStatBlk);
-        mma_commit(mma_s + (b & 1));
-      };
-      bar_expect(ld_a, tile_bytes);
-      bulk_load(sA, gA, tile_bytes, ld_a);
-      for (uint32_t b = 0; b < 2 && b < nblk; ++b) load_n(b);
-      SG_TRACE(0, 4000);
-      bar_wait(ld_a, 0);
-      SG_TRACE(0, 4001);
-      tc_fence_after();
-      tile_to_tmem(tbase + 256, saddr(sA), dp);
-      issue_s(0);
-      for (uint32_t b = 0; b < nblk; ++b) {
-        SG_TRACE(0, b * 8 + 0);
-        if (b + 1 < nblk) issue_s(b + 1);
-        SG_TRACE(0, b * 8 + 1);
-        bar_wait(mma_s + (b & 1), (b >> 1) & 1);
-        SG_TRACE(0, b * 8 + 2);
-        if (b + 2 < nblk) load_n(b + 2);
-      }
-    }
-  } else {  // epilogue
-    // each warp half covers 64 of a block's 128 columns
-    const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16) + hf * (kStatBlk / 2);
-    SG_TRACE(0, 4000);
-    for (uint32_t nb = 0; nb < nblk; ++nb) {
-      SG_TRACE(0, nb * 8 + 0);
-      bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
-      SG_TRACE(0, nb * 8 + 1);
-      tc_fence_after();
-      float v[64];
-      tmem_ld32(lane_addr + (nb & 1) * kStatBlk, v);
-      tmem_ld32(lane_addr + (nb & 1) * kStatBlk + 32, v + 32);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) bar_arrive(epi + (nb & 1));
-      const uint32_t j0 = nb * kStatBlk + hf * (kStatBlk / 2);
-      const uint32_t keep0 = keep_mask(j0, k), keep1 = keep_mask(j0 + 32, k);
-      float zs = 0.f, mn;
-      if ((keep0 & keep1) == 0xffffffffu) {  // every column a negative: no masks
-        float b0 = v[0], b1 = v[1];
-#pragma unroll
-        for (int c = 2; c < 64; c += 2) {
-          b0 = fmaxf(b0, v[c]);
-          b1 = fmaxf(b1, v[c + 1]);
-        }
-        mn = fmaxf(m, fmaxf(b0, b1));
-        const float ml2 = mn * kLog2e;
-        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;  // four chains: MUFU latency overlaps
-#pragma unroll
-        for (int c = 0; c < 64; c += 4) {
-          z0 += ex2(__fmaf_rn(v[c], kLog2e, -ml2));
-          z1 += ex2(__fmaf_rn(v[c + 1], kLog2e, -ml2));
-          z2 += ex2(__fmaf_rn(v[c + 2], kLog2e, -ml2));
-          z3 += ex2(__fmaf_rn(v[c + 3], kLog2e, -ml2));
-        }
-        zs = (z0 + z1) + (z2 + z3);
-      } else {
-        float bm = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
-          bm = fmaxf(bm, kc ? v[c] : -INFINITY);
-        }
-        mn = fmaxf(m, bm);
-        const float ml2 = mn * kLog2e;
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
-          zs += kc ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
-        }
-      }
-      z = (m == -INFINITY ? 0.f : z * ex2((m - mn) * kLog2e)) + zs;
-      m = mn;
-      SG_TRACE(0, nb * 8 + 2);
-    }
-    if (hf == 1) {
-      red_m[row] = m;
-      red_z[row] = z;
-    }
-  }
-  __syncthreads();
-  if (warp < 4 && row < g.valid) {  // combine the two column halves of each row
-    const float m1 = red_m[row], z1 = red_z[row];
-    const float M = fmaxf(m, m1);
-    const float Z = (m == -INFINITY ? 0.f : z * ex2((m - M) * kLog2e)) +
-                    (m1 == -INFINITY ? 0.f : z1 * ex2((m1 - M) * kLog2e));
-    const uint64_t tr = g.row0 + row;
-    a.sh_rowc[tr] = (float)((double)M * (double)kLog2e + log2((double)Z));
-    const uint64_t p = g.c * a.chunk + (tr - g.c * (uint64_t)a.tpc * 128);
-    a.loss[p] = -(a.sh_pos[p] - ((double)M + log((double)Z)));
-  }
-  SG_TRACE(0, 4010);
-  tc_fence_before();
-  __syncthreads();
-  SG_TRACE(0, 4091);
-  if (warp == 0) tmem_free(tbase, 512);
-}
-
-// SG2: per tile, mix = W N - dst with W = exp(S - M) / Z recomputed block by
-// block (128 negatives per block: a tf32 MMA costs the same ~96 cycles at
-// N = 64 or 128).  TMEM (512 columns): mix [0, 128), S buffers [128, 384),
-// W [384, 512) (A of the mix MMA).  smem: IR1 tile (A of the S MMA), N blocks
-// x2 (x1 when dpad = 128 would not fit), one N^T block (two 64-column
+// SG2 (stats + mix, one pass): per tile, S = IR1 N^T block by block (128
+// negatives per block: a tf32 MMA costs the same ~96 cycles at N = 64 or 128)
+// with an online softmax per row -- the unnormalised weights W = 2^((S - mu)
+// log2e) go to TMEM as the A operand of acc += W N; mu moves (and acc is
+// rescaled) only when a block's max exceeds it by more than 2^8 in weight.
+// At the end: c = mu log2e + log2 Z (SG3's weight offset), the loss
+// (train.cpp:274) and mix = acc / Z - dst.  TMEM (512 columns): acc [0, 128),
+// S buffers [128, 384), W [384, 512).  smem: IR1 tile (A of the S MMA), N
+// blocks x2 (x1 when dpad = 128 would not fit), one N^T block (two 64-column
 // core-matrix sub-tiles).
 __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uint32_t tcols,
                                                                 uint32_t nbuf) {
@@ -660,6 +549,9 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
   // 0 ld_a, 1-2 ld_n, 3 ld_t, 4-5 mma_s, 6-7 epi, 8 wrdy, 9 mma_w
   __shared__ uint64_t bars[10];
   __shared__ uint32_t tbase_s;
+  // the two column halves' sums of each row, then 1 / Z (the dynamic buffers
+  // leave ~3 KB of the 227)
+  __shared__ float red_z[2][128];
   uint64_t *ld_a = bars, *ld_n = bars + 1, *ld_t = bars + 3, *mma_s = bars + 4, *epi = bars + 6,
            *wrdy = bars + 8, *mma_w = bars + 9;
   const uint32_t counts[10] = {1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1};
@@ -672,27 +564,35 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
   const int q = warp & 3, hf = warp >> 2;
   const uint32_t row = q * 32 + lane;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
-  // first positive of the tile; lane i < 16 of epilogue warp w: the dst id of
-  // tile row w + 8 i (the mix tail's rows), fetched now, used at the end
   const uint64_t tile_p0 = g.c * a.chunk + (g.row0 - g.c * (uint64_t)a.tpc * 128);
-  uint32_t dst_id = 0;
-  if (warp < kWarps && lane < 128 / kWarps && warp + kWarps * lane < g.valid)
-    dst_id = a.edges[3 * (tile_p0 + warp + kWarps * lane) + 2];
-  if (warp == kWarps) {  // control
+  float mu = -INFINITY, zh = 0.f;  // epilogue: the row's online-softmax state
+  // the tile's dst rows (mix = sum_j w_j n_j - dst, train.cpp:306-323): one
+  // contiguous bulk copy of the prep kernel's tile-major copy into the N
+  // blocks, once they are free (after the last S MMA; with one N buffer the
+  // rows reach into the N^T block, so after the last mix MMA); ld_a's second
+  // phase.  (A gather of the 128 rows here cost half of SG2's time.)
+  const uint32_t dst_bytes = (g.valid * d * 4 + 15) & ~15u;
+  unsigned char* sD = sN + 512;  // past the tail tile's overhang into sN
+  auto load_dst = [&]() {
+    if (!dst_bytes) return;
+    bar_expect(ld_a, dst_bytes);
+    bulk_load(sD, a.sh_D + g.row0 * d, dst_bytes, ld_a);
+  };
+  const unsigned char* gT =
+      reinterpret_cast<const unsigned char*>(a.sh_BT) + g.c * (uint64_t)kp * dp * 4;
+  auto load_t = [&](uint32_t b) {
+    bar_expect(ld_t, blk_bytes);
+    bulk_load(sT, gT + (uint64_t)b * blk_bytes, blk_bytes, ld_t);
+  };
+  if (warp == kWarps) {  // S issuer: the IR1 tile, the N blocks, S = IR1 N^T
     if (lane == 0) {
       const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + g.row0 * dp * 4;
       const unsigned char* gN =
           reinterpret_cast<const unsigned char*>(a.sh_B) + g.c * (uint64_t)kp * dp * 4;
-      const unsigned char* gT =
-          reinterpret_cast<const unsigned char*>(a.sh_BT) + g.c * (uint64_t)kp * dp * 4;
       auto load_n = [&](uint32_t b) {  // N block b into buffer b % nbuf
         const uint32_t i = b % nbuf;
         bar_expect(ld_n + i, blk_bytes);
         bulk_load(sN + i * blk_bytes, gN + (uint64_t)b * blk_bytes, blk_bytes, ld_n + i);
-      };
-      auto load_t = [&](uint32_t b) {
-        bar_expect(ld_t, blk_bytes);
-        bulk_load(sT, gT + (uint64_t)b * blk_bytes, blk_bytes, ld_t);
       };
       auto issue_s = [&](uint32_t b) {
         bar_wait(ld_n + b % nbuf, (b / nbuf) & 1);
@@ -705,7 +605,6 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
       bar_expect(ld_a, tile_bytes);
       bulk_load(sA, gA, tile_bytes, ld_a);
       for (uint32_t b = 0; b < nbuf && b < nblk; ++b) load_n(b);
-      load_t(0);
       bar_wait(ld_a, 0);
       issue_s(0);
       for (uint32_t b = 0; b < nblk; ++b) {
@@ -715,12 +614,21 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
         bar_wait(mma_s + (b & 1), (b >> 1) & 1);
         if (b + nbuf < nblk) load_n(b + nbuf);  // S(b) is done with its buffer
         if (nbuf == 1 && b + 1 < nblk) issue_s(b + 1);
+      }
+      if (nbuf == 2) load_dst();
+    }
+  } else if (warp == kWarps + 1) {  // mix issuer: the N^T blocks, acc += W N
+    // (a second issuing thread: its MMA chain interleaves with the S chain
+    // on the tensor pipe instead of queueing behind it)
+    if (lane == 0) {
+      load_t(0);
+      const uint32_t id = instr_desc(128, dp, false, false);
+      for (uint32_t b = 0; b < nblk; ++b) {
         bar_wait(wrdy, b & 1);  // the epilogue wrote W(b)
         SG_TRACE(1, b * 8 + 2);
         bar_wait(ld_t, b & 1);
         tc_fence_after();
-        // mix += W . N^T over the block's 128 negatives (two N^T sub-tiles)
-        const uint32_t id = instr_desc(128, dp, false, false);
+        // acc += W . N^T over the block's 128 negatives (two N^T sub-tiles)
         for (uint32_t ks = 0; ks < kMixBlk / 8; ++ks)
           mma_tf32_ts(tbase, tbase + 384 + ks * 8,
                       smem_desc(saddr(sT) + (ks >> 3) * sub_bytes + (ks & 7) * 256, 128, 16 * 128),
@@ -731,76 +639,117 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
         SG_TRACE(1, b * 8 + 4);
         if (b + 1 < nblk) load_t(b + 1);
       }
+      if (nbuf != 2) load_dst();
     }
   } else {  // epilogue: warp half hf covers 64 of a block's 128 columns
     const bool valid = row < g.valid;
-    const float rc = valid ? a.sh_rowc[g.row0 + row] : 0.f;
+    // online softmax (train.cpp:262-274 restated): mu = the row's reference
+    // max, zh = this half's sum of 2^((s - mu) log2e); W = the unnormalised
+    // weights, the accumulator rescaled when mu moves and divided by Z at the end
     for (uint32_t nb = 0; nb < nblk; ++nb) {
       SG_TRACE(1, nb * 8 + 0);
       bar_wait(mma_s + (nb & 1), (nb >> 1) & 1);
       tc_fence_after();
       SG_TRACE(1, nb * 8 + 1);
       const uint32_t scol0 = 128 + (nb & 1) * kMixBlk + hf * 64;
-      float v[32], w0[32], w1[32];
-      const uint32_t j0 = nb * kMixBlk + hf * 64;
+      const uint32_t scol1 = 128 + (nb & 1) * kMixBlk + (hf ^ 1) * 64;
+      const uint32_t j0 = nb * kMixBlk + hf * 64, j1 = nb * kMixBlk + (hf ^ 1) * 64;
+      // the block's row max over all 128 columns: the other half's 64 are read
+      // too (warps q and q + 4 share the rows), so both warps of the pair
+      // agree on it with no exchange
+      float bm = -INFINITY;
+      for (int part = 0; part < 2; ++part) {
+        float x[32];
+        tmem_ld32(lane_addr + scol1 + 32 * part, x);
+        const uint32_t kx = valid ? keep_mask(j1 + 32 * part, k) : 0u;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) bm = fmaxf(bm, (kx >> c) & 1u ? x[c] : -INFINITY);
+      }
+      float v[64];
       tmem_ld32(lane_addr + scol0, v);
-      weights32(v, rc, valid ? keep_mask(j0, k) : 0u, w0);
-      tmem_ld32(lane_addr + scol0 + 32, v);
+      tmem_ld32(lane_addr + scol0 + 32, v + 32);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(epi + (nb & 1));
-      weights32(v, rc, valid ? keep_mask(j0 + 32, k) : 0u, w1);
+      if (lane == 0) bar_arrive(epi + (nb & 1));  // the S buffer is free
+      const uint32_t keep0 = valid ? keep_mask(j0, k) : 0u;
+      const uint32_t keep1 = valid ? keep_mask(j0 + 32, k) : 0u;
+      const bool full = (keep0 & keep1) == 0xffffffffu;
+      if (full) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) bm = fmaxf(bm, v[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          bm = fmaxf(bm, ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u ? v[c] : -INFINITY);
+      }
+      const float bmax = bm;
+      // the reference max moves only when the block's max exceeds it by more
+      // than 2^8 in weight, so the accumulator is rarely rescaled; both warps
+      // of the row pair decide alike
+      const float mu_new =
+          (mu == -INFINITY || (bmax - mu) * kLog2e > 8.f) ? bmax : mu;
+      const float f = mu == -INFINITY ? 0.f : ex2((mu - mu_new) * kLog2e);
+      const bool rescale = __any_sync(0xffffffffu, mu != -INFINITY && mu_new != mu);
+      mu = mu_new;
+      const float ml2 = mu == -INFINITY ? 0.f : mu * kLog2e;
+      float z0 = 0.f, z1 = 0.f;
+      if (full) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float e0 = ex2(__fmaf_rn(v[c], kLog2e, -ml2));
+          const float e1 = ex2(__fmaf_rn(v[c + 1], kLog2e, -ml2));
+          z0 += e0;
+          z1 += e1;
+          v[c] = tf32_pos(e0);
+          v[c + 1] = tf32_pos(e1);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const bool kc = ((c < 32 ? keep0 : keep1) >> (c & 31)) & 1u;
+          const float e = kc ? ex2(__fmaf_rn(v[c], kLog2e, -ml2)) : 0.f;
+          z0 += e;
+          v[c] = tf32_pos(e);
+        }
+      }
+      zh = zh * f + (z0 + z1);
       SG_TRACE(1, nb * 8 + 2);
-      if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W free again
+      if (nb >= 1) bar_wait(mma_w, (nb - 1) & 1);  // W and the accumulator free again
       tc_fence_after();
       SG_TRACE(1, nb * 8 + 3);
-      tmem_st32(lane_addr + 384 + hf * 64, w0);
-      tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
+      if (rescale) {  // this half's accumulator columns, scaled to the new reference
+        const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
+        for (uint32_t cc = c0; cc < c1; cc += 16) {
+          float x[16];
+          tmem_ld16(lane_addr + cc, x);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[e] *= f;
+          tmem_st16(lane_addr + cc, x);
+        }
+      }
+      tmem_st32(lane_addr + 384 + hf * 64, v);
+      tmem_st32(lane_addr + 384 + hf * 64 + 32, v + 32);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) bar_arrive(wrdy);
       SG_TRACE(1, nb * 8 + 4);
     }
+    red_z[hf][row] = zh;
   }
-  // the tile's dst rows (mix = sum_j w_j n_j - dst, train.cpp:306-323) go to
-  // shared memory by cp.async while the last mix MMA drains: the N blocks are
-  // free once the last S MMA is done (every epilogue warp has seen it).  Warp
-  // w owns rows w, w + 8, ... (ids fetched at the kernel's start).  (Loads
-  // into registers here were consumed -- converted -- one by one, each
-  // waiting its full latency: half of SG2's time.)
-  constexpr int kRowsPerWarp = 128 / kWarps;
-  const uint32_t dst_s = saddr(sN) + 512;  // past the tail tile's overhang into sN
-  auto stage_dst = [&]() {
-    if (warp >= kWarps) return;
-#pragma unroll 4
-    for (int i = 0; i < kRowsPerWarp; ++i) {
-      const uint32_t r = warp + kWarps * i;
-      const uint32_t id = __shfl_sync(0xffffffffu, dst_id, i);
-      if (r >= g.valid) continue;
-      const float* src = a.theta + (size_t)id * d;
-      if ((d & 3) == 0) {
-        for (uint32_t c = lane; c < d / 4; c += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_s + (r * d + 4 * c) * 4),
-                       "l"(src + 4 * c)
-                       : "memory");
-      } else {
-        for (uint32_t e = lane; e < d; e += 32)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst_s + (r * d + e) * 4),
-                       "l"(src + e)
-                       : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  // with one N buffer the rows reach into the N^T block the last mix MMA reads
-  if (nbuf == 2) stage_dst();
   SG_TRACE(1, 4001);
   __syncthreads();
   SG_TRACE(1, 4002);
+  if (warp < 4 && row < g.valid) {  // the row's statistics: the weights' offset and the loss
+    const float Z = red_z[0][row] + red_z[1][row];
+    const uint64_t tr = g.row0 + row;
+    const uint64_t p = tile_p0 + row;
+    a.sh_rowc[tr] = (float)((double)mu * (double)kLog2e + log2((double)Z));
+    a.loss[p] = -(a.sh_pos[p] - ((double)mu + log((double)Z)));  // train.cpp:274
+    red_z[0][row] = 1.f / Z;
+  }
   bar_wait(mma_w, (nblk - 1) & 1);
   SG_TRACE(1, 4003);
-  if (nbuf != 2) stage_dst();
   tc_fence_after();
   // mix accumulator -> shared tile (the IR1 tile, overhanging into the free N
   // blocks by dpad floats); odd row stride: lanes (rows) hit distinct banks
@@ -816,19 +765,31 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg2_mix_kernel(BatchArgs a, uin
     }
   }
   SG_TRACE(1, 4004);
-  asm volatile("cp.async.wait_all;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   SG_TRACE(1, 4005);
-  if (warp < kWarps) {  // coalesced FP64 rows
-    const float* dsts = reinterpret_cast<const float*>(sN + 512);
-    for (int i = 0; i < kRowsPerWarp; ++i) {
-      const uint32_t r = warp + kWarps * i;
-      if (r >= g.valid) break;
+  // mix rows in FP64, coalesced, by all ten warps (the tail is latency-bound:
+  // two rows per step keep eight independent chains per lane; staging them
+  // for bulk stores measured slower)
+  if (dst_bytes) {
+    bar_wait(ld_a, 1);
+    SG_TRACE(1, 4006);
+    const float* dsts = reinterpret_cast<const float*>(sD);
+    constexpr uint32_t kAll = kWarps + 2;
+    for (uint32_t r = warp; r < g.valid; r += 2 * kAll) {
+      const uint32_t r2 = r + kAll;
+      const bool two = r2 < g.valid;
+      const float inv = red_z[0][r], inv2 = two ? red_z[0][r2] : 0.f;
       double* mx = a.mix + (tile_p0 + r) * d;
-      for (uint32_t e = lane; e < d; e += 32)
-        mx[e] = (double)out[r * ts + e] - (double)dsts[r * d + e];
+      double* mx2 = a.mix + (tile_p0 + r2) * d;
+      for (uint32_t e = lane; e < d; e += 32) {
+        const float o = out[r * ts + e], t = dsts[r * d + e];
+        const float o2 = two ? out[r2 * ts + e] : 0.f, t2 = two ? dsts[r2 * d + e] : 0.f;
+        mx[e] = (double)(o * inv) - (double)t;
+        if (two) mx2[e] = (double)(o2 * inv2) - (double)t2;
+      }
     }
+    SG_TRACE(1, 4007);
   }
   __syncthreads();
   SG_TRACE(1, 4091);
@@ -870,20 +831,20 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   SG_TRACE(2, 4090);
   const uint32_t tbase = tbase_s;
   const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
-  if (warp == kWarps) {  // control
+  const unsigned char* gT = reinterpret_cast<const unsigned char*>(a.sh_AT) + crow0 * dp * 4;
+  auto load_t = [&](uint32_t s) {
+    bar_expect(ld_t, sl_bytes);
+    bulk_load(sT, gT + (uint64_t)s * sl_bytes, sl_bytes, ld_t);
+  };
+  if (warp == kWarps) {  // S issuer: the negative block, the IR1 slices, S^T = N IR1^T
     if (lane == 0) {
       const unsigned char* gA = reinterpret_cast<const unsigned char*>(a.sh_A) + crow0 * dp * 4;
-      const unsigned char* gT = reinterpret_cast<const unsigned char*>(a.sh_AT) + crow0 * dp * 4;
       const unsigned char* gN =
           reinterpret_cast<const unsigned char*>(a.sh_B) + (c * (uint64_t)kp + n0) * dp * 4;
       auto load_a = [&](uint32_t s) {
         const uint32_t i = s % nbuf;
         bar_expect(ld_a + i, sl_bytes);
         bulk_load(sA + i * sl_bytes, gA + (uint64_t)s * sl_bytes, sl_bytes, ld_a + i);
-      };
-      auto load_t = [&](uint32_t s) {
-        bar_expect(ld_t, sl_bytes);
-        bulk_load(sT, gT + (uint64_t)s * sl_bytes, sl_bytes, ld_t);
       };
       auto issue_s = [&](uint32_t s) {
         bar_wait(ld_a + s % nbuf, (s / nbuf) & 1);
@@ -896,10 +857,8 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
       bar_expect(ld_n, nblk_bytes);
       bulk_load(sN, gN, nblk_bytes, ld_n);
       for (uint32_t s = 0; s < nbuf && s < nsl; ++s) load_a(s);
-      load_t(0);
       bar_wait(ld_n, 0);
       issue_s(0);
-      const uint32_t id = instr_desc(128, dp, false, false);
       SG_TRACE(2, 4000);
       for (uint32_t s = 0; s < nsl; ++s) {
         SG_TRACE(2, s * 8 + 0);
@@ -909,6 +868,13 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
         SG_TRACE(2, s * 8 + 2);
         if (s + nbuf < nsl) load_a(s + nbuf);
         if (nbuf == 1 && s + 1 < nsl) issue_s(s + 1);
+      }
+    }
+  } else if (warp == kWarps + 1) {  // G issuer: the IR1^T slices, G += W^T IR1
+    if (lane == 0) {
+      load_t(0);
+      const uint32_t id = instr_desc(128, dp, false, false);
+      for (uint32_t s = 0; s < nsl; ++s) {
         bar_wait(wrdy, s & 1);
         SG_TRACE(2, s * 8 + 3);
         bar_wait(ld_t, s & 1);
@@ -982,27 +948,36 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
   __syncthreads();
   bar_wait(mma_w, (nsl - 1) & 1);
   tc_fence_after();
-  // the negative block (and the IR1 tiles after it) is free now; odd row
-  // stride: lanes (rows) hit distinct banks
+  // G rows: TMEM -> the free negative block as compact rows (the chunk block's
+  // rows are contiguous in sh_G), then one bulk store (a row-by-row copy
+  // loop here was latency-bound: ~9k cycles of 8 warps)
   float* out = reinterpret_cast<float*>(sN);
-  const uint32_t ts = dp + 1;
-  if (warp < kWarps) {
+  const uint32_t nrows = k > n0 ? (k - n0 < 128 ? k - n0 : 128) : 0;
+  const uint32_t g_bytes = nrows * d * 4;
+  float* gdst = a.sh_G + (c * (uint64_t)kp + n0) * d;
+  const bool bulk = g_bytes && (g_bytes & 15) == 0 && ((c * (uint64_t)kp + n0) * d * 4 & 15) == 0;
+  if (warp < kWarps) {  // (tcgen05.ld is warp-collective: every lane loads, rows < nrows store)
     const uint32_t c0 = hf * 64, c1 = hf ? dp : (dp < 64 ? dp : 64);
+    float* o = bulk ? out + row * d : gdst + (uint64_t)row * d;
     for (uint32_t cc = c0; cc < c1; cc += 16) {
       float v[16];
       tmem_ld16(lane_addr + cc, v);
+      if (row < nrows) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) out[row * ts + cc + e] = v[e];
+        for (int e = 0; e < 16; ++e)
+          if (cc + e < d) o[cc + e] = v[e];
+      }
     }
+    if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
-  if (warp < kWarps) {  // G rows, coalesced
-    const uint32_t nrows = k > n0 ? (k - n0 < 128 ? k - n0 : 128) : 0;
-    for (uint32_t r = warp; r < nrows; r += kWarps) {
-      float* gout = a.sh_G + (c * (uint64_t)kp + n0 + r) * d;
-      for (uint32_t e = lane; e < d; e += 32) gout[e] = out[r * ts + e];
-    }
+  if (bulk && threadIdx.x == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(saddr(out)), "r"(g_bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory reusable
   }
   __syncthreads();
   SG_TRACE(2, 4091);
@@ -1058,7 +1033,6 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   shared_gather_kernel<<<(unsigned)(a.nch * (uint64_t)a.kpad / kPrepRows), 256, psm, st>>>(a);
   LGD_LAUNCH_CHECK();
   const size_t t = 128ull * dp * 4;
-  const size_t sm1 = t + 2 * (size_t)kStatBlk * dp * 4;
   // SG2: two N buffers when they fit next to the tile and the N^T block
   const size_t mblk = (size_t)kMixBlk * dp * 4;
   const uint32_t nbuf2 = t + 3 * mblk <= 227 * 1024 ? 2 : 1;
@@ -1066,15 +1040,12 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   const size_t gsl = (size_t)kGradSlice * dp * 4;
   const uint32_t nbuf3 = t + 3 * gsl <= 227 * 1024 ? 2 : 1;
   const size_t sm3 = t + (nbuf3 + 1) * gsl;
-  static size_t set1[kMaxDevices], set2[kMaxDevices], set3[kMaxDevices];  // grow only
+  static size_t set2[kMaxDevices], set3[kMaxDevices];  // grow only
   const int dev = current_device();
-  if (sm1 > set1[dev]) set_smem(sg1_stats_kernel, set1[dev] = sm1);
   if (sm2 > set2[dev]) set_smem(sg2_mix_kernel, set2[dev] = sm2);
   if (sm3 > set3[dev]) set_smem(sg3_grad_kernel, set3[dev] = sm3);
   const unsigned tiles = (unsigned)(a.nch * a.tpc);
   const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
-  sg1_stats_kernel<<<tiles, kThreadsSG, sm1, st>>>(a);
-  LGD_LAUNCH_CHECK();
   sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, nbuf2);
   LGD_LAUNCH_CHECK();
   sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, nbuf3);

@@ -110,6 +110,7 @@ struct BatchArgs {
   uint64_t nch;               // chunks in this batch
   float* sh_A;                // IR1 tiles, core-matrix layout (nch x tpc x 128 rows x dpad)
   float* sh_AT;               // IR1^T per 64-positive slice (dpad x 64), core-matrix layout
+  float* sh_D;                // dst rows per padded tile row (rows x dim), prep -> SG2's tail
   float* sh_B;                // negative rows, core-matrix layout (nch x kpad x dpad)
   float* sh_BT;               // N^T per 64-negative block (dpad x 64)
   float* sh_rowc;             // per padded tile row: log2 of the softmax denominator,

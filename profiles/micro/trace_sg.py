@@ -33,6 +33,8 @@ names = {
         "warp 1": ["top", "S ready", "W computed", "W free", "W written"]},
 }
 for kid, kname in enumerate(["SG1", "SG2", "SG3"]):
+    if not buf[kid].any():
+        continue
     print(f"===== {kname}")
     for w, who in enumerate(("control", "warp 1")):
         row = buf[kid, w]

@@ -6,7 +6,7 @@ exact   one epoch of every model (DistMult, ComplEx, TransE, Dot) at a small
         shape: K1 shuffle, K2 sampler, bucket presort, K3 score, K4 pass 1 + 2
         (hub segments forced by a skewed graph), the relation side pass, then
         K6 evaluate.
-shared  one epoch of shared-negative chunks (tcgen05 SG1-SG3 + K4).
+shared  one epoch of shared-negative chunks (tcgen05 SG2 / SG3 + K4).
 Each finishes in well under a second natively; the checkers slow it ~100x.
 """
 import os
