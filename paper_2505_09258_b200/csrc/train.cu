@@ -321,9 +321,23 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
       const float* row = q < k ? R + (3 + q) * dpad : drow;
       double f = 0.0;
       if (KIND == 3) {  // -||u - t||, squares summed sequentially
-        for (uint32_t i = 0; i < d; ++i) {
-          const double q = ir1[i] - (double)row[i];
-          f += q * q;
+        if ((d & 3) == 0) {  // 16-byte shared loads, the same sequential order
+          for (uint32_t i = 0; i < d; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(row + i);
+            const double2 x0 = *reinterpret_cast<const double2*>(ir1 + i);
+            const double2 x1 = *reinterpret_cast<const double2*>(ir1 + i + 2);
+            const double q0 = x0.x - (double)v.x, q1 = x0.y - (double)v.y;
+            const double q2 = x1.x - (double)v.z, q3 = x1.y - (double)v.w;
+            f += q0 * q0;
+            f += q1 * q1;
+            f += q2 * q2;
+            f += q3 * q3;
+          }
+        } else {
+          for (uint32_t i = 0; i < d; ++i) {
+            const double q = ir1[i] - (double)row[i];
+            f += q * q;
+          }
         }
         f = -sqrt(f);
       } else if ((d & 3) == 0) {

@@ -160,3 +160,50 @@ def test_shared_mode_rejects_unsupported_shapes():
     t2.init_store(1)
     with pytest.raises(lgd.InvalidArgument):
         t2.train_batch(edges, np.array([1, 2, 3, 4], np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["dot", "distmult"])
+def test_shared_online_softmax_rescales(oracle, kind):
+    """SG2's online softmax moves its reference max, and rescales the mix
+    accumulator, only when a later 128-negative block's max exceeds it by more
+    than 2^8 in weight.  Shared negatives whose last blocks hold rows ~300x
+    larger force such rescales; the same negatives with the large rows first
+    need none.  The two orders give the same loss and gradients (the softmax
+    is order-free; FP32 sums in another order), and both match the expanded
+    reference within TF32 tolerances scaled to the large scores."""
+    d, k, chunk, P, V, R = 64, 1000, 256, 1024, 4000, 5
+    rng = np.random.default_rng(17)
+    E0 = rng.uniform(-0.5 / np.sqrt(d), 0.5 / np.sqrt(d), (V, d)).astype(np.float32)
+    E0[V // 2:] *= 300.0  # the large rows: only ever shared negatives
+    S0 = rng.uniform(0, 0.01, (V, d)).astype(np.float32)
+    rE0 = rng.uniform(0.5, 1.0, (R, d)).astype(np.float32)
+    Rm = R if kind != "dot" else 0
+    rels = rng.integers(0, R, P) if Rm else np.full(P, 0xFFFFFFFF)
+    edges = np.stack([rng.integers(0, V // 2, P), rels, rng.integers(0, V // 2, P)],
+                     1).astype(np.uint32)
+    nch = -(-P // chunk)
+    small = rng.integers(0, V // 2, (nch, 512))
+    large = rng.integers(V // 2, V, (nch, k - 512))
+    orders = {"large last (rescales)": np.concatenate([small, large], 1),
+              "large first": np.concatenate([large, small], 1)}
+    got = {}
+    for name, sh in orders.items():
+        shared = sh.reshape(-1).astype(np.uint32)
+        t = trainer(kind, d, V, Rm, edges, k, chunk)
+        t.load_tables(E0, S0)
+        if Rm:
+            t.set_relations(rE0, np.zeros_like(rE0))
+        got[name] = t.batch_gradients(edges, shared)
+        negs = oracle.expand_shared(shared, P, k, chunk)
+        want = oracle.batch(kind, E0.copy(), S0.copy(), rE0.copy() if Rm else None,
+                            np.zeros_like(rE0) if Rm else None, edges, negs, k, apply=False,
+                            grads=True)
+        g = got[name]
+        assert g["loss"] == pytest.approx(want["loss"], rel=1e-3), name
+        assert np.array_equal(g["node_ids"], want["node_ids"]), name
+        assert frob(g["node_grads"], want["node_grads"]) <= 1e-2, name
+        t.close()
+    a, b = got.values()
+    assert a["loss"] == pytest.approx(b["loss"], rel=1e-5)
+    assert np.array_equal(a["node_ids"], b["node_ids"])
+    assert frob(a["node_grads"], b["node_grads"]) <= 1e-4
