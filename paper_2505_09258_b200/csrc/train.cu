@@ -1412,8 +1412,15 @@ constexpr uint32_t kLongSeg = 32;
 // contribution's operand row (f64 width), its weight
 __host__ __device__ constexpr uint32_t seg_slot_bytes(uint32_t rowf) { return 16 * rowf + 16; }
 
+// TransE's K4 runs faster with 80 registers (3 blocks of 256 per SM) than with
+// 64 (4 blocks): Friendster K4 0.907 -> 0.860 ms; the other models are best
+// at 64 (TW DistMult 0.80 vs 0.82, LJ Dot 0.49 vs 0.51, FM ComplEx 0.69 vs 0.70
+// ms; profiles/r02zh, r02zi)
+template <int KIND>
+constexpr int seg_heads_minb() { return KIND == 3 && SEG_MINB == 4 ? 3 : SEG_MINB; }
+
 template <int KIND, int NV, bool SH, bool IR1, bool R64>
-__global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_heads(
+__global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_heads(
     BatchArgs a, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
     uint64_t b0, uint64_t b1) {
   constexpr int NE = 4 * NV;
