@@ -58,8 +58,9 @@ constexpr int kSegThreads = SEG_THREADS;
 #ifndef SEG_DEPTH
 #define SEG_DEPTH 2
 #endif
-// segments whose rows (and first contribution) are in flight per warp in K4's
-// cp.async ring: segment_heads measured 2 best (0.80 ms per TW batch; 3: 0.81,
+// pieces / segments whose rows are in flight per warp in K4's cp.async rings
+// (the chunked and flattened kernels; segment_heads picks its depth per model,
+// seg_heads_depth: TW DistMult measured 2 best, 0.80 ms per batch; 3: 0.81,
 // 4: 0.88 -- the ring's shared memory costs occupancy)
 constexpr int kSegDepth = SEG_DEPTH;
 
@@ -1418,6 +1419,17 @@ __host__ __device__ constexpr uint32_t seg_slot_bytes(uint32_t rowf) { return 16
 // ms; profiles/r02zh, r02zi)
 template <int KIND>
 constexpr int seg_heads_minb() { return KIND == 3 && SEG_MINB == 4 ? 3 : SEG_MINB; }
+// segment_heads' ring depth per model: 3 for Dot / ComplEx (LJ K4 0.499 ->
+// 0.489 ms, FM 0.686 -> 0.683), 2 for DistMult / TransE (TW 0.80 vs 0.81,
+// Friendster 0.866 vs 0.884; profiles/r02m, r02zk); -DSEG_DEPTH_FIXED: SEG_DEPTH for all
+template <int KIND>
+constexpr int seg_heads_depth() {
+#ifdef SEG_DEPTH_FIXED
+  return SEG_DEPTH;
+#else
+  return KIND == 0 || KIND == 2 ? 3 : 2;
+#endif
+}
 
 template <int KIND, int NV, bool SH, bool IR1, bool R64>
 __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_heads(
@@ -1469,16 +1481,17 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     const uint32_t v1 = __shfl_sync(0xffffffffu, w1, o & 31);
     return o < 32 ? v0 : v1;
   };
-  // ring of kSegDepth slots per warp: the theta / state rows AND the first
+  // ring of kDepth slots per warp: the theta / state rows AND the first
   // contribution's operand row and weight of the next segments are in flight
   // (cp.async, one commit group per segment), so a segment starts without a
   // dependent global load
+  constexpr int kDepth = seg_heads_depth<KIND>();
   extern __shared__ __align__(16) float seg_ring[];
   const uint32_t rowf = (a.dim + 3) & ~3u;
   const uint32_t sb = seg_slot_bytes(rowf);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
-                        (threadIdx.x >> 5) * kSegDepth * sb;  // bytes
-  const uint32_t ring_end = ring + kSegDepth * sb;
+                        (threadIdx.x >> 5) * kDepth * sb;  // bytes
+  const uint32_t ring_end = ring + kDepth * sb;
   uint32_t srest = todo;  // segments still to stage, lowest first
   auto stage = [&](uint32_t slot) {
     if (srest) {
@@ -1492,7 +1505,7 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int u = 0; u < kSegDepth; ++u) stage(ring + u * sb);
+  for (int u = 0; u < kDepth; ++u) stage(ring + u * sb);
   uint32_t slot = ring;
 #pragma unroll 1
   while (todo) {
@@ -1501,7 +1514,7 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     const uint32_t len = __shfl_sync(0xffffffffu, my_len, h);
     const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
     const uint32_t v0 = item(h);
-    asm volatile("cp.async.wait_group %0;" ::"n"(kSegDepth - 1) : "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
     __syncwarp();  // lane 0 staged the weight every lane reads
     float th[NE], st[NE];
     L.lds_s(slot, th);
@@ -2053,7 +2066,8 @@ void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStr
 
 template <int KIND, int NV, bool SH, bool IR1, bool R64>
 void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStream_t st) {
-  const size_t smem = (size_t)(kSegThreads / 32) * kSegDepth * seg_slot_bytes((a.dim + 3) & ~3u);
+  const size_t smem =
+      (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * seg_slot_bytes((a.dim + 3) & ~3u);
   static size_t attr[kMaxDevices];
   const int dev = current_device();
   if (smem > attr[dev]) {
