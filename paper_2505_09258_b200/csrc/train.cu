@@ -46,6 +46,11 @@ namespace {
 #define SCORE_WARPS 8
 #endif
 constexpr int kScoreWarps = SCORE_WARPS;
+// warps per K3 block by model: TransE (d = 128 on its BASELINE config, ~11 KB
+// of rows per warp) packs more warps per SM in 4-warp blocks (Friendster
+// +1.4%); 8-warp blocks are best for the rest (TW -1.7% at 4; r02zg)
+template <int KIND>
+constexpr int score_warps() { return KIND == 3 && SCORE_WARPS == 8 ? 4 : SCORE_WARPS; }
 #ifndef SEG_THREADS
 #define SEG_THREADS 256
 #endif
@@ -183,11 +188,12 @@ struct ScoreSmem {
     e_off = f_off + size_t(kk + 1) * 8;
     warp_bytes = (e_off + size_t(kk) * 8 + 15) & ~size_t(15);
   }
-  __host__ __device__ size_t block_bytes() const { return 16 * kScoreWarps + kScoreWarps * warp_bytes; }
+  __host__ __device__ size_t block_bytes(int warps) const { return 16 * warps + warps * warp_bytes; }
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, int use_tma) {
+__global__ void __launch_bounds__(score_warps<KIND>() * 32) score_kernel(BatchArgs a, int use_tma) {
+  constexpr int kWarpsK3 = score_warps<KIND>();
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t k = a.k, d = a.dim, h = d / 2;
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
   const uint32_t dpad = L.dpad, nrows = L.nrows;
   const uint32_t nid = (nrows + 31) & ~31u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-  unsigned char* wbase = smem + 16 * kScoreWarps + warp * L.warp_bytes;
+  unsigned char* wbase = smem + 16 * kWarpsK3 + warp * L.warp_bytes;
   uint32_t* ids = reinterpret_cast<uint32_t*>(wbase + L.ids_off);
   float* rows = reinterpret_cast<float*>(wbase + L.rows_off);
   double* ir1 = reinterpret_cast<double*>(wbase + L.ir1_off);
@@ -245,8 +251,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(BatchArgs a, in
     __syncwarp();
   };
 
-  const uint64_t nwarps = (uint64_t)gridDim.x * kScoreWarps;
-  uint64_t p = (uint64_t)blockIdx.x * kScoreWarps + warp;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarpsK3;
+  uint64_t p = (uint64_t)blockIdx.x * kWarpsK3 + warp;
   uint32_t phase = 0;
   uint32_t id_next = 0;
   const int b = 0;
@@ -2374,7 +2380,8 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
   const uint32_t d = a.dim, k = a.k;
   const uint64_t P = a.P;
   const ScoreSmem L(d, k);
-  const size_t smem = L.block_bytes();
+  constexpr int kW = score_warps<KIND>();
+  const size_t smem = L.block_bytes(kW);
   const int tma = ((d % 4) == 0 && L.nrows <= 32) ? 1 : 0;
   rec(0);
   {
@@ -2391,15 +2398,15 @@ void run_batch(const BatchArgs& a_in, cudaStream_t st, const BatchEvents* ev) {
     }
     if (occ_smem[KIND] != smem) {
       LGD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_val[KIND], score_kernel<KIND>,
-                                                             kScoreWarps * 32, smem));
+                                                             kW * 32, smem));
       occ_smem[KIND] = smem;
     }
     const int per_sm = occ_val[KIND];
     if (per_sm < 1) throw std::invalid_argument("batch shape exceeds shared memory (k, dim)");
-    const uint64_t blocks_needed = (P + kScoreWarps - 1) / kScoreWarps;
+    const uint64_t blocks_needed = (P + kW - 1) / kW;
     const uint64_t cap = (uint64_t)per_sm * a.sm_count;
     const unsigned grid = (unsigned)(blocks_needed < cap ? blocks_needed : cap);
-    score_kernel<KIND><<<grid, kScoreWarps * 32, smem, st>>>(a, tma);
+    score_kernel<KIND><<<grid, kW * 32, smem, st>>>(a, tma);
     LGD_LAUNCH_CHECK();
   }
   if (KIND == 0 && a.side) {  // Dot: the batch loss on the side stream, off K4's path
@@ -2633,7 +2640,9 @@ int sort_bucket(void* temp, size_t temp_bytes, uint32_t* keys[2], uint32_t* vals
   return k.selector;
 }
 
-size_t score_smem_bytes(uint32_t dim, uint32_t k) { return ScoreSmem(dim, k).block_bytes(); }
+size_t score_smem_bytes(uint32_t dim, uint32_t k) {
+  return ScoreSmem(dim, k).block_bytes(kScoreWarps);  // the largest block of any model
+}
 
 #ifdef LGD_TRACE
 extern "C" int lgd_debug_trace_k4(unsigned long long* out) {
