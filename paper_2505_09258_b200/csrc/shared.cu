@@ -31,6 +31,8 @@
 // rounded to TF32 (cvt.rna) when they are written.  The node-gradient
 // contributions (dst: -IR1, negative: G row, src: adj(mix)) then go through
 // the same sort-by-node segmented reduction and Adagrad as the exact path.
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -985,6 +987,239 @@ __global__ void __launch_bounds__(kThreadsSG, 1) sg3_grad_kernel(BatchArgs a, ui
 }
 
 
+// SG3, persistent (two IR1 slice buffers fit): one CTA per SM walks the (chunk,
+// 128-negative block) items blockIdx.x, + gridDim.x, ... as one stream of
+// slices, so a slice's loads, MMAs and epilogue overlap across item
+// boundaries: the next item's IR1 slices and IR1^T slice are prefetched by
+// the ring as usual, its negative block loads as soon as the last S^T MMA of
+// the current item is done, and the epilogue drains G straight from TMEM to
+// global memory while the next item's first S^T MMA runs (acc_free orders
+// the next item's first G MMA after the drain).
+struct Sg3Item {
+  uint64_t c, chunk_rows, crow0;
+  uint32_t n0, nsl;
+};
+__device__ __forceinline__ Sg3Item sg3_item(const BatchArgs& a, uint64_t w) {
+  const uint32_t nbpc = a.kpad / 128;
+  Sg3Item it;
+  it.c = w / nbpc;
+  it.n0 = (uint32_t)(w - it.c * nbpc) * 128;
+  const uint64_t left = a.P - it.c * a.chunk;
+  it.chunk_rows = left < a.chunk ? left : a.chunk;
+  it.nsl = (uint32_t)((it.chunk_rows + kGradSlice - 1) / kGradSlice);
+  it.crow0 = it.c * (uint64_t)a.tpc * 128;
+  return it;
+}
+struct Sg3Cursor {  // (item, slice) of a CTA's slice stream
+  uint64_t w, nitems;
+  uint32_t s, ii, step;
+  Sg3Item it;
+  bool valid;
+  __device__ void start(const BatchArgs& a, uint64_t w0, uint32_t stride, uint64_t n) {
+    w = w0;
+    nitems = n;
+    s = 0;
+    ii = 0;
+    step = stride;
+    valid = w < nitems;
+    if (valid) it = sg3_item(a, w);
+  }
+  __device__ void advance(const BatchArgs& a) {
+    if (!valid) return;
+    if (++s < it.nsl) return;
+    s = 0;
+    ++ii;
+    w += step;
+    valid = w < nitems;
+    if (valid) it = sg3_item(a, w);
+  }
+};
+
+__global__ void __launch_bounds__(kThreadsSG, 1) sg3_persistent_kernel(BatchArgs a, uint32_t tcols,
+                                                                       uint64_t nitems) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const uint32_t dp = a.dpad, k = a.k, kp = a.kpad, d = a.dim;
+  const uint32_t nblk_bytes = 128 * dp * 4, sl_bytes = kGradSlice * dp * 4;
+  const uint32_t sub_bytes = 64 * dp * 4;  // one 64-positive IR1^T sub-tile
+  unsigned char* sN = smem;
+  unsigned char* sA = sN + nblk_bytes;   // 2 x IR1 slice
+  unsigned char* sT = sA + 2 * sl_bytes;  // 1 x IR1^T slice
+  // 0 ld_n, 1-2 ld_a, 3 ld_t, 4-5 mma_s, 6-7 epi, 8 wrdy, 9 mma_w, 10 acc_free
+  __shared__ uint64_t bars[11];
+  __shared__ uint32_t tbase_s;
+  uint64_t *ld_n = bars, *ld_a = bars + 1, *ld_t = bars + 3, *mma_s = bars + 4, *epi = bars + 6,
+           *wrdy = bars + 8, *mma_w = bars + 9, *acc_free = bars + 10;
+  const uint32_t counts[11] = {1, 1, 1, 1, 1, 1, kWarps, kWarps, kWarps, 1, kWarps};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, hf = warp >> 2;
+  const uint32_t row = q * 32 + lane;  // negative n0 + row
+  sg_setup(&tbase_s, tcols, bars, 11, counts);
+  SG_TRACE(2, 4090);
+  const uint32_t tbase = tbase_s;
+  const uint32_t lane_addr = tbase + ((uint32_t)(q * 32) << 16);
+  const unsigned char* gA0 = reinterpret_cast<const unsigned char*>(a.sh_A);
+  const unsigned char* gT0 = reinterpret_cast<const unsigned char*>(a.sh_AT);
+  const unsigned char* gN0 = reinterpret_cast<const unsigned char*>(a.sh_B);
+  Sg3Cursor first;
+  first.start(a, blockIdx.x, gridDim.x, nitems);
+  if (warp == kWarps) {  // S issuer: negative blocks, IR1 slices, S^T = N IR1^T
+    if (lane == 0) {
+      auto load_n = [&](const Sg3Cursor& cu) {
+        bar_expect(ld_n, nblk_bytes);
+        bulk_load(sN, gN0 + (cu.it.c * (uint64_t)kp + cu.it.n0) * dp * 4, nblk_bytes, ld_n);
+      };
+      auto load_a = [&](const Sg3Cursor& cu, uint32_t g) {
+        bar_expect(ld_a + (g & 1), sl_bytes);
+        bulk_load(sA + (g & 1) * sl_bytes, gA0 + (cu.it.crow0 * dp * 4 + (uint64_t)cu.s * sl_bytes),
+                  sl_bytes, ld_a + (g & 1));
+      };
+      auto issue_s = [&](const Sg3Cursor& cu, uint32_t g) {
+        bar_wait(ld_a + (g & 1), (g >> 1) & 1);
+        if (g >= 2) bar_wait(epi + (g & 1), ((g - 2) >> 1) & 1);
+        if (cu.s == 0) bar_wait(ld_n, cu.ii & 1);
+        tc_fence_after();
+        mma_scores_ss(tbase + 128 + (g & 1) * kGradSlice, saddr(sN), saddr(sA + (g & 1) * sl_bytes),
+                      dp, kGradSlice);
+        mma_commit(mma_s + (g & 1));
+      };
+      Sg3Cursor cur = first, ld = first;
+      load_n(cur);
+      load_a(ld, 0);
+      ld.advance(a);
+      if (ld.valid) {
+        load_a(ld, 1);
+        ld.advance(a);
+      }
+      issue_s(cur, 0);
+      Sg3Cursor nx = cur;
+      nx.advance(a);
+      for (uint32_t g = 0; cur.valid; ++g) {
+        SG_TRACE(2, (g & 511) * 8 + 0);
+        const bool crossing = nx.valid && nx.ii != cur.ii;
+        if (nx.valid && !crossing) issue_s(nx, g + 1);
+        bar_wait(mma_s + (g & 1), (g >> 1) & 1);  // S^T(g) done: its IR1 slot (and sN) free
+        SG_TRACE(2, (g & 511) * 8 + 1);
+        if (crossing) {  // the next item's negative block, then its first S^T MMA
+          load_n(nx);
+          issue_s(nx, g + 1);
+        }
+        if (ld.valid) {
+          load_a(ld, g + 2);
+          ld.advance(a);
+        }
+        cur = nx;
+        nx.advance(a);
+      }
+    }
+  } else if (warp == kWarps + 1) {  // G issuer: IR1^T slices, G += W^T IR1
+    if (lane == 0) {
+      auto load_t = [&](const Sg3Cursor& cu) {
+        bar_expect(ld_t, sl_bytes);
+        bulk_load(sT, gT0 + (cu.it.crow0 * dp * 4 + (uint64_t)cu.s * sl_bytes), sl_bytes, ld_t);
+      };
+      const uint32_t id = instr_desc(128, dp, false, false);
+      Sg3Cursor cur = first;
+      load_t(cur);
+      for (uint32_t g = 0; cur.valid; ++g) {
+        bar_wait(wrdy, g & 1);
+        bar_wait(ld_t, g & 1);
+        if (cur.s == 0 && cur.ii > 0) bar_wait(acc_free, (cur.ii - 1) & 1);  // G drained
+        SG_TRACE(2, (g & 511) * 8 + 3);
+        tc_fence_after();
+        for (uint32_t ks = 0; ks < kGradSlice / 8; ++ks)
+          mma_tf32_ts(tbase, tbase + 384 + ks * 8,
+                      smem_desc(saddr(sT) + (ks >> 3) * sub_bytes + (ks & 7) * 256, 128, 16 * 128),
+                      id, (cur.s | ks) != 0);
+        mma_commit(mma_w);
+        bar_wait(mma_w, g & 1);
+        SG_TRACE(2, (g & 511) * 8 + 5);
+        cur.advance(a);
+        if (cur.valid) load_t(cur);
+      }
+    }
+  } else {  // epilogue: row = negative, warp half hf covers 64 of the slice's positives
+    auto load_c = [&](const Sg3Cursor& cu, float& c0, float& c1) {
+      const uint64_t pq0 = (uint64_t)cu.s * kGradSlice + hf * 64 + lane, pq1 = pq0 + 32;
+      c0 = pq0 < cu.it.chunk_rows ? a.sh_rowc[cu.it.crow0 + pq0] : 0.f;
+      c1 = pq1 < cu.it.chunk_rows ? a.sh_rowc[cu.it.crow0 + pq1] : 0.f;
+    };
+    Sg3Cursor cur = first;
+    float cn0 = 0.f, cn1 = 0.f;
+    if (cur.valid) load_c(cur, cn0, cn1);
+    for (uint32_t g = 0; cur.valid; ++g) {
+      const Sg3Item it = cur.it;
+      const bool nvalid = it.n0 + row < k;
+      const uint64_t pq0 = (uint64_t)cur.s * kGradSlice + hf * 64 + lane, pq1 = pq0 + 32;
+      const bool pv0 = pq0 < it.chunk_rows, pv1 = pq1 < it.chunk_rows;
+      const float c0 = cn0, c1 = cn1;
+      Sg3Cursor nx = cur;
+      nx.advance(a);
+      if (nx.valid) load_c(nx, cn0, cn1);
+      const uint32_t pm0 = __ballot_sync(0xffffffffu, pv0);
+      const uint32_t pm1 = __ballot_sync(0xffffffffu, pv1);
+      const uint32_t keep0 = nvalid ? pm0 : 0u, keep1 = nvalid ? pm1 : 0u;
+      bar_wait(mma_s + (g & 1), (g >> 1) & 1);
+      tc_fence_after();
+      const uint32_t scol0 = 128 + (g & 1) * kGradSlice + hf * 64;
+      float v[32], w0[32], w1[32];
+      tmem_ld32(lane_addr + scol0, v);
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, c0, cc)));
+        w0[cc] = (keep0 >> cc) & 1u ? tf32_pos(e) : 0.f;
+      }
+      tmem_ld32(lane_addr + scol0 + 32, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(epi + (g & 1));
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const float e = ex2(__fmaf_rn(v[cc], kLog2e, -__shfl_sync(0xffffffffu, c1, cc)));
+        w1[cc] = (keep1 >> cc) & 1u ? tf32_pos(e) : 0.f;
+      }
+      if (g >= 1) bar_wait(mma_w, (g - 1) & 1);  // W^T free again
+      tc_fence_after();
+      tmem_st32(lane_addr + 384 + hf * 64, w0);
+      tmem_st32(lane_addr + 384 + hf * 64 + 32, w1);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(wrdy);
+      SG_TRACE(2, (g & 511) * 8 + 4);
+      if (cur.s + 1 == it.nsl) {  // the item's last slice: G -> global rows, then acc_free
+        bar_wait(mma_w, g & 1);
+        tc_fence_after();
+        const uint32_t nrows = k > it.n0 ? (k - it.n0 < 128 ? k - it.n0 : 128) : 0;
+        float* grow = a.sh_G + (it.c * (uint64_t)kp + it.n0 + row) * d;
+        const uint32_t c0r = hf * 64, c1r = hf ? dp : (dp < 64 ? dp : 64);
+        for (uint32_t cc = c0r; cc < c1r; cc += 16) {
+          float x[16];
+          tmem_ld16(lane_addr + cc, x);  // warp-collective: every lane loads
+          if (row < nrows) {
+            if ((d & 3) == 0 && cc + 16 <= d) {
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(grow + cc + e) =
+                    make_float4(x[e], x[e + 1], x[e + 2], x[e + 3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (cc + e < d) grow[cc + e] = x[e];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(acc_free);
+      }
+      cur = nx;
+    }
+  }
+  __syncthreads();
+  SG_TRACE(2, 4091);
+  if (warp == 0) tmem_free(tbase, tcols);
+}
+
 template <class K>
 void set_smem(K kernel, size_t bytes) {
   LGD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -997,6 +1232,12 @@ extern "C" int lgd_debug_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) == cudaSuccess ? 0 : 4;
 }
 #endif
+
+// LGD_SG3_CLASSIC=1: one CTA per item (A/B against the persistent SG3)
+static const bool g_sg3_classic = [] {
+  const char* e = std::getenv("LGD_SG3_CLASSIC");
+  return e && std::strtol(e, nullptr, 10) != 0;
+}();
 
 SharedShape shared_shape(uint32_t dim, uint32_t k, uint32_t chunk, uint64_t P) {
   SharedShape s{};
@@ -1048,7 +1289,15 @@ void launch_shared_scores(const BatchArgs& a, cudaStream_t st) {
   const uint32_t tcols = 512;   // + the TMEM A operands at 256 and 384
   sg2_mix_kernel<<<tiles, kThreadsSG, sm2, st>>>(a, tcols, nbuf2);
   LGD_LAUNCH_CHECK();
-  sg3_grad_kernel<<<(unsigned)(a.nch * (a.kpad / 128)), kThreadsSG, sm3, st>>>(a, tcols, nbuf3);
+  const uint64_t items3 = a.nch * (a.kpad / 128);
+  if (nbuf3 == 2 && !g_sg3_classic) {  // persistent: one CTA per SM over the item stream
+    static size_t setp[kMaxDevices];
+    if (sm3 > setp[dev]) set_smem(sg3_persistent_kernel, setp[dev] = sm3);
+    const unsigned grid3 = (unsigned)(items3 < (uint64_t)a.sm_count ? items3 : a.sm_count);
+    sg3_persistent_kernel<<<grid3, kThreadsSG, sm3, st>>>(a, tcols, items3);
+  } else {
+    sg3_grad_kernel<<<(unsigned)items3, kThreadsSG, sm3, st>>>(a, tcols, nbuf3);
+  }
   LGD_LAUNCH_CHECK();
 }
 
