@@ -252,7 +252,9 @@ int lgd_round_end(lgd_context* ctx, lgd_epoch_result* out);
 
 /* A fresh NCCL unique id (128 bytes) on rank 0, to share with every rank. */
 int lgd_comm_unique_id(void* id128);
-/* Joins rank `rank` of `world` (world = 1: no NCCL, a local runner).  The
+/* Joins rank `rank` of `world` over NCCL communicators built from id128
+ * (required for world > 1; at world = 1 a null id runs a local runner with
+ * no NCCL, a non-null id still builds the one-rank communicators).  The
  * tables must exist and stay allocated (lgd_init_store / lgd_load_partition
  * first).  Collective over the ranks. */
 int lgd_comm_init(lgd_context* ctx, const void* id128, uint32_t rank, uint32_t world);

@@ -137,6 +137,7 @@ struct RoundRunner {
   std::vector<std::vector<int>> users;
   std::vector<int> owner;  // partition -> rank with its current rows (-1: all)
   bool local = false;      // virtual ranks in one process
+  bool use_nccl = false;   // NCCL communicators (every multi-process run; optional at world 1)
   // NCCL (multi-process)
   ncclComm_t data = nullptr, ctrl = nullptr;
   cudaStream_t ctrl_stream = nullptr;
@@ -200,7 +201,7 @@ struct RoundRunner {
     arrival_pending.assign(c->n, 0);
     for (uint32_t p = 0; p < c->n; ++p) {
       LGD_CUDA(cudaEventCreateWithFlags(&ready[p], cudaEventDisableTiming |
-                                                       (w > 1 && !local ? cudaEventInterprocess : 0)));
+                                                       (use_nccl && !local ? cudaEventInterprocess : 0)));
       LGD_CUDA(cudaEventCreateWithFlags(&arrived[p], cudaEventDisableTiming));
     }
     LGD_CUDA(cudaEventCreate(&h0));
@@ -448,8 +449,11 @@ int lgd_comm_init(lgd_context* ctx, const void* id128, uint32_t rank, uint32_t w
     ctx->wait_stores();
     ctx->runner.reset();
     auto r = std::make_unique<RoundRunner>();
+    // an id means NCCL communicators, also at world 1 (a one-rank check of the
+    // NCCL / IPC set-up); no id at world 1: a single process without NCCL
+    r->use_nccl = id128 != nullptr;
     r->setup_common(ctx, rank, world);
-    if (world > 1) r->setup_nccl(id128);
+    if (r->use_nccl) r->setup_nccl(id128);
     ctx->runner.reset(r.release());
   });
 }

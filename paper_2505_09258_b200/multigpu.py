@@ -245,7 +245,7 @@ class NativeRounds:
     def __init__(self, trainer, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self.trainer, self.rank, self.world = trainer, rank, world
         buf = None
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # world 1 with an id: one-rank NCCL communicators
             buf = C.create_string_buffer(bytes(nccl_id), 128)
         L._check(L.library().lgd_comm_init(trainer._h, buf, rank, world))
         cnt = np.zeros(1, np.uint32)

@@ -69,6 +69,29 @@ def test_train_round_world1_matches_restatement(oracle, kind):
     t.close()
 
 
+@pytest.mark.parametrize("kind", ["dot", "distmult"])
+def test_one_rank_nccl_communicators_match_local_runner(kind):
+    """lgd_comm_init with an NCCL id at world 1 builds the multi-process
+    machinery for one rank -- libnccl loaded at run time, data + control
+    communicators (ncclCommInitRank, ncclCommSplit), the IPC table / event
+    handles gathered with ncclAllGather -- and trains the same epoch of rounds
+    bit for bit as the local runner (no NCCL)."""
+    p = problem(kind)
+    got = []
+    for nccl in (True, False):
+        t = trainer(kind, p)
+        runner = mg.NativeRounds(t, 0, 1, nccl_id=mg.NativeRounds.unique_id() if nccl else None)
+        loss = 0.0
+        for r in range(runner.num_rounds):
+            res, ms, nbytes = runner.run(0, r)
+            loss += res.loss_sum
+        got.append((loss, t.tables()))
+        t.close()
+    (la, (Ea, Sa)), (lb, (Eb, Sb)) = got
+    assert la == lb
+    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_virtual_ranks_pull_partitions_between_rounds(oracle, world):
     p = problem("dot", n=7)
