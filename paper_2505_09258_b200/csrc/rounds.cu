@@ -210,7 +210,9 @@ struct RoundRunner {
     peer_state.assign(w, nullptr);
     peer_mapped.assign(w, false);
     peer_ready.assign(w, {});
-    lock_step = c->typed() && c->R && w > 1;
+    // typed models sum relation gradients per lock-step batch over NCCL (also
+    // at world 1 when the communicators exist: a one-rank all-reduce)
+    lock_step = c->typed() && c->R && (w > 1 || (use_nccl && !local));
     if (lock_step && local) throw std::invalid_argument("virtual ranks: typed models need the lock-step primitives (lgd_round_step)");
     if (lock_step) rel_buf.reserve(c->R * (c->dim + 1));
   }

@@ -69,13 +69,17 @@ def test_train_round_world1_matches_restatement(oracle, kind):
     t.close()
 
 
-@pytest.mark.parametrize("kind", ["dot", "distmult"])
+@pytest.mark.parametrize("kind", ["dot", "distmult", "complex"])
 def test_one_rank_nccl_communicators_match_local_runner(kind):
     """lgd_comm_init with an NCCL id at world 1 builds the multi-process
     machinery for one rank -- libnccl loaded at run time, data + control
     communicators (ncclCommInitRank, ncclCommSplit), the IPC table / event
-    handles gathered with ncclAllGather -- and trains the same epoch of rounds
-    bit for bit as the local runner (no NCCL)."""
+    handles gathered with ncclAllGather -- and, for typed models, runs the
+    lock-step batches with the per-batch ncclAllReduce of the relation
+    gradients.  The epoch of rounds equals the local runner's (no NCCL): bit
+    for bit for Dot, within the rounds tolerance for typed models (the
+    relation step runs as the lock-step kernel instead of the side-stream
+    pass)."""
     p = problem(kind)
     got = []
     for nccl in (True, False):
@@ -88,8 +92,13 @@ def test_one_rank_nccl_communicators_match_local_runner(kind):
         got.append((loss, t.tables()))
         t.close()
     (la, (Ea, Sa)), (lb, (Eb, Sb)) = got
-    assert la == lb
-    assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    if kind == "dot":
+        assert la == lb
+        assert np.array_equal(Ea, Eb) and np.array_equal(Sa, Sb)
+    else:
+        assert la == pytest.approx(lb, rel=1e-12)
+        assert np.mean(Ea == Eb) >= 0.99 and np.linalg.norm(Ea - Eb) <= 1e-7 * np.linalg.norm(Eb)
+        assert np.mean(Sa == Sb) >= 0.99
 
 
 @pytest.mark.parametrize("world", [2, 3])
