@@ -49,6 +49,16 @@ extern "C" {
 
 const char* lgd_last_error(void) { return g_last_error.c_str(); }
 
+// shared-negative chunks (shared.cu): 16-byte operand rows, the mix / G
+// accumulators within 128 TMEM columns, the dot-product models
+static void check_shared_mode(int model_kind, uint32_t dim, const lgd_train_options& o) {
+  if (!o.shared_chunk) return;
+  if (model_kind == LGD_MODEL_TRANSE)
+    throw std::invalid_argument("shared-negative chunks support the Dot, DistMult and ComplEx models");
+  if (dim % 4 != 0 || dim > 128)
+    throw std::invalid_argument("shared-negative chunks need a dimension that is a multiple of 4, at most 128");
+}
+
 int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_options* options,
                int device) {
   return guarded([&] {
@@ -60,6 +70,7 @@ int lgd_create(lgd_context** out, int model_kind, uint32_t dim, const lgd_train_
       throw std::invalid_argument("complex model requires an even dimension");
     if ((model_kind == LGD_MODEL_COMPLEX ? dim / 2 : dim) > 256)
       throw std::invalid_argument("embedding dimension too large (max 256, ComplEx 512)");
+    if (options) check_shared_mode(model_kind, dim, *options);
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
       throw lgd::cuda_error("no CUDA device: the B200 path has no CPU fallback");
@@ -145,6 +156,7 @@ void lgd_destroy(lgd_context* ctx) { delete ctx; }
 int lgd_set_options(lgd_context* ctx, const lgd_train_options* options) {
   return guarded([&] {
     if (!ctx || !options) throw std::invalid_argument("null argument");
+    check_shared_mode(ctx->kind, ctx->dim, *options);
     ctx->opt = *options;
   });
 }

@@ -45,6 +45,10 @@ def test_argument_validation_before_device():
         lgd.Trainer(lgd.ScoreModel("complex", 7))
     with pytest.raises(lgd.InvalidArgument):
         lgd.Trainer(lgd.ScoreModel("dot", 0))
+    # shared-negative chunks: dot-product models, dim % 4 == 0 and <= 128 (legend_b200.h)
+    for kind, d in (("transe", 64), ("distmult", 130), ("dot", 50)):
+        with pytest.raises(lgd.InvalidArgument, match="shared-negative"):
+            lgd.Trainer(lgd.ScoreModel(kind, d), lgd.TrainOptions(negatives=8, shared_chunk=64))
 
 
 def test_store_calls_reject_null_context_without_gpu():
