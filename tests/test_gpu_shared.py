@@ -151,15 +151,15 @@ def _plan_arrays(plan):
 
 
 def test_shared_mode_rejects_unsupported_shapes():
+    """TransE and dimensions off the 16-byte rows / 128 TMEM columns are
+    refused when the options are set (lgd_create, lgd_set_options)."""
     edges = np.array([[0, 0, 1], [1, 0, 2]], np.uint32)
-    t = trainer("transe", 16, 10, 2, edges, 4, 2)
-    t.init_store(1)
-    with pytest.raises(lgd.InvalidArgument):
-        t.train_batch(edges, np.array([1, 2, 3, 4], np.uint32))
-    t2 = trainer("distmult", 6, 10, 2, edges, 4, 2)  # d % 4 != 0
-    t2.init_store(1)
-    with pytest.raises(lgd.InvalidArgument):
-        t2.train_batch(edges, np.array([1, 2, 3, 4], np.uint32))
+    with pytest.raises(lgd.InvalidArgument, match="shared-negative"):
+        trainer("transe", 16, 10, 2, edges, 4, 2)
+    with pytest.raises(lgd.InvalidArgument, match="shared-negative"):
+        trainer("distmult", 6, 10, 2, edges, 4, 2)  # d % 4 != 0
+    with pytest.raises(lgd.InvalidArgument, match="shared-negative"):
+        trainer("dot", 132, 10, 0, edges, 4, 2)  # more than 128 TMEM columns
 
 
 @pytest.mark.parametrize("kind", ["dot", "distmult"])
