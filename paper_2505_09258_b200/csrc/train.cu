@@ -1064,6 +1064,35 @@ __device__ __forceinline__ void stage_item(const SegCtx& x, const Lanes<KIND, NV
   else
     L.cpa_s(op_s, x.snap + row, true);
 }
+// stage_item for the bulk-copy staging (segment_heads of TransE), lane 0
+// only: the weight as an 8-byte cp.async, and the operand row's source and
+// size for a TMA bulk copy
+template <int KIND, bool SH, bool IR1>
+__device__ __forceinline__ const void* stage_op_bulk(const SegCtx& x, uint32_t val, uint32_t w_s,
+                                                     uint32_t& bytes) {
+  const uint32_t p = val >> x.pshift;
+  const uint32_t slot = val & x.smask;
+  const uint64_t row = (uint64_t)p * x.d;
+  if (SH && slot == 1) {
+    bytes = x.d * 4;
+    return x.gneg + row;
+  }
+  if (slot - 1u < x.k || (KIND == 3 && slot == 0)) {
+    const double* w = slot == 0 ? x.w + x.cpos_off + p : x.w + (uint64_t)p * x.k + (slot - 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(w_s), "l"(w) : "memory");
+  }
+  if (slot > x.k) {
+    bytes = x.d * 8;
+    return x.mix + row;
+  }
+  if (IR1 && !SH) {
+    bytes = x.d * 8;
+    return x.ir1 + row;
+  }
+  bytes = x.d * 4;
+  return x.snap + row;
+}
+
 template <int KIND, int NV, bool SH, bool IR1>
 __device__ __forceinline__ void load_item_staged(const SegCtx& x, const Lanes<KIND, NV>& L,
                                                  uint32_t val, uint32_t op_s, uint32_t w_s,
@@ -1499,20 +1528,58 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
                         (threadIdx.x >> 5) * kDepth * sb;  // bytes
   const uint32_t ring_end = ring + kDepth * sb;
   uint32_t srest = todo;  // segments still to stage, lowest first
+  // TransE stages its rows as TMA bulk copies issued by one lane (one
+  // mbarrier per ring slot, after all warps' rings): Friendster K4 0.870 ->
+  // 0.829 ms; at the 64-register cap of the other models the variant spills
+  // (TW -17%, LJ -21%, FM -2%; profiles/r02zy, r02zz)
+  constexpr bool kBulk = KIND == 3;
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(seg_ring) +
+                                               (size_t)(kSegThreads / 32) * kDepth * sb) +
+                   (threadIdx.x >> 5) * kDepth;
+  if constexpr (kBulk) {
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) mbar_init(wbar + u, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   auto stage = [&](uint32_t slot) {
     if (srest) {
       const int h = __ffs(srest) - 1;
       srest &= srest - 1;
       const uint64_t off = (uint64_t)__shfl_sync(0xffffffffu, my_row, h) * d;
-      L.cpa_s(slot, theta + off, true);
-      L.cpa_s(slot + rowf * 4, state + off, true);
-      stage_item<KIND, NV, SH, IR1>(x, L, item(h), slot + 8 * rowf, slot + 16 * rowf, lane);
+      if constexpr (kBulk) {  // three bulk copies from lane 0, tracked by the slot's mbarrier
+        const uint32_t v = item(h);
+        if (lane == 0) {
+          const uint32_t bar = smem_addr(wbar + (slot - ring) / sb);
+          const uint32_t rb = (uint32_t)d * 4;
+          uint32_t ob;
+          const void* op = stage_op_bulk<KIND, SH, IR1>(x, v, slot + 16 * rowf, ob);
+          mbar_arrive_expect_tx(wbar + (slot - ring) / sb, 2 * rb + ob);
+          const uint32_t dst[3] = {slot, slot + rowf * 4, slot + 8 * rowf};
+          const void* src[3] = {theta + off, state + off, op};
+          const uint32_t len[3] = {rb, rb, ob};
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(dst[c]),
+                "l"(src[c]), "r"(len[c]), "r"(bar)
+                : "memory");
+        }
+      } else {
+        L.cpa_s(slot, theta + off, true);
+        L.cpa_s(slot + rowf * 4, state + off, true);
+        stage_item<KIND, NV, SH, IR1>(x, L, item(h), slot + 8 * rowf, slot + 16 * rowf, lane);
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
   for (int u = 0; u < kDepth; ++u) stage(ring + u * sb);
   uint32_t slot = ring;
+  uint32_t seg_i = 0;  // segments consumed (the slot's mbarrier phase)
 #pragma unroll 1
   while (todo) {
     const int h = __ffs(todo) - 1;
@@ -1521,6 +1588,11 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
     const uint32_t v0 = item(h);
     asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
+    if constexpr (kBulk) {
+      while (!mbar_try_wait(wbar + seg_i % kDepth, (seg_i / kDepth) & 1)) {
+      }
+      ++seg_i;
+    }
     __syncwarp();  // lane 0 staged the weight every lane reads
     float th[NE], st[NE];
     L.lds_s(slot, th);
@@ -2073,7 +2145,8 @@ void launch_vec_pass1(const BatchArgs& a, uint64_t items, unsigned grid, cudaStr
 template <int KIND, int NV, bool SH, bool IR1, bool R64>
 void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStream_t st) {
   const size_t smem =
-      (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * seg_slot_bytes((a.dim + 3) & ~3u);
+      (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * seg_slot_bytes((a.dim + 3) & ~3u) +
+      (KIND == 3 ? (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * 8 : 0);  // slot mbarriers
   static size_t attr[kMaxDevices];
   const int dev = current_device();
   if (smem > attr[dev]) {
