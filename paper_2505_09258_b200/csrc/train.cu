@@ -63,6 +63,9 @@ constexpr int kSegThreads = SEG_THREADS;
 #ifndef SEG_DEPTH
 #define SEG_DEPTH 2
 #endif
+#ifndef K4_BULK_ALL  // 1: every model's segment_heads stages by TMA bulk copies (A/B)
+#define K4_BULK_ALL 0
+#endif
 // pieces / segments whose rows are in flight per warp in K4's cp.async rings
 // (the chunked and flattened kernels; segment_heads picks its depth per model,
 // seg_heads_depth: TW DistMult measured 2 best, 0.80 ms per batch; 3: 0.81,
@@ -110,6 +113,25 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// the same on a 32-bit shared-memory address (no generic pointer kept live)
+__device__ __forceinline__ void mbar_init_s(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
@@ -1526,25 +1548,24 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
   const uint32_t sb = seg_slot_bytes(rowf);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(seg_ring) +
                         (threadIdx.x >> 5) * kDepth * sb;  // bytes
-  const uint32_t ring_end = ring + kDepth * sb;
   uint32_t srest = todo;  // segments still to stage, lowest first
   // TransE stages its rows as TMA bulk copies issued by one lane (one
   // mbarrier per ring slot, after all warps' rings): Friendster K4 0.870 ->
   // 0.829 ms; at the 64-register cap of the other models the variant spills
-  // (TW -17%, LJ -21%, FM -2%; profiles/r02zy, r02zz)
-  constexpr bool kBulk = KIND == 3;
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(seg_ring) +
-                                               (size_t)(kSegThreads / 32) * kDepth * sb) +
-                   (threadIdx.x >> 5) * kDepth;
+  // (TW -17%, LJ -21%, FM -2%; profiles/r02zy, r02zz; -DK4_BULK_ALL=1 builds that A/B)
+  constexpr bool kBulk = K4_BULK_ALL || KIND == 3;
+  const uint32_t bars = (uint32_t)__cvta_generic_to_shared(seg_ring) +
+                        (kSegThreads / 32) * kDepth * sb + (threadIdx.x >> 5) * kDepth * 8;
   if constexpr (kBulk) {
     if (lane == 0) {
 #pragma unroll
-      for (int u = 0; u < kDepth; ++u) mbar_init(wbar + u, 1);
+      for (int u = 0; u < kDepth; ++u) mbar_init_s(bars + 8 * u, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
   }
-  auto stage = [&](uint32_t slot) {
+  auto stage = [&](uint32_t u) {  // ring slot u
+    const uint32_t slot = ring + u * sb;
     if (srest) {
       const int h = __ffs(srest) - 1;
       srest &= srest - 1;
@@ -1552,11 +1573,10 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
       if constexpr (kBulk) {  // three bulk copies from lane 0, tracked by the slot's mbarrier
         const uint32_t v = item(h);
         if (lane == 0) {
-          const uint32_t bar = smem_addr(wbar + (slot - ring) / sb);
           const uint32_t rb = (uint32_t)d * 4;
           uint32_t ob;
           const void* op = stage_op_bulk<KIND, SH, IR1>(x, v, slot + 16 * rowf, ob);
-          mbar_arrive_expect_tx(wbar + (slot - ring) / sb, 2 * rb + ob);
+          mbar_expect_s(bars + 8 * u, 2 * rb + ob);
           const uint32_t dst[3] = {slot, slot + rowf * 4, slot + 8 * rowf};
           const void* src[3] = {theta + off, state + off, op};
           const uint32_t len[3] = {rb, rb, ob};
@@ -1565,7 +1585,7 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
                 "[%3];" ::"r"(dst[c]),
-                "l"(src[c]), "r"(len[c]), "r"(bar)
+                "l"(src[c]), "r"(len[c]), "r"(bars + 8 * u)
                 : "memory");
         }
       } else {
@@ -1577,9 +1597,8 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 #pragma unroll
-  for (int u = 0; u < kDepth; ++u) stage(ring + u * sb);
-  uint32_t slot = ring;
-  uint32_t seg_i = 0;  // segments consumed (the slot's mbarrier phase)
+  for (int u = 0; u < kDepth; ++u) stage(u);
+  uint32_t u = 0, ph = 0;  // the slot being consumed and its mbarrier phase
 #pragma unroll 1
   while (todo) {
     const int h = __ffs(todo) - 1;
@@ -1588,11 +1607,8 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     const uint32_t row = __shfl_sync(0xffffffffu, my_row, h);
     const uint32_t v0 = item(h);
     asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
-    if constexpr (kBulk) {
-      while (!mbar_try_wait(wbar + seg_i % kDepth, (seg_i / kDepth) & 1)) {
-      }
-      ++seg_i;
-    }
+    if constexpr (kBulk) mbar_wait_s(bars + 8 * u, ph);
+    const uint32_t slot = ring + u * sb;
     __syncwarp();  // lane 0 staged the weight every lane reads
     float th[NE], st[NE];
     L.lds_s(slot, th);
@@ -1612,8 +1628,11 @@ __global__ void __launch_bounds__(kSegThreads, seg_heads_minb<KIND>()) segment_h
     L.stf(theta + (uint64_t)row * d, th);
     L.stf(state + (uint64_t)row * d, st);
     __syncwarp();  // every lane read the weight before the slot is restaged
-    stage(slot);  // the slot just read is free again
-    slot = slot + sb == ring_end ? ring : slot + sb;
+    stage(u);  // the slot just read is free again
+    if (++u == kDepth) {
+      u = 0;
+      ph ^= 1;
+    }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -2146,7 +2165,7 @@ template <int KIND, int NV, bool SH, bool IR1, bool R64>
 void launch_segment_heads_(const BatchArgs& a, uint64_t b0, uint64_t b1, cudaStream_t st) {
   const size_t smem =
       (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * seg_slot_bytes((a.dim + 3) & ~3u) +
-      (KIND == 3 ? (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * 8 : 0);  // slot mbarriers
+      ((K4_BULK_ALL || KIND == 3) ? (size_t)(kSegThreads / 32) * seg_heads_depth<KIND>() * 8 : 0);  // slot mbarriers
   static size_t attr[kMaxDevices];
   const int dev = current_device();
   if (smem > attr[dev]) {
