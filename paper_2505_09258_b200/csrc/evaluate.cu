@@ -27,6 +27,28 @@ namespace lgd {
 namespace {
 
 constexpr int kEvalWarps = 4;
+#ifndef EVAL_BULK  // candidate rows staged by one TMA bulk copy per row (0: 16-byte cp.async pieces)
+#define EVAL_BULK 1
+#endif
+
+__device__ __forceinline__ void ev_bar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void ev_bar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ev_bar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+}
 
 __global__ void eval_candidates_kernel(uint64_t seed, uint64_t t0, uint64_t T, uint32_t ncand,
                                        uint64_t V, uint32_t* __restrict__ cand) {
@@ -50,13 +72,14 @@ __global__ void eval_candidates_kernel(uint64_t seed, uint64_t t0, uint64_t T, u
 // banks in every quarter warp
 struct EvalSmem {
   uint32_t dpad, rstride;
-  size_t ir1_off, rows_off, warp_bytes;
+  size_t ir1_off, rows_off, bars_off, warp_bytes;
   __host__ __device__ explicit EvalSmem(uint32_t d) {
     dpad = (d + 3) & ~3u;
     rstride = (dpad / 4) % 2 ? dpad : dpad + 4;
     ir1_off = 0;
     rows_off = (size_t)dpad * 8;
-    warp_bytes = rows_off + 2 * 32 * (size_t)rstride * 4;
+    bars_off = rows_off + 2 * 32 * (size_t)rstride * 4;
+    warp_bytes = bars_off + 16;  // + one mbarrier per row buffer (bulk staging)
   }
 };
 
@@ -76,6 +99,17 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
   const bool vec = (d & 3) == 0;
   const uint64_t nwarps = (uint64_t)gridDim.x * kEvalWarps;
   const uint32_t nrows = ncand + 1;  // row 0: the true destination
+  const bool bulk = EVAL_BULK && vec;
+  const uint32_t bars = (uint32_t)__cvta_generic_to_shared(wb + L.bars_off);
+  if (bulk) {
+    if (lane == 0) {
+      ev_bar_init(bars);
+      ev_bar_init(bars + 8);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  uint32_t gchunk = 0;  // chunks staged by this warp so far: buffer gchunk & 1, phase (gchunk >> 1) & 1
   for (uint64_t t = (uint64_t)blockIdx.x * kEvalWarps + warp; t < T; t += nwarps) {
     const uint32_t s = edges[3 * t], r = edges[3 * t + 1], dd = edges[3 * t + 2];
     const uint32_t* my = cand + t * ncand;
@@ -100,10 +134,24 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
     }
     auto row_id = [&](uint32_t q) { return q == 0 ? dd : my[q - 1]; };
     // stage rows [32 c, 32 c + 32) into buffer c & 1 (zero rows past the end)
+    const uint32_t g0 = gchunk;  // this edge's chunk c is the warp's chunk g0 + c
     auto stage = [&](uint32_t c) {
-      float* buf = rows + (c & 1) * 32 * rs;
+      const uint32_t gb = (g0 + c) & 1;
+      float* buf = rows + gb * 32 * rs;
       const uint32_t q0 = 32 * c;
       const uint32_t my_id = q0 + lane < nrows ? row_id(q0 + lane) : 0;
+      if (bulk) {  // lane q copies row q: one bulk copy per row, counted on the buffer's mbarrier
+        const uint32_t n = nrows - q0 < 32 ? nrows - q0 : 32;
+        if (lane == 0) ev_bar_expect(bars + 8 * gb, n * d * 4);
+        __syncwarp();
+        if (lane < (int)n)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+              "[%3];" ::"r"((uint32_t)__cvta_generic_to_shared(buf + lane * rs)),
+              "l"(theta + (size_t)my_id * d), "r"(d * 4), "r"(bars + 8 * gb)
+              : "memory");
+        return;
+      }
       for (int q = 0; q < 32; ++q) {
         const uint32_t id = __shfl_sync(0xffffffffu, my_id, q);
         if (q0 + q >= nrows) break;
@@ -130,7 +178,10 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
     double truth = 0.0;
     uint32_t beaten = 0;
     for (uint32_t c = 0; c < nchunks; ++c) {
-      if (c + 1 < nchunks) {
+      if (bulk) {
+        if (c + 1 < nchunks) stage(c + 1);
+        ev_bar_wait(bars + 8 * ((g0 + c) & 1), ((g0 + c) >> 1) & 1);
+      } else if (c + 1 < nchunks) {
         stage(c + 1);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
@@ -138,7 +189,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
       }
       __syncwarp();
       const uint32_t q = 32 * c + lane;
-      const float* row = rows + (c & 1) * 32 * rs + lane * rs;
+      const float* row = rows + ((g0 + c) & 1) * 32 * rs + lane * rs;
       double f = 0.0;
       if (q < nrows) {
         if (KIND == 3) {  // -||u - t||, squares summed sequentially
@@ -180,6 +231,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_score_kernel(
       beaten += __popc(__ballot_sync(0xffffffffu, b));
       __syncwarp();  // the buffer is restaged by the next iteration's stage(c + 2)
     }
+    gchunk = g0 + nchunks;
     if (lane == 0) {
       const uint64_t rank = 1ull + beaten;
       rr[t] = 1.0 / (double)rank;
