@@ -1787,6 +1787,9 @@ __global__ void __launch_bounds__(kSegThreads, SEG_MINB) segment_flat(
 #ifndef WS_PRODUCERS
 #define WS_PRODUCERS 4
 #endif
+#ifndef WS_BULK  // 1: producers stage a segment with three TMA bulk copies from one lane
+#define WS_BULK 1
+#endif
 constexpr int kWsProducers = WS_PRODUCERS;
 constexpr int kWsConsumers = 8;
 constexpr int kWsDepth = 3;
@@ -1829,7 +1832,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) segment_ws(
   const uint32_t slots = (uint32_t)__cvta_generic_to_shared(ws_smem) + ws_bar_bytes();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kWsConsumers * kWsDepth; ++i) {
-      mbar_init(full + i, 33);  // 32 producer lanes' copies + the metadata arrive
+      // bulk staging: lane 0's expect-tx arrive + its cp.async (weight) arrive;
+      // else 32 producer lanes' copies + the metadata arrive
+      mbar_init(full + i, WS_BULK ? 2 : 33);
       mbar_init(empty + i, 1);  // the consumer's release
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1895,16 +1900,40 @@ __global__ void __launch_bounds__(kWsThreads, 2) segment_ws(
         uint32_t sa, par;
         const int s = claim(c, sa, par);
         const uint64_t off = (uint64_t)row * d;
-        L.cpa_s(sa, a.theta + off, true);
-        L.cpa_s(sa + 4 * rowf, a.state + off, true);
-        stage_item<KIND, NV, SH, IR1>(x, L, val, sa + 8 * rowf, sa + 16 * rowf, lane);
-        if (lane == 0) {
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16 * rowf + 16),
-                       "r"(row), "r"(len), "r"((uint32_t)(base + h)), "r"(val)
-                       : "memory");
-          mbar_arrive(full + c * kWsDepth + s);
+        if (WS_BULK) {  // lane 0: three TMA bulk copies on the slot's full barrier
+          if (lane == 0) {
+            const uint32_t fb = smem_addr(full + c * kWsDepth + s);
+            const uint32_t rb = (uint32_t)d * 4;
+            uint32_t ob;
+            const void* op = stage_op_bulk<KIND, SH, IR1>(x, val, sa + 16 * rowf, ob);
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16 * rowf + 16),
+                         "r"(row), "r"(len), "r"((uint32_t)(base + h)), "r"(val)
+                         : "memory");
+            mbar_expect_s(fb, 2 * rb + ob);
+            const uint32_t dst[3] = {sa, sa + 4 * rowf, sa + 8 * rowf};
+            const void* src[3] = {a.theta + off, a.state + off, op};
+            const uint32_t len3[3] = {rb, rb, ob};
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                  "%2, [%3];" ::"r"(dst[q]),
+                  "l"(src[q]), "r"(len3[q]), "r"(fb)
+                  : "memory");
+            mbar_arrive_cpasync(full + c * kWsDepth + s);  // the weight's cp.async
+          }
+        } else {
+          L.cpa_s(sa, a.theta + off, true);
+          L.cpa_s(sa + 4 * rowf, a.state + off, true);
+          stage_item<KIND, NV, SH, IR1>(x, L, val, sa + 8 * rowf, sa + 16 * rowf, lane);
+          if (lane == 0) {
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + 16 * rowf + 16),
+                         "r"(row), "r"(len), "r"((uint32_t)(base + h)), "r"(val)
+                         : "memory");
+            mbar_arrive(full + c * kWsDepth + s);
+          }
+          mbar_arrive_cpasync(full + c * kWsDepth + s);
         }
-        mbar_arrive_cpasync(full + c * kWsDepth + s);
       }
     }
     for (int t = 0; t < kWsPer; ++t) {  // end of work: a zero-length slot per consumer
@@ -1916,8 +1945,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) segment_ws(
                      "r"(0u), "r"(0u), "r"(0u), "r"(0u)
                      : "memory");
         mbar_arrive(full + c * kWsDepth + s);
+        if (WS_BULK) mbar_arrive_cpasync(full + c * kWsDepth + s);
       }
-      mbar_arrive_cpasync(full + c * kWsDepth + s);
+      if (!WS_BULK) mbar_arrive_cpasync(full + c * kWsDepth + s);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
