@@ -453,17 +453,6 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t dtmem, uint32_t atmem, uint
       "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// a [128 x dpad] K-major core-matrix tile in shared memory -> TMEM columns
-// [tcol, tcol + dpad), lane = row (one 128 x 8 slice per tcgen05.cp; ordered
-// before the MMAs this thread issues next)
-__device__ __forceinline__ void tile_to_tmem(uint32_t tcol, uint32_t a0, uint32_t dp) {
-  const uint32_t kcore = (dp / 4) * 128;
-  for (uint32_t ks = 0; ks < dp / 8; ++ks)
-    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tcol + ks * 8),
-                 "l"(smem_desc(a0 + ks * 256, 128, kcore))
-                 : "memory");
-}
-
 // 2^x, flush-to-zero approximation (one MUFU op; 2^-inf = +0)
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -475,21 +464,6 @@ __device__ __forceinline__ float tf32_pos(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 constexpr float kLog2e = 1.4426950408889634f;
-// softmax weights of 32 scores, branch-free: w = 2^(s log2e - c) with the
-// row's c = M log2e + log2 Z (= 2^(s log2e - M log2e) / Z, one MUFU op and no
-// multiply), zero where !keep (bit c of keep)
-__device__ __forceinline__ void weights32(const float* v, float rc, uint32_t keep, float* w) {
-  if (keep == 0xffffffffu) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) w[c] = tf32_pos(ex2(__fmaf_rn(v[c], kLog2e, -rc)));
-  } else {
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const float e = ex2(__fmaf_rn(v[c], kLog2e, -rc));
-      w[c] = (keep >> c) & 1u ? tf32_pos(e) : 0.f;
-    }
-  }
-}
 __device__ __forceinline__ uint32_t keep_mask(uint32_t j0, uint32_t limit) {
   // bit c set iff j0 + c < limit
   if (j0 >= limit) return 0u;
@@ -497,16 +471,8 @@ __device__ __forceinline__ uint32_t keep_mask(uint32_t j0, uint32_t limit) {
   return n >= 32 ? 0xffffffffu : (1u << n) - 1u;
 }
 
-// S = A . B^T over K = dpad into TMEM columns dcol (N = n columns); A in
-// TMEM at acol, B K-major in shared memory
-__device__ __forceinline__ void mma_scores(uint32_t dcol, uint32_t acol, uint32_t b0, uint32_t dp,
-                                           uint32_t n) {
-  const uint32_t kcore = (dp / 4) * 128;
-  const uint32_t id = instr_desc(128, n, false, false);
-  for (uint32_t ks = 0; ks < dp / 8; ++ks)
-    mma_tf32_ts(dcol, acol + ks * 8, smem_desc(b0 + ks * 256, 128, kcore), id, ks > 0);
-}
-// the same with A in shared memory (K-major core-matrix tile at a0)
+// S = A . B^T over K = dpad into TMEM columns dcol (N = n columns), A and B
+// K-major core-matrix tiles in shared memory
 __device__ __forceinline__ void mma_scores_ss(uint32_t dcol, uint32_t a0, uint32_t b0, uint32_t dp,
                                               uint32_t n) {
   const uint32_t kcore = (dp / 4) * 128;
@@ -515,7 +481,7 @@ __device__ __forceinline__ void mma_scores_ss(uint32_t dcol, uint32_t a0, uint32
     mma_tf32(dcol, smem_desc(a0 + ks * 256, 128, kcore), smem_desc(b0 + ks * 256, 128, kcore), id,
              ks > 0);
 }
-// barrier setup shared by the three kernels
+// barrier setup shared by the tensor-core kernels
 __device__ __forceinline__ void sg_setup(uint32_t* tbase_s, uint32_t tcols, uint64_t* bars,
                                          int nbars, const uint32_t* counts) {
   const int warp = threadIdx.x >> 5;
