@@ -313,21 +313,28 @@ __global__ void __launch_bounds__(256) shared_gather_kernel(BatchArgs a) {
     if (mv) myid = a.negs[mc * k + mj];
   }
   const uint32_t vmask = __ballot_sync(0xffffffffu, mv);
+  // the warp's rows by TMA bulk copies (lane i < 8 copies row i; random rows
+  // gathered per lane are load-path bound), then TF32 rounding in place
+  __shared__ uint64_t gbar[8];
+  if (lane == 0) {
+    bar_init(gbar + warp, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bar_expect(gbar + warp, __popc(vmask) * d * 4);
+  }
+  __syncwarp();
+  if (mv) bulk_load(ptile + (warp * 8 + lane) * ts, a.theta + (size_t)myid * d, d * 4, gbar + warp);
+#pragma unroll 4
+  for (int i = 0; i < 8; ++i) {  // zero the padded slots and the columns past d
+    float* trow = ptile + (warp * 8 + i) * ts;
+    for (uint32_t e = ((vmask >> i) & 1u ? d : 0u) + lane; e < dp; e += 32) trow[e] = 0.f;
+  }
+  bar_wait(gbar + warp, 0);
 #pragma unroll 4
   for (int i = 0; i < 8; ++i) {
-    float* trow = ptile + (warp * 8 + i) * ts;
-    if (!((vmask >> i) & 1u)) {
-      for (uint32_t e = lane; e < dp; e += 32) trow[e] = 0.f;
-      continue;
-    }
-    const uint32_t id = __shfl_sync(0xffffffffu, myid, i);
-    const float* row = a.theta + (size_t)id * d;
-    if (4 * (uint32_t)lane < d) {
-      const float4 v = *reinterpret_cast<const float4*>(row + 4 * lane);
-      *reinterpret_cast<float4*>(trow + 4 * lane) =
-          make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-    }
-    for (uint32_t e = d + lane; e < dp; e += 32) trow[e] = 0.f;
+    if (!((vmask >> i) & 1u) || 4 * (uint32_t)lane >= d) continue;
+    float4* t4 = reinterpret_cast<float4*>(ptile + (warp * 8 + i) * ts + 4 * lane);
+    const float4 v = *t4;
+    *t4 = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
   }
   if (lane < 8 && mv) {
     const uint64_t item = 2 * a.P + mc * k + mj;
